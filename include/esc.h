@@ -1,0 +1,230 @@
+/*
+ * esc.h — C ABI of the B200-native exact-selectivity-computation (ESC) hot path.
+ *
+ * The reference (`escdb`, /root/reference/pkg/src/escdb) is pure Python + numpy and has no
+ * FFI layer; its drop-in boundary is a set of Python function signatures.  Each entry point
+ * below replaces the numpy body of one of them (file:line in the reference):
+ *
+ *   esc_scan_count   executor.count_star            executor.py:218-224  (+ _eval_mask :180-199,
+ *                    _eval_atom :149-177, _eval_fncall :128-146, _text_lut/_apply_lut :73-94)
+ *                    reached through optimizer.compute_exact_selectivity optimizer.py:152-168
+ *                    and executor.execute_count executor.py:232-250
+ *   esc_compact      executor.eval_predicate        executor.py:202-215  (row ids, ascending)
+ *                    optimizer.materialize_pushdown  optimizer.py:180-194 (eval + Column.take
+ *                    storage.py:176-184 of every needed column, fused into one pass)
+ *   esc_gather       storage.Column.take             storage.py:176-184
+ *
+ * All pointers in esc_column_t / output arrays are DEVICE pointers (or host-mapped pinned
+ * memory for `result`).  No entry point allocates or frees caller memory; scratch lives in a
+ * caller-provided workspace (esc_workspace_bytes / esc_workspace_init).  Every entry point is
+ * asynchronous on `stream` (a cudaStream_t passed as void*) and returns ESC_OK or an error
+ * code; esc_last_error() returns a thread-local message for the last failure.
+ *
+ * Semantics (bit-exact with the reference):
+ *   - every atom is false when any operand is NULL; AND/OR/NOT are two-valued above that;
+ *   - comparisons happen in the numpy (NEP 50) promotion domain chosen by the host compiler
+ *     (int64 exact / float32 / float64), carried in esc_instr_t.domain;
+ *   - UDF programs evaluate CPython float semantics (no FMA contraction, floored %, //);
+ *   - row order of every compaction output is ascending logical row order.
+ */
+#ifndef ESC_H_
+#define ESC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESC_ABI_VERSION 1
+
+#define ESC_MAX_COLS 32     /* column slots one program may reference            */
+#define ESC_MAX_INSTRS 96   /* boolean program length                              */
+#define ESC_MAX_UDFS 8      /* UDF atoms per program                               */
+#define ESC_MAX_UDF_OPS 128 /* total UDF arithmetic ops per program                */
+#define ESC_MAX_UDF_ARGS 8  /* arguments per UDF                                   */
+#define ESC_MAX_STACK 16    /* nesting depth of the boolean program                */
+#define ESC_MAX_PROJ 32     /* projected columns one compaction may emit           */
+
+/* status codes */
+enum {
+  ESC_OK = 0,
+  ESC_ERR_INVALID = 1,   /* malformed program / arguments                     */
+  ESC_ERR_CUDA = 2,      /* CUDA runtime error (message has the CUDA string)    */
+  ESC_ERR_WORKSPACE = 3, /* workspace too small / misaligned                    */
+  ESC_ERR_UNSUPPORTED = 4
+};
+
+/* physical storage types of a column (native widths, little endian) */
+enum {
+  ESC_I8 = 0, ESC_I16 = 1, ESC_I32 = 2, ESC_I64 = 3,
+  ESC_F32 = 4, ESC_F64 = 5, ESC_U8 = 6, ESC_U16 = 7, ESC_U32 = 8
+};
+
+/* boolean-program opcodes */
+enum {
+  ESC_OP_CMP = 1,     /* col_a <cmp> k0                 (Equality / Comparison)       */
+  ESC_OP_RANGE = 2,   /* k0 <= col_a <= k1 (inclusive)  (Range)                       */
+  ESC_OP_LUT = 3,     /* bit lut[aux + code(col_a)]      (TEXT range/ordering)         */
+  ESC_OP_COLCMP = 4,  /* col_a <cmp> col_b              (ColumnCompare)               */
+  ESC_OP_NOTNULL = 5, /* ~null(col_a)                   (FoldedAtom(True))            */
+  ESC_OP_FALSE = 6,   /* all false                      (FoldedAtom(False))           */
+  ESC_OP_UDF = 7,     /* udf[aux](args) <cmp> k0.f      (FnCall)                      */
+  ESC_OP_PUSH = 8,    /* open a nested group combined into the outer result by `combine` */
+  ESC_OP_POP = 9,     /* close the group: acc = saved <combine> acc                     */
+  ESC_OP_NOT = 10     /* acc = ~acc (two-valued NOT)                                   */
+};
+
+/* how an atom / group result merges into the running accumulator */
+enum { ESC_COMB_SET = 0, ESC_COMB_AND = 1, ESC_COMB_OR = 2 };
+
+/* comparison operators */
+enum { ESC_CMP_EQ = 0, ESC_CMP_NE = 1, ESC_CMP_LT = 2, ESC_CMP_LE = 3, ESC_CMP_GT = 4, ESC_CMP_GE = 5 };
+
+/* comparison domains (numpy NEP 50 promotion of column dtype with the constant) */
+enum { ESC_DOM_I64 = 0, ESC_DOM_F32 = 1, ESC_DOM_F64 = 2 };
+
+/* UDF opcodes (postfix, float64 stack; CPython float semantics) */
+enum {
+  ESC_UDF_ARG = 1,      /* push float64(arg[a]) (DECIMAL: / divisor[a])  */
+  ESC_UDF_CONST = 2,    /* push k                                        */
+  ESC_UDF_ADD = 3, ESC_UDF_SUB = 4, ESC_UDF_MUL = 5,
+  ESC_UDF_DIV = 6,      /* ZeroDivisionError on /0                      */
+  ESC_UDF_MOD = 7,      /* CPython float_rem (floored), error on %0     */
+  ESC_UDF_FLOORDIV = 8, /* CPython float_floor_div, error on //0        */
+  ESC_UDF_NEG = 9, ESC_UDF_ABS = 10,
+  ESC_UDF_SQUARE = 11   /* x ** 2 (OverflowError when finite x overflows) */
+};
+
+/* UDF failure codes (low 3 bits of esc_result_t.udf_fail[]) */
+enum { ESC_FAIL_DIV = 1, ESC_FAIL_MOD = 2, ESC_FAIL_FLOORDIV = 3, ESC_FAIL_POW = 4 };
+
+typedef union {
+  int64_t i;
+  double f;
+} esc_const_t;
+
+typedef struct {
+  uint8_t op;      /* ESC_OP_*                                      */
+  uint8_t combine; /* ESC_COMB_*                                    */
+  uint8_t cmp;     /* ESC_CMP_*                                     */
+  uint8_t domain;  /* ESC_DOM_*                                     */
+  uint8_t col_a;   /* column slot                                   */
+  uint8_t col_b;   /* second column slot (COLCMP)                   */
+  uint8_t neg;     /* invert the atom result before combining       */
+  uint8_t pad0;
+  uint32_t aux;    /* LUT word offset (LUT) / UDF index (UDF)      */
+  uint32_t aux2;   /* LUT size in codes (LUT)                       */
+  esc_const_t k0;
+  esc_const_t k1;
+} esc_instr_t; /* 32 bytes */
+
+typedef struct {
+  uint8_t op;  /* ESC_UDF_* */
+  uint8_t arg; /* argument index for ESC_UDF_ARG */
+  uint8_t pad[6];
+  double k;    /* constant for ESC_UDF_CONST */
+} esc_udf_op_t; /* 16 bytes */
+
+typedef struct {
+  uint16_t first_op; /* index into udf_ops                               */
+  uint8_t n_ops;
+  uint8_t n_args;
+  uint8_t dense;     /* 1: evaluate on every row to detect failures      */
+  uint8_t pad[3];
+  uint8_t arg_col[ESC_MAX_UDF_ARGS];  /* column slot per argument          */
+  double arg_div[ESC_MAX_UDF_ARGS];   /* DECIMAL descale divisor, 0 = none */
+} esc_udf_t;
+
+/* A compiled predicate (host memory; passed to the kernel by value). */
+typedef struct {
+  uint32_t abi_version;
+  uint16_t n_instrs;
+  uint16_t n_udfs;
+  uint16_t n_udf_ops;
+  uint16_t max_depth;
+  uint32_t lut_words;            /* 32-bit words at `lut` (device memory)  */
+  const uint32_t* lut;           /* device pointer to concatenated LUT bitmaps, may be NULL */
+  esc_instr_t instrs[ESC_MAX_INSTRS];
+  esc_udf_t udfs[ESC_MAX_UDFS];
+  esc_udf_op_t udf_ops[ESC_MAX_UDF_OPS];
+} esc_program_t;
+
+/* One column slot: device buffers at native width. */
+typedef struct {
+  const void* data;     /* device pointer, `nrows` values of `dtype`                  */
+  const uint8_t* nulls; /* device pointer to a bool mask (1 = NULL), or NULL if none  */
+  int32_t dtype;        /* ESC_I8 ...                                                 */
+  int32_t flags;        /* ESC_COL_* hints                                            */
+} esc_column_t;
+
+/* esc_column_t.flags: stage this column through shared memory even when the program does not
+ * reference it (a projection-only column of a dense compaction: reading it whole by TMA beats
+ * sector-granular gathers once most sectors hold a hit). */
+#define ESC_COL_STAGE 1
+
+/* Result block written by the last CTA of a launch (device or host-mapped pinned memory). */
+typedef struct {
+  uint64_t count;                  /* exact qualifying rows                               */
+  uint64_t udf_fail[ESC_MAX_UDFS]; /* (first failing logical row << 3 | code), ~0 = none  */
+} esc_result_t;
+
+/* Output of a compaction: one destination per projected slot. */
+typedef struct {
+  int32_t n_proj;
+  int32_t pad;
+  int32_t slot[ESC_MAX_PROJ];          /* column slot of each projected column        */
+  void* out_values[ESC_MAX_PROJ];      /* device buffers, `capacity` values each      */
+  uint8_t* out_nulls[ESC_MAX_PROJ];    /* device bool buffers or NULL                 */
+  int64_t* out_row_ids;                /* optional: physical row id of every hit      */
+  int64_t capacity;                    /* rows beyond capacity are counted, not written */
+} esc_outputs_t;
+
+/* ---- workspace ------------------------------------------------------------------------ */
+
+/* Bytes of workspace a launch over `nrows` rows needs (tile status words + counters). */
+size_t esc_workspace_bytes(int64_t nrows);
+
+/* One-time initialisation of a workspace (async memset on `stream`). Launches leave the
+ * workspace clean again, so this is only needed after allocation or after a failed launch. */
+int esc_workspace_init(void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- hot path --------------------------------------------------------------------------- */
+
+/* Exact count of rows satisfying `prog` over logical rows [0, nrows).
+ * replaces executor.count_star (executor.py:218-224).
+ * d_row_ids: optional device int64 array; logical row i reads physical row d_row_ids[i]
+ * (RowSelection chaining, executor.py:211-215).  Writes `result` on completion. */
+int esc_scan_count(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols,
+                   int64_t nrows, const int64_t* d_row_ids, esc_result_t* result,
+                   void* d_ws, size_t ws_bytes, void* stream);
+
+/* Fused predicate + exact count + order-preserving compaction of the projected columns
+ * (single pass, decoupled look-back).  replaces executor.eval_predicate (executor.py:202-215)
+ * and optimizer.materialize_pushdown (optimizer.py:180-194). */
+int esc_compact(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols,
+                int64_t nrows, const int64_t* d_row_ids, const esc_outputs_t* outs,
+                esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream);
+
+/* out[i] = col[idx[i]] (values and, when present, nulls).  replaces Column.take
+ * (storage.py:176-184). */
+int esc_gather(const esc_column_t* col, const int64_t* d_idx, int64_t n, void* out_values,
+               uint8_t* out_nulls, void* stream);
+
+/* ---- misc ------------------------------------------------------------------------------- */
+
+const char* esc_last_error(void);
+int esc_abi_version(void);
+/* Number of SMs of the current device (0 when no device). */
+int esc_device_sm_count(void);
+/* sizeof() of the ABI structs, for binding checks: 0 program, 1 instr, 2 udf, 3 udf_op,
+ * 4 column, 5 result, 6 outputs; -1 for an unknown id. */
+int esc_struct_size(int which);
+/* Tile geometry the kernels use for a program over these columns (for roofline accounting). */
+int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESC_H_ */

@@ -1,0 +1,257 @@
+"""CPU ORACLE for the ESC hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline / ``--impl
+reference`` legs may import this module, and only as the checker or as the timed reference CPU
+implementation.  The product package never imports it (there is no CPU fallback).
+
+This is a numpy restatement of the reference's algorithm for the selectivity sub-query
+(``/root/reference/pkg/src/escdb``, Python 3.12 + numpy 2.3).  Each function cites the reference
+lines it follows.  It works on plain numpy columns and on predicates in the JSON form below, so
+it shares no code with the product.  It is PINNED against golden vectors produced by running the
+reference itself (``tests/golden/make_golden.py``; checked by ``tests/test_oracle_golden.py``).
+
+Predicate JSON (one list per node)::
+
+    ["eq", ref, v]            Equality            ["cmp", ref, op, v]     Comparison
+    ["range", ref, lo, hi]    Range (inclusive)   ["colcmp", ref, op, ref] ColumnCompare
+    ["fn", name, [ref...], op, v]  FnCall         ["folded", ref, bool]    FoldedAtom
+    ["and", [...]]  ["or", [...]]  ["not", x]
+    ref = [column_name, decimal_scale_or_null]
+
+Values are ints, floats (``{"float": "nan"|"inf"|"-inf"}`` for non-finite) or strings.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+class OracleExecutionError(Exception):
+    """Stands for the reference's ExecutionError (same message text)."""
+
+
+@dataclass
+class OColumn:
+    values: np.ndarray
+    nulls: np.ndarray            # bool, True = NULL (reference Column.null_mask)
+    kind: str = "INT64"
+    scale: int = 0
+    words: list | None = None    # dictionary strings (TEXT)
+
+
+@dataclass
+class OTable:
+    name: str
+    columns: dict = field(default_factory=dict)  # name -> OColumn (insertion = base order)
+
+    @property
+    def row_count(self) -> int:
+        return len(next(iter(self.columns.values())).values)
+
+
+def decode_value(v):
+    if isinstance(v, dict) and "float" in v:
+        return float(v["float"])
+    return v
+
+
+_OPS = {
+    "=": np.equal, "<>": np.not_equal, "<": np.less, "<=": np.less_equal,
+    ">": np.greater, ">=": np.greater_equal,
+}
+
+
+def _compare(values, op, const):
+    """executor.py:97-110 — numpy comparison (NEP 50 promotion applies)."""
+    if op not in _OPS:
+        raise OracleExecutionError(f"unknown comparison operator {op!r}")
+    return _OPS[op](values, const)
+
+
+def _text_lut(col: OColumn, op: str, value: str) -> np.ndarray:
+    """executor.py:73-87 — bool LUT over the dictionary's decoded strings."""
+    strings = np.asarray(col.words or [], dtype=object)
+    if strings.size == 0:
+        return np.zeros(0, dtype=bool)
+    if op in ("<", "<=", ">", ">="):
+        return np.asarray(_OPS[op](strings, value), dtype=bool)
+    raise OracleExecutionError(f"unsupported TEXT comparison operator {op!r}")
+
+
+def _apply_lut(lut, codes, nulls):
+    """executor.py:90-94."""
+    if lut.size == 0:
+        return np.zeros(codes.shape, dtype=bool)
+    safe = np.where(nulls, 0, codes)
+    return lut[safe] & ~nulls
+
+
+class _Slices:
+    """executor.py:47-70 — lazily gathered (values, nulls) per column."""
+
+    def __init__(self, table: OTable, rows):
+        self.table, self.rows, self.cache = table, rows, {}
+
+    def get(self, name):
+        if name not in self.cache:
+            c = self.table.columns[name]
+            if self.rows is None:
+                self.cache[name] = (c.values, c.nulls)
+            else:
+                self.cache[name] = (c.values[self.rows], c.nulls[self.rows])
+        return self.cache[name]
+
+    @property
+    def size(self):
+        return self.table.row_count if self.rows is None else int(self.rows.size)
+
+
+def _udf(node, slices: _Slices, udfs: dict):
+    """executor.py:113-146 — float64 args (DECIMAL / 10**s), np.frompyfunc, error -> first row."""
+    _, name, refs, op, value = node
+    fn = udfs.get(name)
+    if fn is None:
+        raise OracleExecutionError(f"function {name!r} has no bound implementation")
+    arrays = []
+    any_null = np.zeros(slices.size, dtype=bool)
+    for cname, scale in refs:
+        vals, nulls = slices.get(cname)
+        out = vals.astype(np.float64)
+        if scale:
+            out = out / float(10**scale)
+        arrays.append(out)
+        any_null |= nulls
+    try:
+        raw = np.frompyfunc(fn, len(arrays), 1)(*arrays)
+    except Exception as exc:  # noqa: BLE001 - mirror of the reference's catch-all
+        for i in range(slices.size):
+            try:
+                fn(*(float(a[i]) for a in arrays))
+            except Exception:  # noqa: BLE001
+                raise OracleExecutionError(f"UDF {name!r} failed at row {i}: {exc}") from exc
+        raise OracleExecutionError(f"UDF {name!r} failed: {exc}") from exc
+    results = raw.astype(np.float64) if raw.size else np.zeros(0, dtype=np.float64)
+    return _compare(results, op, decode_value(value)) & ~any_null
+
+
+def _atom(node, slices: _Slices, udfs: dict):
+    """executor.py:149-177."""
+    tag = node[0]
+    if tag == "eq":
+        vals, nulls = slices.get(node[1][0])
+        return (vals == decode_value(node[2])) & ~nulls
+    if tag == "cmp":
+        vals, nulls = slices.get(node[1][0])
+        v = decode_value(node[3])
+        if isinstance(v, str):
+            return _apply_lut(_text_lut(slices.table.columns[node[1][0]], node[2], v), vals, nulls)
+        return _compare(vals, node[2], v) & ~nulls
+    if tag == "range":
+        vals, nulls = slices.get(node[1][0])
+        lo, hi = decode_value(node[2]), decode_value(node[3])
+        if isinstance(lo, str):
+            col = slices.table.columns[node[1][0]]
+            return _apply_lut(_text_lut(col, ">=", lo) & _text_lut(col, "<=", hi), vals, nulls)
+        return (vals >= lo) & (vals <= hi) & ~nulls
+    if tag == "colcmp":
+        lv, ln = slices.get(node[1][0])
+        rv, rn = slices.get(node[3][0])
+        return _compare(lv, node[2], rv) & ~ln & ~rn
+    if tag == "fn":
+        return _udf(node, slices, udfs)
+    if tag == "folded":
+        _, nulls = slices.get(node[1][0])
+        return ~nulls if node[2] else np.zeros(slices.size, dtype=bool)
+    raise OracleExecutionError(f"unknown atom {node!r}")
+
+
+def eval_mask(node, slices: _Slices, udfs: dict):
+    """executor.py:180-199 — whole-slice short circuit; two-valued NOT."""
+    tag = node[0]
+    if tag == "and":
+        items = node[1]
+        mask = eval_mask(items[0], slices, udfs)
+        for item in items[1:]:
+            if not mask.any():
+                break
+            mask = mask & eval_mask(item, slices, udfs)
+        return mask
+    if tag == "or":
+        items = node[1]
+        mask = eval_mask(items[0], slices, udfs)
+        for item in items[1:]:
+            if mask.all():
+                break
+            mask = mask | eval_mask(item, slices, udfs)
+        return mask
+    if tag == "not":
+        return ~eval_mask(node[1], slices, udfs)
+    return _atom(node, slices, udfs)
+
+
+def count_star(table: OTable, pred, udfs=None) -> int:
+    """executor.py:218-224."""
+    if pred is None:
+        return table.row_count
+    return int(np.count_nonzero(eval_mask(pred, _Slices(table, None), udfs or {})))
+
+
+def eval_predicate(table: OTable, pred, rows=None, udfs=None) -> np.ndarray:
+    """executor.py:202-215 — ascending int64 row ids (``rows``: a prior selection)."""
+    if pred is None:
+        return np.arange(table.row_count, dtype=np.int64) if rows is None else rows
+    mask = eval_mask(pred, _Slices(table, rows), udfs or {})
+    if rows is None:
+        return np.flatnonzero(mask).astype(np.int64)
+    return rows[mask]
+
+
+def take(col: OColumn, idx) -> OColumn:
+    """storage.py:176-184."""
+    return OColumn(col.values[idx], col.nulls[idx], col.kind, col.scale, col.words)
+
+
+def materialize(table: OTable, pred, needed, udfs=None) -> dict:
+    """optimizer.py:189-193 — re-evaluate, gather the needed columns in the given order."""
+    rows = eval_predicate(table, pred, None, udfs)
+    return {name: take(table.columns[name], rows) for name in needed}
+
+
+# -------------------------------------------------------------------------------------------
+# planner policy and ordering (exact, host logic)
+# -------------------------------------------------------------------------------------------
+def decide_pushdown(row_count: int, count: int, min_table_size=1000, max_selectivity=0.2) -> bool:
+    """optimizer.py:171-177 — inclusive thresholds, exact rational comparison."""
+    from fractions import Fraction
+
+    if row_count < min_table_size or row_count <= 0:
+        return False
+    return Fraction(count, row_count) <= max_selectivity
+
+
+def order_builds(aliases, edges, probe, effective) -> list:
+    """optimizer.py:208-228 — greedy smallest adjacent effective cardinality, ties by alias.
+    ``edges`` = [(alias_a, alias_b), ...]."""
+    connected, remaining, order = {probe}, [a for a in aliases if a != probe], []
+    while remaining:
+        cands = [a for a in remaining
+                 if any((a == x and y in connected) or (a == y and x in connected) for x, y in edges)]
+        if not cands:
+            raise OracleExecutionError("cartesian product required")
+        pick = min(cands, key=lambda a: (effective[a], a))
+        order.append(pick)
+        connected.add(pick)
+        remaining.remove(pick)
+    return order
+
+
+def py_mod(x: float, y: float) -> float:
+    """CPython float ``%`` (what the reference's UDFs compute); used by tests."""
+    return x % y
+
+
+def is_finite(x) -> bool:
+    return isinstance(x, (int, float)) and math.isfinite(x)

@@ -1,0 +1,286 @@
+"""Predicate evaluation on the GPU: exact counts, row selections, fused materialization.
+
+Drop-in for the hot half of ``escdb.executor`` (reference ``pkg/src/escdb/executor.py:23-250``):
+
+=====================  =============================================  ==========================
+function               reference                                      device path
+=====================  =============================================  ==========================
+``count_star``         ``executor.py:218-224``                        K1 ``esc_scan_count``
+``eval_predicate``     ``executor.py:202-215``                        K1 (size) + K2 row ids
+``execute_count``      ``executor.py:232-250``                        host shim -> ``count_star``
+``materialize``        ``optimizer.py:191-192`` (eval + take)         K2 ``esc_compact`` (1 pass)
+``take_column``        ``storage.py:176-184``                         ``esc_gather``
+=====================  =============================================  ==========================
+
+UDF failures keep the reference's observable behaviour: the reference evaluates a UDF on every
+row of the slice whenever the UDF is *reached* by its whole-slice short circuit
+(``executor.py:183-196``: an AND stops once its running mask has no true row, an OR once it has
+no false row) and reports ``ExecutionError("UDF 'f' failed at row i: <python message>")`` for
+the first failing row (``executor.py:133-144``).  A UDF that can fail is evaluated densely by the
+kernel, which records its first failing row; the host then replays the short-circuit decisions
+with exact device counts of the sibling prefixes and raises exactly when the reference would.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from . import expr as ex
+from .compiler import CompiledPredicate, compile_predicate
+from .errors import ExecutionError
+from .ra import RaAggregate, RaProject, RaScan, RaSelect, RaTempScan
+from .storage import Column, ColumnTable
+from .udf import FAIL_MESSAGES
+
+_NO_FAIL = (1 << 64) - 1
+
+
+@dataclass
+class RowSelection:
+    """Subset of a table's rows: ascending device row ids, or every row (``indices=None``)."""
+
+    table: ColumnTable
+    indices: torch.Tensor | None = None
+
+    @property
+    def count(self) -> int:
+        return self.table.row_count if self.indices is None else int(self.indices.numel())
+
+    def to_indices(self) -> torch.Tensor:
+        if self.indices is None:
+            return torch.arange(self.table.row_count, dtype=torch.int64, device=self.table.device)
+        return self.indices
+
+
+# ------------------------------------------------------------------------------------------------
+# launches
+# ------------------------------------------------------------------------------------------------
+def _stream(device: torch.device) -> torch.cuda.Stream:
+    if device.type != "cuda":
+        raise N.NativeUnavailable(f"table lives on {device}; the ESC kernels need a CUDA device")
+    return torch.cuda.current_stream(device)
+
+
+def _row_ids(selection: RowSelection | None):
+    if selection is None or selection.indices is None:
+        return None, (selection.table.row_count if selection is not None else None)
+    ids = selection.indices
+    if ids.dtype != torch.int64 or not ids.is_contiguous():
+        ids = ids.to(torch.int64).contiguous()
+    return ids, int(ids.numel())
+
+
+def launch_count(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int,
+                 sync: bool = True):
+    """K1 over ``n`` logical rows; returns (count, [udf fail words]) after a stream sync."""
+    lib = N.load_library()
+    stream = _stream(table.device)
+    ws = N.workspace(table.device, stream)
+    ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
+    cols = cp.column_array()
+    N.check(lib.esc_scan_count(C.byref(cp.program), cols, cp.ncols, n,
+                               C.c_void_p(ids.data_ptr()) if ids is not None else None,
+                               C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
+                               C.c_void_p(stream.cuda_stream)), "esc_scan_count")
+    if not sync:
+        return None
+    stream.synchronize()
+    return ws.read_result(cp.n_udfs)
+
+
+def launch_compact(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int,
+                   proj_cols: list, capacity: int, want_row_ids: bool, stage_proj: bool = False):
+    """K2: fused predicate + count + order-preserving compaction of ``proj_cols`` (and/or the
+    physical row ids) into fresh buffers of ``capacity`` rows."""
+    lib = N.load_library()
+    stream = _stream(table.device)
+    ws = N.workspace(table.device, stream)
+    ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
+    extra, slots = [], []
+    for col in proj_cols:
+        if col.name in cp.slot_of:
+            slots.append(cp.slot_of[col.name])
+        else:
+            slots.append(cp.ncols + len(extra))
+            extra.append(col)
+    if cp.ncols + len(extra) > N.MAX_COLS or len(proj_cols) > N.MAX_PROJ:
+        raise ExecutionError("too many columns for one compaction")
+    cols = cp.column_array(extra)
+    if stage_proj:
+        for k in range(cp.ncols, cp.ncols + len(extra)):
+            cols[k].flags |= N.COL_STAGE
+    outs = N.EscOutputs()
+    outs.n_proj = len(proj_cols)
+    outs.capacity = capacity
+    values, nulls = [], []
+    dev = table.device
+    for k, col in enumerate(proj_cols):
+        v = torch.empty(capacity, dtype=col.values.dtype, device=dev)
+        m = torch.empty(capacity, dtype=torch.bool, device=dev) if col.nulls is not None else None
+        values.append(v)
+        nulls.append(m)
+        outs.slot[k] = slots[k]
+        outs.out_values[k] = v.data_ptr() if capacity else None
+        outs.out_nulls[k] = m.data_ptr() if m is not None and capacity else None
+    rows = torch.empty(capacity, dtype=torch.int64, device=dev) if want_row_ids else None
+    outs.out_row_ids = rows.data_ptr() if rows is not None and capacity else None
+    N.check(lib.esc_compact(C.byref(cp.program), cols, cp.ncols + len(extra), n,
+                            C.c_void_p(ids.data_ptr()) if ids is not None else None, C.byref(outs),
+                            C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
+                            C.c_void_p(stream.cuda_stream)), "esc_compact")
+    stream.synchronize()
+    count, fails = ws.read_result(cp.n_udfs)
+    return count, fails, values, nulls, rows
+
+
+# ------------------------------------------------------------------------------------------------
+# UDF error replay (reference short-circuit semantics)
+# ------------------------------------------------------------------------------------------------
+def _contains(node, targets: set) -> bool:
+    return any(id(a) in targets for a in ex.atoms(node))
+
+
+def raise_udf_errors(table: ColumnTable, cp: CompiledPredicate, fails: list, ids, n: int):
+    """Raise the ExecutionError the reference would raise for this evaluation, if any."""
+    failing = {}
+    for node_id, u in cp.udf_index.items():
+        if u < len(fails) and fails[u] != _NO_FAIL:
+            failing[node_id] = (fails[u] >> 3, fails[u] & 7)
+    unbound = {id(a) for a in cp.unbound}
+    targets = set(failing) | unbound
+    if not targets:
+        return
+
+    def count(sub) -> int:
+        scp = compile_predicate(table, sub)
+        c, _ = launch_count(scp, table, ids, n)
+        return c
+
+    def check(node):
+        if isinstance(node, ex.FnCall):
+            if id(node) in unbound:
+                raise ExecutionError(f"function {node.name!r} has no bound implementation")
+            if id(node) in failing:
+                row, code = failing[id(node)]
+                raise ExecutionError(f"UDF {node.name!r} failed at row {row}: {FAIL_MESSAGES[code]}")
+            return
+        if isinstance(node, ex.ATOM_TYPES):
+            return
+        if isinstance(node, ex.Not):
+            return check(node.child)
+        items = node.items
+        check(items[0])
+        for k in range(1, len(items)):
+            if not _contains(items[k], targets):
+                continue
+            prefix = type(node)(tuple(items[:k]))
+            c = count(prefix)
+            if isinstance(node, ex.And) and c == 0:
+                return  # reference: `if not mask.any(): break`
+            if isinstance(node, ex.Or) and c == n:
+                return  # reference: `if mask.all(): break`
+            check(items[k])
+
+    check(cp.pred)
+
+
+# ------------------------------------------------------------------------------------------------
+# public API (reference names)
+# ------------------------------------------------------------------------------------------------
+def _count_with_errors(table, pred, selection=None) -> int:
+    cp = compile_predicate(table, pred)
+    ids, n = _row_ids(selection if selection is not None else RowSelection(table))
+    count, fails = launch_count(cp, table, ids, n)
+    if cp.unbound or cp.may_fail:
+        raise_udf_errors(table, cp, fails, ids, n)
+    return count
+
+
+def count_star(table: ColumnTable, pred: ex.Expr | None) -> int:
+    """Exact number of rows satisfying ``pred`` (reference ``executor.py:218-224``); nothing is
+    materialised — one fused scan over the predicate columns."""
+    if pred is None:
+        return table.row_count
+    return _count_with_errors(table, pred)
+
+
+def eval_predicate(table: ColumnTable, pred: ex.Expr | None,
+                   selection: RowSelection | None = None) -> RowSelection:
+    """Rows of ``selection`` (default: all) satisfying ``pred`` as ascending device row ids
+    (reference ``executor.py:202-215``)."""
+    if selection is None:
+        selection = RowSelection(table)
+    if pred is None:
+        return selection
+    cp = compile_predicate(table, pred)
+    ids, n = _row_ids(selection)
+    k = _count_with_errors(table, pred, selection)
+    count, _, _, _, rows = launch_compact(cp, table, ids, n, [], k, want_row_ids=True)
+    if count != k:
+        raise ExecutionError(f"internal: compaction counted {count} rows, scan counted {k}")
+    return RowSelection(table, rows)
+
+
+def materialize(table: ColumnTable, pred: ex.Expr, needed, count: int | None = None,
+                stage_proj: bool | None = None) -> list[Column]:
+    """Qualifying rows of ``needed`` columns, in row order, as new device columns — the fused
+    equivalent of ``eval_predicate(...).to_indices()`` + ``Column.take`` per column
+    (reference ``optimizer.py:191-192``).  ``count`` (when the ESC count sub-query already
+    produced it) sizes the outputs and saves the sizing scan."""
+    cp = compile_predicate(table, pred)
+    ids, n = _row_ids(RowSelection(table))
+    if count is None:
+        count = _count_with_errors(table, pred)
+    proj = [table.column(name) for name in needed]
+    if stage_proj is None:
+        # stream projection-only columns through smem once hits are dense enough that nearly
+        # every 32-byte sector of those columns is touched anyway
+        stage_proj = n > 0 and count * 8 >= n
+    got, _, values, nulls, _ = launch_compact(cp, table, ids, n, proj, count, want_row_ids=False,
+                                              stage_proj=stage_proj)
+    if got != count:
+        raise ExecutionError(f"internal: compaction counted {got} rows, expected {count}")
+    return [Column(c.name, c.kind, v, m, c.dictionary) for c, v, m in zip(proj, values, nulls)]
+
+
+def take_column(col: Column, indices) -> Column:
+    """``Column.take`` on the device (reference ``storage.py:176-184``)."""
+    lib = N.load_library()
+    dev = col.device
+    stream = _stream(dev)
+    idx = indices if isinstance(indices, torch.Tensor) else torch.as_tensor(indices)
+    idx = idx.to(device=dev, dtype=torch.int64).contiguous()
+    n = int(idx.numel())
+    out = torch.empty(n, dtype=col.values.dtype, device=dev)
+    nulls = torch.empty(n, dtype=torch.bool, device=dev) if col.nulls is not None else None
+    desc = N.EscColumn()
+    desc.data = col.values.data_ptr() if len(col) else None
+    desc.nulls = col.nulls.data_ptr() if col.nulls is not None and len(col) else None
+    desc.dtype = N.dtype_code(col.values)
+    N.check(lib.esc_gather(C.byref(desc), C.c_void_p(idx.data_ptr()) if n else None, n,
+                           C.c_void_p(out.data_ptr()) if n else None,
+                           C.c_void_p(nulls.data_ptr()) if nulls is not None and n else None,
+                           C.c_void_p(stream.cuda_stream)), "esc_gather")
+    return Column(col.name, col.kind, out, nulls, col.dictionary)
+
+
+def execute_count(ra, catalog) -> int:
+    """Single-table COUNT tree: Aggregate over optional Select over optional Project over a
+    Scan / TempScan (reference ``executor.py:232-250``)."""
+    node = ra.child if isinstance(ra, RaAggregate) else ra
+    pred = None
+    if isinstance(node, RaSelect):
+        pred, node = node.predicate, node.child
+    if isinstance(node, RaProject):
+        node = node.child
+    if isinstance(node, RaScan):
+        table = catalog.table(node.table)
+    elif isinstance(node, RaTempScan):
+        table = catalog.resolve_temp(node.handle)
+    else:
+        raise ExecutionError(f"cannot count over node {type(node).__name__}")
+    return count_star(table, pred)
