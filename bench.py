@@ -1,0 +1,515 @@
+#!/usr/bin/env python
+"""ESC selectivity sub-query benchmark (B200).
+
+One *step* = the per-table ESC sub-query on config 4 of BASELINE.json (600M rows: Zipf A,
+correlated B, float32 C, uniform D; predicate ``A = 0 AND C BETWEEN -0.5 AND 1.0 AND (D = 17 OR
+D > 900) AND (B*3 + D) % 7 > 3`` with the last term a Python UDF): exact count + push-down
+decision + order-preserving materialization of (A, C, D) — one fused kernel pass per GPU, plus
+one NCCL count/offset exchange when the table is row-partitioned over N > 1 GPUs (strong
+scaling: the 600M rows are split across the ranks).
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference algorithm's CPU
+implementation (the numpy port in ``oracle/``) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only when MEASURED_PEAKS.json is absent
+L2_BYTES = 126 * 2**20
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--rows", type=int, default=600_000_000)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extras", action="store_true")
+    p.add_argument("--sweep", default="", help="write the config-5 selectivity sweep JSON here")
+    p.add_argument("--cpu-sample-rows", type=int, default=0)
+    return p.parse_args()
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def recorded_traffic(kind: str):
+    """dram bytes per launch from the committed ncu capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(kind)
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:6], float(parts[6])))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        loaded = [r for r in rows if r[3] > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU side: the reference algorithm (numpy port) over row-range chunks in a process pool
+# ------------------------------------------------------------------------------------------------
+_CPU_STATE = {}
+
+
+def _cpu_chunk(bounds):
+    from oracle import esc_oracle as O
+
+    lo, hi = bounds
+    st = _CPU_STATE
+    t = O.OTable("t", {k: O.OColumn(v[lo:hi], np.zeros(hi - lo, bool)) for k, v in st["cols"].items()})
+    count = O.count_star(t, st["pred"], st["udfs"])
+    mat = O.materialize(t, st["pred"], st["project"], st["udfs"])  # reference re-scans
+    return count, sum(c.values.nbytes for c in mat.values())
+
+
+def cpu_reference_run(cols: dict, pred, project, udfs, rows: int, procs: int, reps: int = 1):
+    """Time the reference algorithm (count sub-query + materialization) over ``rows`` rows split
+    into ``procs`` contiguous chunks run in parallel processes; returns (seconds per rep, count)."""
+    import multiprocessing as mp
+
+    _CPU_STATE.update(cols={k: v[:rows] for k, v in cols.items()}, pred=pred, project=project, udfs=udfs)
+    bounds = [((i * rows) // procs, ((i + 1) * rows) // procs) for i in range(procs)]
+    ctx = mp.get_context("fork")
+    times, count = [], 0
+    with ctx.Pool(procs) as pool:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_chunk, bounds)
+            times.append(time.perf_counter() - t0)
+            count = sum(r[0] for r in res)
+    return times, count
+
+
+def default_cpu_rows(procs: int) -> int:
+    # config 4 through the reference costs ~0.4 us/row/core (Python UDF via np.frompyfunc, twice):
+    # ~1.2M rows per core keeps one rep near 1 s, a bounded sample of the 600M-row workload
+    return 1_200_000 * procs
+
+
+# ------------------------------------------------------------------------------------------------
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from paper_1901_01488_b200 import datagen
+
+    procs = os.cpu_count() or 1
+    rows = args.cpu_sample_rows or default_cpu_rows(procs)
+    w = datagen.config4_blocked(args.rows, 0, rows)
+    cols = {k: v[1] for k, v in w.columns.items()}
+    times, count = cpu_reference_run(cols, w.pred, w.project, w.udfs, rows, procs, reps=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    per_step = sum(timed) / len(timed)
+    value = rows / per_step
+    line = {
+        "impl": "reference", "metric": "rows/s (ESC sub-query: scan+count+compaction)", "value": value,
+        "unit": "rows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "i32+f32+f64", "data": "synthetic (block-seeded Appendix B config-4 recipe)",
+        "config": {"workload": "config4 (BASELINE configs[3]) bounded sample", "rows_total": args.rows,
+                   "sample_rows": rows, "sample_count": count},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": "port",
+                         "sample": f"first {rows} rows of config 4, {procs} processes x contiguous row ranges; "
+                                   "numpy port of executor.count_star + optimizer.materialize_pushdown "
+                                   "(Python UDF via np.frompyfunc)"},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_1901_01488_b200 import datagen
+
+    n = args.rows
+    bounds = [((r * n) // world, ((r + 1) * n) // world) for r in range(world)]
+    lo, hi = bounds[rank]
+    m = hi - lo
+
+    # host shard, generated straight into pinned buffers (they feed both the resident table and
+    # the end-to-end leg's host->device copies)
+    threads = max(1, (os.cpu_count() or 1) // world)
+    pinned = {k: torch.empty(m, dtype=torch.float32 if k == "C" else torch.int32, pin_memory=True) for k in "ABCD"}
+    t0 = time.perf_counter()
+    w = datagen.config4_blocked(n, lo, hi, out={k: v.numpy() for k, v in pinned.items()}, threads=threads)
+    gen_s = time.perf_counter() - t0
+
+    # CPU baseline BEFORE any CUDA context exists (the pool forks)
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = os.cpu_count() or 1
+        rows = min(m, args.cpu_sample_rows or default_cpu_rows(procs))
+        cols = {k: v[1] for k, v in w.columns.items()}
+        times, _ = cpu_reference_run(cols, w.pred, w.project, w.udfs, rows, procs, reps=2)
+        per = min(times[1:]) if len(times) > 1 else times[0]
+        cpu_baseline = {"value": rows / per, "unit": "rows/s", "cores": procs, "kind": "port",
+                        "sample": f"first {rows} rows of this config-4 shard; numpy port of the reference "
+                                  f"(count sub-query + materialization) in {procs} processes"}
+
+    import torch.distributed as dist
+
+    from paper_1901_01488_b200 import executor, multigpu, optimizer, serde
+    from paper_1901_01488_b200.catalog import Catalog
+    from paper_1901_01488_b200.storage import Column, ColumnTable, parse_kind
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pred = serde.from_json(w.pred, "t", w.udfs)
+    cfg = optimizer.EscConfig()
+
+    def make_table():
+        return ColumnTable("t", [Column(k, parse_kind(w.columns[k][0]), pinned[k].to(dev, non_blocking=True))
+                                 for k in "ABCD"])
+
+    table = make_table()
+    torch.cuda.synchronize()
+    cat = Catalog()
+    cat.register(table)
+    st = multigpu.ShardedTable("t", table, n, lo, rank, world)
+
+    def step():
+        if world > 1:
+            d = multigpu.sharded_esc_subquery(st, pred, w.project, cfg)
+            return d.exact_count, d.local_count
+        d = optimizer.esc_subquery(cat, "t", pred, w.project, cfg)
+        cat.temps.sweep()
+        return d.exact_count, d.exact_count
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    stream = torch.cuda.current_stream()
+    executor.KERNEL_EVENTS = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            total, local = step()
+        e1.record(stream)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    events = executor.KERNEL_EVENTS
+    executor.KERNEL_EVENTS = None
+    kern_ms = [a.elapsed_time(b) for a, b, k in events if k == "compact"]
+    launches = len(events)
+    kern_avg = statistics.mean(kern_ms)
+    k_local = local
+    algo_bytes = m * w.pred_bytes_per_row() + k_local * sum(w.columns[c][1].itemsize for c in w.project)
+    peak, peak_src = peak_hbm()
+    achieved = algo_bytes / (kern_avg * 1e-3) / 1e9
+    value = n / (ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers ----------------------------------
+    e2e = None
+    if not args.no_e2e:
+        proj_bytes = sum(w.columns[c][1].itemsize for c in w.project)
+
+        def e2e_step():
+            t = make_table()                                    # H2D of this rank's shard
+            c2 = Catalog()
+            c2.register(t)
+            if world > 1:
+                d = multigpu.sharded_esc_subquery(multigpu.ShardedTable("t", t, n, lo, rank, world), pred,
+                                                  w.project, cfg)
+                outs = d.columns or []
+                kk = d.local_count
+            else:
+                d = optimizer.esc_subquery(c2, "t", pred, w.project, cfg)
+                outs = c2.resolve_temp(d.temp).columns if d.temp is not None else []
+                kk = d.exact_count
+            host = [c.values.to("cpu") for c in outs]            # D2H of the result
+            c2.temps.sweep()
+            return kk, host
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            kk, _ = e2e_step()
+        s1.record(stream)
+        barrier()
+        ems = max_over_ranks(s0.elapsed_time(s1)) / args.steps
+        e2e = {"value": n / (ems * 1e-3), "unit": "rows/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": m * 16, "d2h_bytes_per_step": kk * proj_bytes,
+               "path": "ColumnTable from pinned host tensors -> optimizer.esc_subquery -> temp columns .to('cpu')"}
+
+    extras = {}
+    if not args.no_extras and world == 1:
+        extras = run_extras(table, w, pred, cfg, dev, peak)
+    if args.sweep and world == 1:
+        del table, cat, st
+        torch.cuda.empty_cache()
+        sweep = run_sweep(args, dev, peak)
+        with open(args.sweep, "w") as fh:
+            json.dump(sweep, fh, indent=1)
+
+    if rank == 0:
+        line = {
+            "metric": "rows/s (ESC sub-query: fused scan+count+compaction)",
+            "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "i32+f32+f64", "data": "synthetic (block-seeded Appendix B config-4 recipe)",
+            "config": {"workload": "config4: 600M-row table, A=x AND C BETWEEN -0.5 AND 1.0 AND (D=17 OR D>900) "
+                                   "AND udf(B,D)>3; count + compaction of (A,C,D)",
+                       "rows": n, "rows_per_gpu": m, "count": total, "selectivity": total / n,
+                       "l2": f"inputs {m * 16 / 1e9:.1f} GB per GPU >> L2 (126 MB): no flush needed",
+                       "parallelism": f"row-partitioned x{world}, NCCL all_gather of counts",
+                       "host_gen_s": round(gen_s, 1)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": recorded_traffic("compact_config4"),
+                         "peak_source": peak_src, "kernel": "esc_scan_kernel<C,COMPACT=true>",
+                         "kernel_ms": kern_avg, "algorithmic_bytes": algo_bytes},
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "extras": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _flush_l2(dev):
+    import torch
+
+    buf = getattr(_flush_l2, "buf", None)
+    if buf is None:
+        buf = _flush_l2.buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    buf.zero_()
+
+
+def _time_kernels(fn, reps, dev, flush=False):
+    import torch
+
+    from paper_1901_01488_b200 import executor
+
+    executor.KERNEL_EVENTS = []
+    for _ in range(reps):
+        if flush:
+            _flush_l2(dev)
+        fn()
+    torch.cuda.synchronize()
+    ev = executor.KERNEL_EVENTS
+    executor.KERNEL_EVENTS = None
+    return [(a.elapsed_time(b), k) for a, b, k in ev]
+
+
+def run_extras(table, w, pred, cfg, dev, peak):
+    """Secondary numbers: count-only K1 on config 4, config 2 (L2 flushed), config 3 ESC overhead."""
+    import torch
+
+    from paper_1901_01488_b200 import count_star, datagen, executor, optimizer, ra, serde
+    from paper_1901_01488_b200.catalog import Catalog
+    from paper_1901_01488_b200.storage import Column, ColumnTable, Dictionary, parse_kind
+
+    out = {}
+    n = table.row_count
+    for _ in range(2):
+        count_star(table, pred)
+    t = _time_kernels(lambda: count_star(table, pred), 5, dev)
+    kms = statistics.mean(x for x, k in t if k == "count")
+    gbs = n * w.pred_bytes_per_row() / (kms * 1e-3) / 1e9
+    out["config4_count_only"] = {"kernel_ms": kms, "rows_per_s": n / (kms * 1e-3), "GBps": gbs, "frac": gbs / peak}
+
+    # config 2: exact recipe, 6M rows (72 MB of predicate columns < L2: flush between reps)
+    w2 = datagen.config2()
+    t2 = ColumnTable("lineitem", [Column(k, parse_kind(v[0]), v[1], None, Dictionary(v[2]) if len(v) > 2 else None,
+                                         device=dev) for k, v in w2.columns.items()])
+    c2 = Catalog()
+    c2.register(t2)
+    p2 = serde.from_json(w2.pred, "lineitem")
+    d = optimizer.esc_subquery(c2, "lineitem", p2, w2.project, cfg)
+    c2.temps.sweep()
+    tt = _time_kernels(lambda: (optimizer.esc_subquery(c2, "lineitem", p2, w2.project, cfg), c2.temps.sweep()),
+                       10, dev, flush=True)
+    kms = statistics.mean(x for x, k in tt if k == "compact")
+    b2 = w2.algorithmic_bytes(d.exact_count)
+    out["config2_fused"] = {"count": d.exact_count, "kernel_ms": kms, "rows_per_s": w2.nrows / (kms * 1e-3),
+                            "GBps": b2 / (kms * 1e-3) / 1e9, "frac": b2 / (kms * 1e-3) / 1e9 / peak,
+                            "note": "L2 flushed before every rep"}
+
+    # config 3: ESC overhead of the 4-dimension star query (reference definition, engine.py:69)
+    g = datagen.config3(fact_rows=1)
+    c3 = Catalog()
+    for name, cols in g.items():
+        if name == "fact":
+            continue
+        c3.register(ColumnTable(name, [Column(k, parse_kind(v[0]), v[1], None,
+                                              Dictionary(v[2]) if len(v) > 2 else None, device=dev)
+                                       for k, v in cols.items()]))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(30)
+    fact_cols = []
+    for fk, dim in (("f_datekey", "date"), ("f_custkey", "customer"), ("f_suppkey", "supplier"), ("f_partkey", "part")):
+        fact_cols.append(Column(fk, parse_kind("INT32"), torch.randint(1, datagen.DIM_SIZES[dim] + 1, (60_000_000,),
+                                                                       generator=gen, device=dev, dtype=torch.int32)))
+    c3.register(ColumnTable("fact", fact_cols))
+    from paper_1901_01488_b200 import expr as ex
+
+    conj = [ex.ColumnCompare(ex.ColumnRef("fact", a), "=", ex.ColumnRef(dim, b))
+            for _, a, dim, b in datagen.CONFIG3_EDGES]
+    conj += [serde.from_json(j, dim) for dim, j in datagen.CONFIG3_WHERE.items()]
+    q = ra.query(c3, ["fact", "date", "customer", "supplier", "part"], ex.And(tuple(conj)))
+    overheads, walls, plan_ = [], [], None
+    for i in range(12):
+        t0 = time.perf_counter()
+        plan_ = optimizer.plan(q, c3, cfg)
+        wall = (time.perf_counter() - t0) * 1e3
+        if i >= 2:
+            overheads.append(optimizer.esc_overhead_ms(plan_))
+            walls.append(wall)
+        c3.temps.sweep()
+    out["config3_esc"] = {
+        "overhead_ms_median": statistics.median(overheads), "plan_wall_ms_median": statistics.median(walls),
+        "decisions": [(d.table, d.exact_count, d.row_count, d.pushed_down) for d in plan_.decisions],
+        "build_order": plan_.build_order, "build_card_sum": plan_.build_card_sum,
+        "target_ms": 5.0, "reference_cpu_ms": 0.66,
+    }
+    return out
+
+
+def run_sweep(args, dev, peak):
+    """Config 5: single-range and 4-column conjunctive predicates at six selectivities, count-only
+    vs fused count+compaction of (c0, c1, c4, c5); HBM GB/s vs selectivity."""
+    import torch
+
+    from paper_1901_01488_b200 import count_star, datagen, executor, optimizer, serde
+    from paper_1901_01488_b200.catalog import Catalog
+    from paper_1901_01488_b200.storage import Column, ColumnTable, parse_kind
+
+    n = args.rows
+    w = datagen.config5_blocked(n, 0.01)
+    t = ColumnTable("t", [Column(k, parse_kind(v[0]), v[1], device=dev) for k, v in w.columns.items()])
+    del w
+    res = []
+    for conj4 in (False, True):
+        for s in datagen.CONFIG5_SELECTIVITIES:
+            wl = datagen.config5(8, s, conj4)
+            wl.columns = {k: (("INT32" if int(k[1]) < 4 else "INT64"), np.empty(n, np.int32 if int(k[1]) < 4 else np.int64))
+                          for k in t._by_name}
+            p = serde.from_json(wl.pred, "t")
+            cat = Catalog()
+            cat.register(t)
+            cfg = optimizer.EscConfig(max_selectivity=1.0)
+            count_star(t, p)
+            tc = _time_kernels(lambda: count_star(t, p), 3, dev)
+            cms = statistics.mean(x for x, k in tc if k == "count")
+            k = count_star(t, p)
+            tm = _time_kernels(lambda: executor.materialize(t, p, wl.project, count=k), 3, dev)
+            mms = statistics.mean(x for x, kk in tm if kk == "compact")
+            bc = wl.algorithmic_bytes(k, materialize=False)
+            bm = wl.algorithmic_bytes(k, materialize=True)
+            res.append({"pred": "conj4" if conj4 else "single", "s": s, "count": k, "count_ms": cms,
+                        "count_GBps": bc / cms / 1e6, "count_frac": bc / cms / 1e6 / peak,
+                        "compact_ms": mms, "compact_GBps": bm / mms / 1e6, "compact_frac": bm / mms / 1e6 / peak})
+            torch.cuda.empty_cache()
+    return {"rows": n, "peak_GBps": peak, "results": res}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -30,8 +30,20 @@
 #ifndef ESC_H_
 #define ESC_H_
 
+#ifdef __CUDACC_RTC__  /* compiled by NVRTC for the JIT tier: no system headers */
+typedef signed char int8_t;
+typedef short int16_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long size_t;
+#else
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -218,6 +230,13 @@ const char* esc_last_error(void);
 int esc_abi_version(void);
 /* Number of SMs of the current device (0 when no device). */
 int esc_device_sm_count(void);
+/* JIT tier (NVRTC-specialised predicate evaluators for large scans).
+ * mode 0 = off (interpreter only), 1 = auto (scans of >= min_rows rows; default 2^22),
+ * 2 = always; min_rows < 0 keeps the current threshold. */
+int esc_set_jit(int mode, int64_t min_rows);
+/* out[0..4] = modules compiled, cache hits, compile failures, total compile microseconds,
+ * NVRTC available (0/1). */
+int esc_jit_stats(int64_t* out);
 /* sizeof() of the ABI structs, for binding checks: 0 program, 1 instr, 2 udf, 3 udf_op,
  * 4 column, 5 result, 6 outputs; -1 for an unknown id. */
 int esc_struct_size(int which);

@@ -100,6 +100,8 @@ _SIGNATURES = {
     "esc_device_sm_count": (C.c_int, []),
     "esc_struct_size": (C.c_int, [C.c_int]),
     "esc_tile_rows": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32]),
+    "esc_set_jit": (C.c_int, [C.c_int, C.c_int64]),
+    "esc_jit_stats": (C.c_int, [C.POINTER(C.c_int64)]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -132,6 +134,18 @@ def load_library(path: str = LIB_PATH):
                                         f"C={lib.esc_struct_size(i)} ctypes={C.sizeof(st)}")
         _lib = lib
         return lib
+
+
+def set_jit(mode: int, min_rows: int = -1):
+    """0 = interpreter only, 1 = JIT scans of >= min_rows rows, 2 = always JIT."""
+    check(load_library().esc_set_jit(int(mode), int(min_rows)), "esc_set_jit")
+
+
+def jit_stats() -> dict:
+    out = (C.c_int64 * 5)()
+    check(load_library().esc_jit_stats(out), "esc_jit_stats")
+    return {"compiled": out[0], "hits": out[1], "failures": out[2], "compile_ms": out[3] / 1e3,
+            "nvrtc": bool(out[4])}
 
 
 def check(rc: int, what: str):

@@ -1,0 +1,892 @@
+// esc_device.cuh — device side of the ESC kernels (design notes: esc_kernels.cu).
+//
+// Compiled twice: ahead of time by nvcc (esc_kernels.cu, predicate = the opcode interpreter) and
+// at run time by NVRTC for the JIT tier (predicate = generated straight-line code, jit.cpp), so
+// it includes no system headers.
+#pragma once
+
+#include "esc.h"
+
+namespace esc {
+
+
+constexpr int kConsumerWarps = 16;
+constexpr int kChunkRows = 128;  // one warp chunk: 32 lanes x 4 consecutive rows
+constexpr int kMaxStages = 8;
+constexpr uint32_t kSmemBudget = 200 * 1024;  // dynamic smem for the stage ring
+constexpr int kStatusValueBits = 46;
+constexpr unsigned long long kStatusValueMask = (1ull << kStatusValueBits) - 1;
+constexpr unsigned long long kFlagAggregate = 1;
+constexpr unsigned long long kFlagPrefix = 2;
+constexpr uint32_t kNoNulls = 0xFFFFFFFFu;
+
+template <bool COMPACT>
+struct Layout {
+  static constexpr int kFirstConsumer = COMPACT ? 2 : 1;
+  static constexpr int kThreads = (kFirstConsumer + kConsumerWarps) * 32;
+};
+
+// ------------------------------------------------------------------------------------------
+// workspace layout
+// ------------------------------------------------------------------------------------------
+struct WsHeader {
+  unsigned long long count;   // running count (atomicAdd per CTA)
+  unsigned long long ticket;  // tile ticket counter (compaction)
+  unsigned long long done;    // CTAs finished (last-CTA detection)
+  unsigned long long pad0;
+  unsigned long long fail[ESC_MAX_UDFS];  // first failing row per UDF (packed), ~0 = none
+  unsigned long long pad1[4];
+};
+static_assert(sizeof(WsHeader) == 128, "header is one 128-byte line");
+
+// lowered (kernel-internal) opcodes
+enum KOp : uint8_t {
+  K_RANGE_S8 = 0, K_RANGE_U8, K_RANGE_S16, K_RANGE_U16, K_RANGE_S32,  // int32 domain
+  K_RANGE_S64, K_RANGE_U32,                                           // int64 domain
+  K_RANGE_F32,                                                        // float32 column
+  K_RANGE_F64,                                                        // any column -> float64
+  K_LUT, K_COLCMP, K_NOTNULL, K_FALSE, K_UDF, K_PUSH, K_POP, K_NOT
+};
+
+struct KInstr {
+  uint8_t op, combine, neg, col, col_b, cmp, domain, inv;  // inv: NE lowered to !EQ, applied before the NULL floor
+  uint32_t soff;  // smem offset of col's values in a stage
+  uint32_t noff;  // smem offset of col's null bytes in a stage, kNoNulls if the column has none
+  union { long long i; double f; } lo, hi;
+  uint32_t aux, aux2;  // LUT word offset / size, UDF index
+  uint32_t soff_b, noff_b;  // second column (COLCMP)
+};
+
+struct KCol {
+  const uint8_t* data;
+  const uint8_t* nulls;
+  int32_t dtype;
+  int32_t width;
+  int32_t staged;       // values staged in smem for full tiles
+  int32_t nulls_staged; // null bytes staged in smem for full tiles
+  uint32_t smem_off;
+  uint32_t smem_null_off;
+};
+
+struct KParams {
+  KInstr ins[ESC_MAX_INSTRS];
+  esc_udf_t udfs[ESC_MAX_UDFS];
+  esc_udf_op_t udf_ops[ESC_MAX_UDF_OPS];
+  const uint32_t* lut;
+  KCol cols[ESC_MAX_COLS];
+  int32_t n_ins;
+  int32_t ncols;
+  int32_t chunks;       // C
+  int32_t tile_rows;    // T = kConsumerWarps * 128 * C
+  int32_t stages;
+  uint32_t stage_bytes;
+  uint32_t epoch;
+  int32_t all_staged;   // every column the program reads is staged (fast evaluator usable)
+  int64_t nrows;
+  int64_t n_tiles;
+  int64_t n_full_tiles;  // tiles [0, n_full_tiles) are staged with TMA
+  const int64_t* row_ids;
+  WsHeader* hdr;
+  unsigned long long* status;
+  esc_result_t* result;
+  esc_outputs_t outs;
+};
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers: mbarrier, bulk copy, release/acquire
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// scalar loads (cold paths: tail tiles, selections, UDF arguments, scatter)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ long long ld_int(const uint8_t* p, int dtype) {
+  switch (dtype) {
+    case ESC_I8: return *reinterpret_cast<const int8_t*>(p);
+    case ESC_I16: return *reinterpret_cast<const int16_t*>(p);
+    case ESC_I32: return *reinterpret_cast<const int32_t*>(p);
+    case ESC_U8: return *reinterpret_cast<const uint8_t*>(p);
+    case ESC_U16: return *reinterpret_cast<const uint16_t*>(p);
+    case ESC_U32: return *reinterpret_cast<const uint32_t*>(p);
+    default: return *reinterpret_cast<const long long*>(p);
+  }
+}
+// float64 value of any column type (numpy's astype(float64): RN for int64)
+__device__ __forceinline__ double ld_f64(const uint8_t* p, int dtype) {
+  switch (dtype) {
+    case ESC_F32: return (double)*reinterpret_cast<const float*>(p);
+    case ESC_F64: return *reinterpret_cast<const double*>(p);
+    case ESC_I64: return __ll2double_rn(*reinterpret_cast<const long long*>(p));
+    default: return (double)ld_int(p, dtype);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// hot path: staged tile, smem-only opcode loops
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void lds4(const uint8_t* p, T (&v)[4]) {
+  if constexpr (sizeof(T) == 1) {
+    union { uint32_t u; T t[4]; } x;
+    x.u = *reinterpret_cast<const uint32_t*>(p);
+    v[0] = x.t[0]; v[1] = x.t[1]; v[2] = x.t[2]; v[3] = x.t[3];
+  } else if constexpr (sizeof(T) == 2) {
+    union { uint2 u; T t[4]; } x;
+    x.u = *reinterpret_cast<const uint2*>(p);
+    v[0] = x.t[0]; v[1] = x.t[1]; v[2] = x.t[2]; v[3] = x.t[3];
+  } else if constexpr (sizeof(T) == 4) {
+    union { uint4 u; T t[4]; } x;
+    x.u = *reinterpret_cast<const uint4*>(p);
+    v[0] = x.t[0]; v[1] = x.t[1]; v[2] = x.t[2]; v[3] = x.t[3];
+  } else {
+    union { uint4 u[2]; T t[4]; } x;
+    x.u[0] = reinterpret_cast<const uint4*>(p)[0];
+    x.u[1] = reinterpret_cast<const uint4*>(p)[1];
+    v[0] = x.t[0]; v[1] = x.t[1]; v[2] = x.t[2]; v[3] = x.t[3];
+  }
+}
+
+// int32 domain: (u32)v - (u32)lo <= span  <=>  lo <= v <= hi (wrapping arithmetic)
+template <typename T, int C>
+__device__ __forceinline__ uint32_t range_i32(const uint8_t* col, int local0, int32_t lo, uint32_t span) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    T v[4];
+    lds4<T>(col + (size_t)(local0 + kChunkRows * c) * sizeof(T), v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((uint32_t)(int32_t)v[j] - (uint32_t)lo <= span) r |= 1u << (4 * c + j);  // unsigned: no UB
+  }
+  return r;
+}
+
+template <typename T, int C>
+__device__ __forceinline__ uint32_t range_i64(const uint8_t* col, int local0, long long lo, unsigned long long span) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    T v[4];
+    lds4<T>(col + (size_t)(local0 + kChunkRows * c) * sizeof(T), v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((unsigned long long)(long long)v[j] - (unsigned long long)lo <= span) r |= 1u << (4 * c + j);
+  }
+  return r;
+}
+
+template <int C>
+__device__ __forceinline__ uint32_t range_f32(const uint8_t* col, int local0, float lo, float hi) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    float v[4];
+    lds4<float>(col + (size_t)(local0 + kChunkRows * c) * 4, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (v[j] >= lo && v[j] <= hi) r |= 1u << (4 * c + j);
+  }
+  return r;
+}
+
+template <int C>
+__device__ __forceinline__ uint32_t null_bits_staged(const uint8_t* nb, int local0) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const uint32_t x = *reinterpret_cast<const uint32_t*>(nb + local0 + kChunkRows * c);
+    bits |= ((((x & 0x01010101u) * 0x01020408u) >> 24) & 0xFu) << (4 * c);  // bit 0 of each byte
+  }
+  return bits;
+}
+
+__device__ __forceinline__ bool cmp_any(int cmp, double a, double b) {
+  switch (cmp) {
+    case ESC_CMP_EQ: return a == b;
+    case ESC_CMP_NE: return a != b;
+    case ESC_CMP_LT: return a < b;
+    case ESC_CMP_LE: return a <= b;
+    case ESC_CMP_GT: return a > b;
+    default: return a >= b;
+  }
+}
+__device__ __forceinline__ bool cmp_any(int cmp, long long a, long long b) {
+  switch (cmp) {
+    case ESC_CMP_EQ: return a == b;
+    case ESC_CMP_NE: return a != b;
+    case ESC_CMP_LT: return a < b;
+    case ESC_CMP_LE: return a <= b;
+    case ESC_CMP_GT: return a > b;
+    default: return a >= b;
+  }
+}
+__device__ __forceinline__ bool cmp_any(int cmp, float a, float b) {
+  switch (cmp) {
+    case ESC_CMP_EQ: return a == b;
+    case ESC_CMP_NE: return a != b;
+    case ESC_CMP_LT: return a < b;
+    case ESC_CMP_LE: return a <= b;
+    case ESC_CMP_GT: return a > b;
+    default: return a >= b;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// row addressing for one lane of one tile
+// ------------------------------------------------------------------------------------------
+struct RowRef {
+  const uint8_t* stage;  // smem stage (nullptr: direct HBM reads)
+  int64_t grow0;         // logical row of the lane's chunk-0 first row
+  int32_t local0;        // row of chunk 0 within the tile
+  int64_t nrows;
+  const int64_t* ids;    // row-id selection (logical -> physical) or nullptr
+};
+
+__device__ __forceinline__ int64_t logical_row(const RowRef& rr, int bit) {
+  return rr.grow0 + kChunkRows * (bit >> 2) + (bit & 3);
+}
+__device__ __forceinline__ int32_t local_row(const RowRef& rr, int bit) {
+  return rr.local0 + kChunkRows * (bit >> 2) + (bit & 3);
+}
+__device__ __forceinline__ int64_t phys_row(const RowRef& rr, int64_t r) {
+  return rr.ids ? __ldg(rr.ids + r) : r;
+}
+
+// pointer to a column value of the row at `bit`: smem when staged, else HBM
+__device__ __forceinline__ const uint8_t* value_ptr(const KCol& col, const RowRef& rr, int bit) {
+  if (rr.stage != nullptr && col.staged) return rr.stage + col.smem_off + (size_t)local_row(rr, bit) * col.width;
+  return col.data + (size_t)phys_row(rr, logical_row(rr, bit)) * col.width;
+}
+__device__ __forceinline__ bool is_null(const KCol& col, const RowRef& rr, int bit) {
+  if (col.nulls == nullptr) return false;
+  if (rr.stage != nullptr && col.nulls_staged) return rr.stage[col.smem_null_off + local_row(rr, bit)] != 0;
+  return __ldg(col.nulls + phys_row(rr, logical_row(rr, bit))) != 0;
+}
+
+// ---- UDF: CPython float semantics ----------------------------------------------------------
+// CPython float_rem (Objects/floatobject.c)
+__device__ __forceinline__ double py_mod(double vx, double wx) {
+  double mod = fmod(vx, wx);
+  if (mod != 0.0) {
+    if ((wx < 0.0) != (mod < 0.0)) mod = __dadd_rn(mod, wx);
+  } else {
+    mod = copysign(0.0, wx);
+  }
+  return mod;
+}
+
+// CPython _float_div_mod -> floordiv
+__device__ __forceinline__ double py_floordiv(double vx, double wx) {
+  double mod = fmod(vx, wx);
+  double div = __ddiv_rn(__dsub_rn(vx, mod), wx);
+  if (mod != 0.0) {
+    if ((wx < 0.0) != (mod < 0.0)) div = __dsub_rn(div, 1.0);
+  }
+  double fd;
+  if (div != 0.0) {
+    fd = floor(div);
+    if (__dsub_rn(div, fd) > 0.5) fd = __dadd_rn(fd, 1.0);
+  } else {
+    fd = copysign(0.0, __ddiv_rn(vx, wx));
+  }
+  return fd;
+}
+
+__device__ __noinline__ double udf_eval(const KParams& p, const esc_udf_t& u, const RowRef& rr, int bit,
+                                        uint32_t* fail) {
+  double stk[16];
+  int sp = 0;
+  double args[ESC_MAX_UDF_ARGS];
+  for (int a = 0; a < u.n_args; ++a) {
+    const KCol& col = p.cols[u.arg_col[a]];
+    double x = ld_f64(value_ptr(col, rr, bit), col.dtype);
+    if (u.arg_div[a] != 0.0) x = __ddiv_rn(x, u.arg_div[a]);
+    args[a] = x;
+  }
+  for (int i = 0; i < u.n_ops; ++i) {
+    const esc_udf_op_t& o = p.udf_ops[u.first_op + i];
+    switch (o.op) {
+      case ESC_UDF_ARG: stk[sp++] = args[o.arg]; break;
+      case ESC_UDF_CONST: stk[sp++] = o.k; break;
+      case ESC_UDF_NEG: stk[sp - 1] = -stk[sp - 1]; break;
+      case ESC_UDF_ABS: stk[sp - 1] = fabs(stk[sp - 1]); break;
+      case ESC_UDF_SQUARE: {
+        const double x = stk[sp - 1];
+        const double y = __dmul_rn(x, x);
+        if (isinf(y) && isfinite(x)) { *fail = ESC_FAIL_POW; return 0.0; }
+        stk[sp - 1] = y;
+        break;
+      }
+      default: {
+        const double b = stk[--sp];
+        const double a = stk[sp - 1];
+        double r;
+        switch (o.op) {
+          case ESC_UDF_ADD: r = __dadd_rn(a, b); break;
+          case ESC_UDF_SUB: r = __dsub_rn(a, b); break;
+          case ESC_UDF_MUL: r = __dmul_rn(a, b); break;
+          case ESC_UDF_DIV:
+            if (b == 0.0) { *fail = ESC_FAIL_DIV; return 0.0; }
+            r = __ddiv_rn(a, b);
+            break;
+          case ESC_UDF_MOD:
+            if (b == 0.0) { *fail = ESC_FAIL_MOD; return 0.0; }
+            r = py_mod(a, b);
+            break;
+          default:  // FLOORDIV
+            if (b == 0.0) { *fail = ESC_FAIL_FLOORDIV; return 0.0; }
+            r = py_floordiv(a, b);
+            break;
+        }
+        stk[sp - 1] = r;
+      }
+    }
+  }
+  return stk[0];
+}
+
+// UDF atom on the rows of `todo` (all valid rows when the UDF can fail, else the rows whose
+// value can still change the result); false where any argument is NULL (executor.py:146)
+__device__ __noinline__ uint32_t atom_udf(const KParams& p, const KInstr& I, const RowRef& rr, uint32_t care,
+                                          uint32_t valid) {
+  const esc_udf_t& u = p.udfs[I.aux];
+  uint32_t todo = u.dense ? valid : (care & valid);
+  uint32_t r = 0;
+  while (todo) {
+    const int bit = __ffs(todo) - 1;
+    todo &= todo - 1;
+    uint32_t failed = 0;
+    const double v = udf_eval(p, u, rr, bit, &failed);
+    if (failed) {
+      atomicMin(&p.hdr->fail[I.aux], (unsigned long long)(logical_row(rr, bit) << 3) | failed);
+      continue;
+    }
+    bool anynull = false;
+    for (int a = 0; a < u.n_args; ++a) anynull |= is_null(p.cols[u.arg_col[a]], rr, bit);
+    if (!anynull && cmp_any(I.cmp, v, I.lo.f)) r |= 1u << bit;
+  }
+  return r;
+}
+
+// ---- generic per-row atom evaluation (cold: tail tiles, selections, LUT, column compare) ----
+__device__ __noinline__ uint32_t atom_generic(const KParams& p, const KInstr& I, const RowRef& rr, uint32_t valid) {
+  uint32_t r = 0;
+  uint32_t todo = valid;
+  while (todo) {
+    const int bit = __ffs(todo) - 1;
+    todo &= todo - 1;
+    bool t = false;
+    switch (I.op) {
+      case K_NOTNULL:
+        t = true;
+        break;
+      case K_RANGE_F32: {
+        const float v = *reinterpret_cast<const float*>(value_ptr(p.cols[I.col], rr, bit));
+        t = v >= (float)I.lo.f && v <= (float)I.hi.f;
+        break;
+      }
+      case K_RANGE_F64: {
+        const KCol& col = p.cols[I.col];
+        const double v = ld_f64(value_ptr(col, rr, bit), col.dtype);
+        t = v >= I.lo.f && v <= I.hi.f;
+        break;
+      }
+      case K_LUT: {
+        const KCol& col = p.cols[I.col];
+        const long long code = ld_int(value_ptr(col, rr, bit), col.dtype);
+        if (code >= 0 && code < (long long)I.aux2) t = (__ldg(p.lut + I.aux + (code >> 5)) >> (code & 31)) & 1u;
+        break;
+      }
+      case K_COLCMP: {
+        const KCol& a = p.cols[I.col];
+        const KCol& b = p.cols[I.col_b];
+        const uint8_t* pa = value_ptr(a, rr, bit);
+        const uint8_t* pb = value_ptr(b, rr, bit);
+        if (I.domain == ESC_DOM_I64) {
+          t = cmp_any(I.cmp, ld_int(pa, a.dtype), ld_int(pb, b.dtype));
+        } else if (I.domain == ESC_DOM_F32) {  // f32 x {f32, int8, int16, uint8, uint16}: exact in f32
+          t = cmp_any(I.cmp, (float)ld_f64(pa, a.dtype), (float)ld_f64(pb, b.dtype));
+        } else {
+          t = cmp_any(I.cmp, ld_f64(pa, a.dtype), ld_f64(pb, b.dtype));
+        }
+        if (is_null(b, rr, bit)) t = false;
+        break;
+      }
+      default: {  // integer ranges
+        const KCol& col = p.cols[I.col];
+        const long long v = ld_int(value_ptr(col, rr, bit), col.dtype);
+        t = v >= I.lo.i && v <= I.hi.i;
+        break;
+      }
+    }
+    if (I.inv) t = !t;
+    if (t && !is_null(p.cols[I.col], rr, bit)) r |= 1u << bit;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint32_t combine(int mode, uint32_t acc, uint32_t r) {
+  return mode == ESC_COMB_AND ? (acc & r) : mode == ESC_COMB_OR ? (acc | r) : r;
+}
+__device__ __forceinline__ uint32_t care_for(int mode, uint32_t acc, uint32_t care) {
+  return mode == ESC_COMB_AND ? (care & acc) : mode == ESC_COMB_OR ? (care & ~acc) : care;
+}
+
+// Evaluate the program on this lane's 4*C rows. FAST: the tile is staged and every program
+// column is in smem, so range opcodes run the smem loops; otherwise every atom takes the
+// generic per-row path.
+template <int C, bool FAST>
+__device__ __forceinline__ uint32_t eval_program(const KParams& p, const RowRef& rr, uint32_t valid) {
+  uint32_t acc = 0, care = valid;
+  uint32_t stk_acc[ESC_MAX_STACK], stk_care[ESC_MAX_STACK];
+  int sp = 0;
+  const int n = p.n_ins;
+  for (int pc = 0; pc < n; ++pc) {
+    const KInstr& I = p.ins[pc];
+    const int op = I.op;
+    uint32_t r;
+    const uint8_t* col = rr.stage + I.soff;
+    const int l0 = rr.local0;
+    switch (op) {
+      case K_PUSH:
+        stk_acc[sp] = acc;
+        stk_care[sp] = care;
+        ++sp;
+        care = care_for(I.combine, acc, care);
+        acc = 0;
+        continue;
+      case K_POP:
+        --sp;
+        acc = combine(I.combine, stk_acc[sp], acc);
+        care = stk_care[sp];
+        continue;
+      case K_NOT:
+        acc = ~acc;
+        continue;
+      case K_FALSE:
+        r = 0;
+        break;
+      case K_UDF:
+        r = atom_udf(p, I, rr, care_for(I.combine, acc, care), valid);
+        break;
+      case K_RANGE_S8:
+        r = FAST ? range_i32<int8_t, C>(col, l0, (int32_t)I.lo.i, (uint32_t)(I.hi.i - I.lo.i)) : atom_generic(p, I, rr, valid);
+        break;
+      case K_RANGE_U8:
+        r = FAST ? range_i32<uint8_t, C>(col, l0, (int32_t)I.lo.i, (uint32_t)(I.hi.i - I.lo.i)) : atom_generic(p, I, rr, valid);
+        break;
+      case K_RANGE_S16:
+        r = FAST ? range_i32<int16_t, C>(col, l0, (int32_t)I.lo.i, (uint32_t)(I.hi.i - I.lo.i)) : atom_generic(p, I, rr, valid);
+        break;
+      case K_RANGE_U16:
+        r = FAST ? range_i32<uint16_t, C>(col, l0, (int32_t)I.lo.i, (uint32_t)(I.hi.i - I.lo.i)) : atom_generic(p, I, rr, valid);
+        break;
+      case K_RANGE_S32:
+        r = FAST ? range_i32<int32_t, C>(col, l0, (int32_t)I.lo.i, (uint32_t)(I.hi.i - I.lo.i)) : atom_generic(p, I, rr, valid);
+        break;
+      case K_RANGE_S64:
+        r = FAST ? range_i64<long long, C>(col, l0, I.lo.i, (unsigned long long)I.hi.i - (unsigned long long)I.lo.i)
+                 : atom_generic(p, I, rr, valid);
+        break;
+      case K_RANGE_U32:
+        r = FAST ? range_i64<uint32_t, C>(col, l0, I.lo.i, (unsigned long long)I.hi.i - (unsigned long long)I.lo.i)
+                 : atom_generic(p, I, rr, valid);
+        break;
+      case K_RANGE_F32:
+        r = FAST ? range_f32<C>(col, l0, (float)I.lo.f, (float)I.hi.f) : atom_generic(p, I, rr, valid);
+        break;
+      case K_NOTNULL:
+        r = FAST ? (I.noff != kNoNulls ? ~null_bits_staged<C>(rr.stage + I.noff, l0) : 0xFFFFFFFFu)
+                 : atom_generic(p, I, rr, valid);
+        break;
+      default:  // K_RANGE_F64, K_LUT, K_COLCMP
+        r = atom_generic(p, I, rr, valid);
+        break;
+    }
+    if (FAST && op <= K_RANGE_F32) {
+      if (I.inv) r = ~r;
+      if (I.noff != kNoNulls) r &= ~null_bits_staged<C>(rr.stage + I.noff, l0);
+    }
+    if (I.neg) r = ~r;
+    acc = combine(I.combine, acc, r);
+  }
+  return acc & valid;
+}
+
+template <int C>
+__device__ __noinline__ uint32_t eval_direct(const KParams& p, const RowRef& rr, uint32_t valid) {
+  return eval_program<C, false>(p, rr, valid);
+}
+
+// Predicate evaluator of the ahead-of-time kernels: the opcode interpreter over a staged tile.
+// The JIT tier substitutes a generated straight-line evaluator with the same signature.
+struct InterpPred {
+  template <int C>
+  static __device__ __forceinline__ uint32_t eval(const KParams& p, const RowRef& rr, uint32_t valid) {
+    return eval_program<C, true>(p, rr, valid);
+  }
+};
+
+__device__ __forceinline__ uint32_t valid_bits(int64_t grow0, int64_t nrows, int C) {
+  uint32_t v = 0;
+  for (int c = 0; c < C; ++c)
+    for (int j = 0; j < 4; ++j) v |= (uint32_t)(grow0 + kChunkRows * c + j < nrows) << (4 * c + j);
+  return v;
+}
+
+// ------------------------------------------------------------------------------------------
+// decoupled look-back (one warp)
+// ------------------------------------------------------------------------------------------
+__device__ unsigned long long lookback_warp(unsigned long long* status, int64_t tile, unsigned long long agg,
+                                            uint32_t epoch, int lane) {
+  // the tile's aggregate (tile 0: its inclusive prefix) was published by the last consumer warp
+  const unsigned long long tag = (unsigned long long)epoch << 48;
+  if (tile == 0) return 0;
+  unsigned long long excl = 0;
+  int64_t q = tile - 1;
+  while (true) {
+    const int64_t idx = q - lane;
+    bool ok = true, pre = true;
+    unsigned long long val = 0;
+    if (idx >= 0) {
+      const unsigned long long w = ld_acquire(&status[idx]);
+      ok = (w >> 48) == epoch;
+      pre = ok && ((w >> kStatusValueBits) & 3ull) == kFlagPrefix;
+      val = w & kStatusValueMask;
+    }
+    const unsigned pm = __ballot_sync(0xFFFFFFFFu, pre);
+    const unsigned okm = __ballot_sync(0xFFFFFFFFu, ok);
+    const int first = pm ? __ffs(pm) - 1 : 31;
+    const unsigned need = first == 31 ? 0xFFFFFFFFu : ((1u << (first + 1)) - 1u);
+    if ((okm & need) != need) continue;  // a needed predecessor has not published: re-read
+    unsigned long long part = (lane <= first && idx >= 0) ? val : 0ull;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, d);
+    excl += part;
+    if (pm) break;
+    q -= 32;
+  }
+  if (lane == 0) st_release(&status[tile], tag | (kFlagPrefix << kStatusValueBits) | (excl + agg));
+  return excl;
+}
+
+// write this lane's hits of `chunk` starting at global position `pos`
+__device__ __forceinline__ void write_hits(const KParams& p, const RowRef& rr, uint32_t bits, int chunk,
+                                           unsigned long long pos) {
+  const esc_outputs_t& o = p.outs;
+  for (int j = 0; j < 4; ++j) {
+    const int bit = 4 * chunk + j;
+    if (!((bits >> bit) & 1u)) continue;
+    if ((int64_t)pos < o.capacity) {
+      for (int k = 0; k < o.n_proj; ++k) {
+        const KCol& col = p.cols[o.slot[k]];
+        const uint8_t* src = value_ptr(col, rr, bit);
+        uint8_t* dst = static_cast<uint8_t*>(o.out_values[k]) + (size_t)pos * col.width;
+        switch (col.width) {
+          case 1: *dst = *src; break;
+          case 2: *reinterpret_cast<uint16_t*>(dst) = *reinterpret_cast<const uint16_t*>(src); break;
+          case 4: *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(src); break;
+          default: *reinterpret_cast<uint64_t*>(dst) = *reinterpret_cast<const uint64_t*>(src); break;
+        }
+        if (o.out_nulls[k] != nullptr) o.out_nulls[k][pos] = is_null(col, rr, bit) ? 1 : 0;
+      }
+      if (o.out_row_ids != nullptr) o.out_row_ids[pos] = phys_row(rr, logical_row(rr, bit));
+    }
+    ++pos;
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void scatter_tile(const KParams& p, const RowRef& rr, uint32_t bits, uint32_t incl,
+                                             uint32_t packed, uint32_t wtot_packed, unsigned long long warp_base) {
+  const uint32_t excl = incl - packed;
+  uint32_t chunk_base = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if ((bits >> (4 * c)) & 0xFu) write_hits(p, rr, bits, c, warp_base + chunk_base + ((excl >> (8 * c)) & 0xFFu));
+    chunk_base += (wtot_packed >> (8 * c)) & 0xFFu;
+  }
+}
+
+__device__ __forceinline__ void finish_cta(const KParams& p, unsigned long long cta_count) {
+  if (cta_count) atomicAdd(&p.hdr->count, cta_count);
+  __threadfence();
+  const unsigned long long prev = atomicAdd(&p.hdr->done, 1ull);
+  if (prev == gridDim.x - 1) {
+    __threadfence();
+    volatile WsHeader* h = p.hdr;
+    p.result->count = h->count;
+    for (int i = 0; i < ESC_MAX_UDFS; ++i) {
+      p.result->udf_fail[i] = h->fail[i];
+      h->fail[i] = ~0ull;
+    }
+    h->count = 0;
+    h->ticket = 0;
+    h->done = 0;
+    __threadfence_system();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// the kernel
+// ------------------------------------------------------------------------------------------
+template <int C, bool COMPACT, class Pred>
+__global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int S = p.stages;
+  uint8_t* ring = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+  uint64_t* empty_bar = full_bar + kMaxStages;
+  uint64_t* agg_bar = empty_bar + kMaxStages;
+  uint64_t* pref_bar = agg_bar + kMaxStages;
+  long long* tile_of = reinterpret_cast<long long*>(pref_bar + kMaxStages);
+  unsigned long long* s_base = reinterpret_cast<unsigned long long*>(tile_of + kMaxStages);
+  unsigned long long* s_red = s_base + kMaxStages;                                  // [kConsumerWarps]
+  uint32_t* s_wtot = reinterpret_cast<uint32_t*>(s_red + kConsumerWarps);           // [kMaxStages][16]
+  uint32_t* s_woff = s_wtot + kMaxStages * kConsumerWarps;                          // [kMaxStages][16]
+  uint32_t* s_tsum = s_woff + kMaxStages * kConsumerWarps;                          // [kMaxStages]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x < kMaxStages) s_tsum[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+      mbar_init(&agg_bar[s], kConsumerWarps);
+      mbar_init(&pref_bar[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ===================== producer =====================
+    if (lane == 0) {
+      const uint64_t policy = evict_first_policy();
+      int64_t static_next = blockIdx.x;
+      int s = 0;
+      uint32_t ph = 0;
+      for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+        int64_t tile;
+        if constexpr (COMPACT) {
+          tile = (int64_t)atomicAdd(&p.hdr->ticket, 1ull);
+        } else {
+          tile = static_next;
+          static_next += gridDim.x;
+        }
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        if (tile >= p.n_tiles) {
+          tile_of[s] = -1;
+          mbar_arrive(&full_bar[s]);
+          break;
+        }
+        tile_of[s] = tile;
+        if (tile < p.n_full_tiles) {
+          mbar_arrive_expect_tx(&full_bar[s], p.stage_bytes);
+          uint8_t* dst = ring + (size_t)s * p.stage_bytes;
+          const int64_t row0 = tile * p.tile_rows;
+          for (int i = 0; i < p.ncols; ++i) {
+            const KCol& col = p.cols[i];
+            if (col.staged)
+              bulk_g2s(dst + col.smem_off, col.data + (size_t)row0 * col.width, (uint32_t)p.tile_rows * col.width,
+                       &full_bar[s], policy);
+            if (col.nulls_staged)
+              bulk_g2s(dst + col.smem_null_off, col.nulls + row0, (uint32_t)p.tile_rows, &full_bar[s], policy);
+          }
+        } else {
+          mbar_arrive(&full_bar[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  if (COMPACT && warp == 1) {
+    // ===================== look-back warp (K2) =====================
+    unsigned long long my_count = 0;
+    int s = 0;
+    uint32_t ph = 0;
+    for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+      mbar_wait(&full_bar[s], ph);
+      const int64_t tile = tile_of[s];
+      if (tile < 0) break;
+      mbar_wait(&agg_bar[s], ph);
+      const uint32_t v = lane < kConsumerWarps ? s_wtot[s * kConsumerWarps + lane] : 0u;
+      uint32_t sc = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, sc, d);
+        if (lane >= d) sc += t;
+      }
+      if (lane < kConsumerWarps) s_woff[s * kConsumerWarps + lane] = sc - v;
+      const uint32_t total = __shfl_sync(0xFFFFFFFFu, sc, 31);
+      const unsigned long long excl = lookback_warp(p.status, tile, total, p.epoch, lane);
+      my_count += total;
+      __syncwarp();
+      if (lane == 0) {
+        s_base[s] = excl;
+        mbar_arrive(&pref_bar[s]);
+      }
+    }
+    if (lane == 0) finish_cta(p, my_count);
+    return;
+  }
+
+  // ===================== consumers =====================
+  const int cw = warp - Layout<COMPACT>::kFirstConsumer;
+  const int local0 = cw * (kChunkRows * C) + 4 * lane;
+  unsigned long long my_count = 0;
+  // deferred (K2) state of the previous tile
+  bool have_prev = false;
+  int s_prev = 0;
+  uint32_t ph_prev = 0, bits_prev = 0, incl_prev = 0, packed_prev = 0, wtp_prev = 0;
+  RowRef rr_prev{};
+
+  int s = 0;
+  uint32_t ph = 0;
+  for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+    mbar_wait(&full_bar[s], ph);
+    const int64_t tile = tile_of[s];
+    RowRef rr{};
+    uint32_t bits = 0, incl = 0, packed = 0, wtp = 0;
+    if (tile >= 0) {
+      rr.stage = (tile < p.n_full_tiles) ? ring + (size_t)s * p.stage_bytes : nullptr;
+      rr.local0 = local0;
+      rr.grow0 = tile * p.tile_rows + local0;
+      rr.nrows = p.nrows;
+      rr.ids = p.row_ids;
+      if (rr.stage != nullptr && p.all_staged) {
+        bits = Pred::template eval<C>(p, rr, (4 * C == 32) ? 0xFFFFFFFFu : ((1u << (4 * C)) - 1u));
+      } else {
+        bits = eval_direct<C>(p, rr, valid_bits(rr.grow0, p.nrows, C));
+      }
+      if constexpr (!COMPACT) {
+        my_count += __popc(bits);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+      } else {
+        // per-chunk lane counts in 8-bit fields: one warp scan ranks every chunk
+#pragma unroll
+        for (int c = 0; c < C; ++c) packed |= (uint32_t)__popc((bits >> (4 * c)) & 0xFu) << (8 * c);
+        incl = packed;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+          if (lane >= d) incl += t;
+        }
+        wtp = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        uint32_t wtot = 0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) wtot += (wtp >> (8 * c)) & 0xFFu;
+        if (lane == 0) {
+          s_wtot[s * kConsumerWarps + cw] = wtot;
+          // the last warp to finish the tile publishes its aggregate right away, so successors'
+          // look-backs never wait for this CTA's look-back warp to reach the tile
+          const uint32_t now = atomicAdd(&s_tsum[s], (1u << 20) + wtot) + (1u << 20) + wtot;
+          if ((now >> 20) == kConsumerWarps) {
+            s_tsum[s] = 0;
+            const unsigned long long tag = (unsigned long long)p.epoch << 48;
+            const unsigned long long flag = tile == 0 ? kFlagPrefix : kFlagAggregate;
+            st_release(&p.status[tile], tag | (flag << kStatusValueBits) | (now & 0xFFFFFu));
+          }
+          mbar_arrive(&agg_bar[s]);
+        }
+      }
+    }
+    if constexpr (COMPACT) {
+      if (have_prev) {
+        mbar_wait(&pref_bar[s_prev], ph_prev);
+        const unsigned long long base = s_base[s_prev] + s_woff[s_prev * kConsumerWarps + cw];
+        scatter_tile<C>(p, rr_prev, bits_prev, incl_prev, packed_prev, wtp_prev, base);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s_prev]);
+      }
+      have_prev = tile >= 0;
+      s_prev = s;
+      ph_prev = ph;
+      bits_prev = bits;
+      incl_prev = incl;
+      packed_prev = packed;
+      wtp_prev = wtp;
+      rr_prev = rr;
+    }
+    if (tile < 0) break;
+  }
+
+  if constexpr (!COMPACT) {
+    // ---- CTA reduction, global accumulation, last-CTA finalisation ----
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) my_count += __shfl_down_sync(0xFFFFFFFFu, my_count, d);
+    if (lane == 0) s_red[cw] = my_count;
+    consumer_bar();
+    if (cw == 0 && lane == 0) {
+      unsigned long long tot = 0;
+      for (int w = 0; w < kConsumerWarps; ++w) tot += s_red[w];
+      finish_cta(p, tot);
+    }
+  }
+}
+
+// gather: out[i] = col[idx[i]]
+template <typename T>
+__global__ void gather_kernel(const T* __restrict__ src, const uint8_t* __restrict__ nulls,
+                              const int64_t* __restrict__ idx, int64_t n, T* __restrict__ out,
+                              uint8_t* __restrict__ out_nulls) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = __ldg(idx + i);
+    out[i] = __ldg(src + r);
+    if (out_nulls != nullptr) out_nulls[i] = nulls != nullptr ? __ldg(nulls + r) : 0;
+  }
+}
+
+}  // namespace esc

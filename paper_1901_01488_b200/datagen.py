@@ -211,3 +211,69 @@ CONFIG3_WHERE = {
 }
 CONFIG3_EDGES = [("fact", "f_datekey", "date", "d_datekey"), ("fact", "f_custkey", "customer", "c_custkey"),
                  ("fact", "f_suppkey", "supplier", "s_suppkey"), ("fact", "f_partkey", "part", "p_partkey")]
+
+
+# ---- block-seeded variants for the 600M-row benchmarks ----------------------------------------
+# The exact Appendix B recipes above draw each column from one sequential stream, which takes
+# ~2 minutes single-threaded at 600M rows and cannot be split by rank.  The benchmark therefore
+# uses the SAME per-row distributions drawn in independent blocks of BLOCK_ROWS rows, block b
+# seeded with SeedSequence([42, stream, b]): any row range (one rank's shard) is generated alone,
+# in parallel threads (numpy releases the GIL), directly into caller-provided (pinned) buffers.
+BLOCK_ROWS = 2_500_000
+
+
+def _blocked(n: int, row_begin: int, row_end: int, out: dict, fill_block, threads: int | None = None):
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    b0, b1 = row_begin // BLOCK_ROWS, (row_end + BLOCK_ROWS - 1) // BLOCK_ROWS
+
+    def work(b):
+        lo, hi = b * BLOCK_ROWS, min(n, (b + 1) * BLOCK_ROWS)
+        block = fill_block(b, hi - lo)
+        s, e = max(lo, row_begin), min(hi, row_end)
+        for name, arr in block.items():
+            out[name][s - row_begin:e - row_begin] = arr[s - lo:e - lo]
+
+    with ThreadPoolExecutor(threads or min(32, os.cpu_count() or 1)) as pool:
+        list(pool.map(work, range(b0, b1)))
+    return out
+
+
+def config4_blocked(n: int = 600_000_000, row_begin: int = 0, row_end: int | None = None,
+                    out: dict | None = None, threads: int | None = None) -> Workload:
+    row_end = n if row_end is None else row_end
+    m = row_end - row_begin
+    out = out or {k: np.empty(m, dtype=np.float32 if k == "C" else np.int32) for k in "ABCD"}
+
+    def fill(b, k):
+        g = np.random.default_rng(np.random.SeedSequence([SEED, 4, b]))
+        a = ((g.zipf(1.1, k) - 1) % 1_000_000).astype(np.int32)
+        return {"A": a, "B": (a % 1000 + g.integers(-5, 6, k)).astype(np.int32),
+                "C": g.standard_normal(k).astype(np.float32), "D": g.integers(0, 1000, k).astype(np.int32)}
+
+    _blocked(n, row_begin, row_end, out, fill, threads)
+    w = config4(8)  # predicate / projection / UDF of the config (tiny throwaway data)
+    w.columns = {"A": ("INT32", out["A"]), "B": ("INT32", out["B"]), "C": ("FLOAT32", out["C"]),
+                 "D": ("INT32", out["D"])}
+    w.note = f"block-seeded config-4 recipe, rows [{row_begin}, {row_end}) of {n}"
+    return w
+
+
+def config5_blocked(n: int = 600_000_000, s: float = 0.01, conj4: bool = False, row_begin: int = 0,
+                    row_end: int | None = None, out: dict | None = None, threads: int | None = None) -> Workload:
+    row_end = n if row_end is None else row_end
+    m = row_end - row_begin
+    out = out or {f"c{i}": np.empty(m, dtype=np.int32 if i < 4 else np.int64) for i in range(8)}
+
+    def fill(b, k):
+        g = np.random.default_rng(np.random.SeedSequence([SEED, 5, b]))
+        d = {f"c{i}": g.integers(0, 1_000_000, k).astype(np.int32) for i in range(4)}
+        d.update({f"c{i}": g.integers(0, 10**12, k).astype(np.int64) for i in range(4, 8)})
+        return d
+
+    _blocked(n, row_begin, row_end, out, fill, threads)
+    w = config5(8, s, conj4)
+    w.columns = {k: ("INT32" if int(k[1]) < 4 else "INT64", v) for k, v in out.items()}
+    w.note = f"block-seeded config-5 recipe, rows [{row_begin}, {row_end}) of {n}"
+    return w

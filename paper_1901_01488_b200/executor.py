@@ -38,6 +38,25 @@ from .udf import FAIL_MESSAGES
 
 _NO_FAIL = (1 << 64) - 1
 
+# bench/profiling hook: when a list, every kernel launch appends (start_event, end_event, kind)
+# recorded on the launching stream around the launch (before any host synchronisation)
+KERNEL_EVENTS: list | None = None
+
+
+def _ev_start(stream):
+    if KERNEL_EVENTS is None:
+        return None
+    ev = torch.cuda.Event(enable_timing=True)
+    ev.record(stream)
+    return ev
+
+
+def _ev_end(stream, ev0, kind):
+    if ev0 is not None and KERNEL_EVENTS is not None:
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1.record(stream)
+        KERNEL_EVENTS.append((ev0, ev1, kind))
+
 
 @dataclass
 class RowSelection:
@@ -82,10 +101,12 @@ def launch_count(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | 
     ws = N.workspace(table.device, stream)
     ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
     cols = cp.column_array()
+    ev0 = _ev_start(stream)
     N.check(lib.esc_scan_count(C.byref(cp.program), cols, cp.ncols, n,
                                C.c_void_p(ids.data_ptr()) if ids is not None else None,
                                C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
                                C.c_void_p(stream.cuda_stream)), "esc_scan_count")
+    _ev_end(stream, ev0, "count")
     if not sync:
         return None
     stream.synchronize()
@@ -128,10 +149,12 @@ def launch_compact(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor 
         outs.out_nulls[k] = m.data_ptr() if m is not None and capacity else None
     rows = torch.empty(capacity, dtype=torch.int64, device=dev) if want_row_ids else None
     outs.out_row_ids = rows.data_ptr() if rows is not None and capacity else None
+    ev0 = _ev_start(stream)
     N.check(lib.esc_compact(C.byref(cp.program), cols, cp.ncols + len(extra), n,
                             C.c_void_p(ids.data_ptr()) if ids is not None else None, C.byref(outs),
                             C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
                             C.c_void_p(stream.cuda_stream)), "esc_compact")
+    _ev_end(stream, ev0, "compact")
     stream.synchronize()
     count, fails = ws.read_result(cp.n_udfs)
     return count, fails, values, nulls, rows
@@ -144,8 +167,11 @@ def _contains(node, targets: set) -> bool:
     return any(id(a) in targets for a in ex.atoms(node))
 
 
-def raise_udf_errors(table: ColumnTable, cp: CompiledPredicate, fails: list, ids, n: int):
-    """Raise the ExecutionError the reference would raise for this evaluation, if any."""
+def raise_udf_errors(table: ColumnTable, cp: CompiledPredicate, fails: list, ids, n: int, count_fn=None):
+    """Raise the ExecutionError the reference would raise for this evaluation, if any.
+
+    ``count_fn(sub_predicate) -> int`` counts a sibling prefix over the slice (default: a local
+    device count; the multi-GPU path passes a global one)."""
     failing = {}
     for node_id, u in cp.udf_index.items():
         if u < len(fails) and fails[u] != _NO_FAIL:
@@ -156,6 +182,8 @@ def raise_udf_errors(table: ColumnTable, cp: CompiledPredicate, fails: list, ids
         return
 
     def count(sub) -> int:
+        if count_fn is not None:
+            return count_fn(sub)
         scp = compile_predicate(table, sub)
         c, _ = launch_count(scp, table, ids, n)
         return c
@@ -245,6 +273,33 @@ def materialize(table: ColumnTable, pred: ex.Expr, needed, count: int | None = N
     if got != count:
         raise ExecutionError(f"internal: compaction counted {got} rows, expected {count}")
     return [Column(c.name, c.kind, v, m, c.dictionary) for c, v, m in zip(proj, values, nulls)]
+
+
+def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: int):
+    """ONE fused pass: exact count + order-preserving compaction of ``needed`` bounded by
+    ``capacity`` rows.  Returns ``(count, columns)``; ``columns`` is None when the count
+    exceeds the capacity (the caller's push-down threshold rejected the table anyway).
+
+    The planner uses this for the ESC sub-query: with ``capacity = floor(max_selectivity *
+    rows)`` every table the policy would push down is fully materialised by the same scan that
+    counts it, instead of count-then-rescan (reference ``optimizer.py:317-327``)."""
+    cp = compile_predicate(table, pred)
+    ids, n = _row_ids(RowSelection(table))
+    capacity = max(0, min(int(capacity), n))
+    proj = [table.column(name) for name in needed]
+    count, fails, values, nulls, _ = launch_compact(cp, table, ids, n, proj, capacity, want_row_ids=False)
+    if cp.unbound or cp.may_fail:
+        raise_udf_errors(table, cp, fails, ids, n)
+    if count > capacity:
+        return count, None
+    out = []
+    for c, v, m in zip(proj, values, nulls):
+        if count < capacity:
+            # keep the temp table compact: copy the hits out of the capacity-sized buffer
+            v = v[:count].clone()
+            m = m[:count].clone() if m is not None else None
+        out.append(Column(c.name, c.kind, v, m, c.dictionary))
+    return count, out
 
 
 def take_column(col: Column, indices) -> Column:

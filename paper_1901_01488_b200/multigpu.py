@@ -1,0 +1,180 @@
+"""K3: row-range partitioning of a table across the GPUs of one box + the count/offset exchange.
+
+The reference's only parallelism is a row-range split (``np.linspace`` bounds,
+``executor.py:485-489``) whose fragments are concatenated in chunk order (``executor.py:500-504``).
+Here one process drives one GPU (``torch.distributed``, NCCL over NVLink/NVSwitch); rank ``r``
+holds rows ``[floor(r*N/G), floor((r+1)*N/G))`` of every table resident in its HBM.  An ESC
+sub-query runs the fused scan/count/compaction kernel on each rank's shard, then a single
+``all_gather`` of one int64 per rank yields the global count (for the push-down decision) and
+the exclusive prefix offsets that place each rank's compacted slice in the global, order-
+preserving result: the slices concatenated in rank order ARE the reference's row order.  No
+table data crosses NVLink; the sharded temp stays where it was produced.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from fractions import Fraction
+
+import torch
+import torch.distributed as dist
+
+from . import executor
+from .compiler import compile_predicate
+from .errors import EscdbError, ExecutionError, NoPredicate
+from .optimizer import EscConfig, _trivially_true, decide_pushdown
+from .storage import Column, ColumnTable
+
+_NO_FAIL = (1 << 64) - 1
+
+
+def shard_bounds(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous row range of every rank (balanced to within one row)."""
+    return [((r * n) // world, ((r + 1) * n) // world) for r in range(world)]
+
+
+def exclusive_offsets(counts) -> list[int]:
+    out, acc = [], 0
+    for c in counts:
+        out.append(acc)
+        acc += int(c)
+    return out
+
+
+def _comm_device(group=None) -> torch.device:
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def exchange_counts(local: int, group=None) -> tuple[int, list[int], list[int]]:
+    """all_gather of one int64 per rank -> (global count, per-rank counts, exclusive offsets)."""
+    world = dist.get_world_size(group)
+    dev = _comm_device(group)
+    mine = torch.tensor([int(local)], dtype=torch.int64, device=dev)
+    every = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(every, mine, group=group)
+    counts = [int(x) for x in every.cpu().tolist()]
+    return sum(counts), counts, exclusive_offsets(counts)
+
+
+def allreduce_min(values: list[int], group=None) -> list[int]:
+    """Element-wise minimum over ranks of unsigned 64-bit words (failure rows)."""
+    if not values:
+        return []
+    dev = _comm_device(group)
+    # map u64 -> i64 order-preservingly for the signed reduction
+    t = torch.tensor([v - (1 << 63) for v in values], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return [int(v) + (1 << 63) for v in t.cpu().tolist()]
+
+
+@dataclass
+class ShardedTable:
+    """One rank's slice of a row-partitioned table."""
+
+    name: str
+    local: ColumnTable
+    global_rows: int
+    row_begin: int
+    rank: int
+    world: int
+
+    @property
+    def row_end(self) -> int:
+        return self.row_begin + self.local.row_count
+
+
+@dataclass
+class ShardedDecision:
+    table: str
+    exact_count: int           # global
+    row_count: int             # global
+    selectivity: Fraction
+    qualified: bool
+    local_count: int
+    offset: int                # global position of this rank's first compacted row
+    counts: list               # per-rank counts
+    columns: list | None       # this rank's compacted slice (None when not materialized)
+
+
+def _global_replay(st: ShardedTable, cp, local_fails: list, group):
+    """UDF error semantics over the GLOBAL table: first failing row = min over ranks (global row
+    ids), short-circuit decisions from global prefix counts (all ranks walk the same tree)."""
+    shifted = [(((f >> 3) + st.row_begin) << 3) | (f & 7) if f != _NO_FAIL else _NO_FAIL for f in local_fails]
+    fails = allreduce_min(shifted, group)
+    any_unbound = bool(cp.unbound)
+    if not any_unbound and all(f == _NO_FAIL for f in fails):
+        return
+
+    class _GlobalCount:
+        def __call__(self, sub):
+            c, _ = executor.launch_count(compile_predicate(st.local, sub), st.local, None, st.local.row_count)
+            total, _, _ = exchange_counts(c, group)
+            return total
+
+    executor.raise_udf_errors(st.local, cp, fails, None, st.global_rows, count_fn=_GlobalCount())
+
+
+def sharded_esc_subquery(st: ShardedTable, predicate, needed, config: EscConfig, group=None) -> ShardedDecision:
+    """The fused ESC step on every rank's shard + one count exchange."""
+    if predicate is None or _trivially_true(predicate):
+        raise NoPredicate(f"table {st.name!r} has no filtering predicate")
+    rc = st.global_rows
+    fused = config.materialize and rc > 0 and rc >= config.min_table_size
+    cp = compile_predicate(st.local, predicate)
+    n = st.local.row_count
+    try:
+        if fused:
+            cap = min(n, math.floor(Fraction(config.max_selectivity) * rc))
+            proj = [st.local.column(c) for c in needed]
+            local, fails, values, nulls, _ = executor.launch_compact(cp, st.local, None, n, proj, cap, False)
+        else:
+            (local, fails), values, nulls, proj, cap = executor.launch_count(cp, st.local, None, n), [], [], [], 0
+        if cp.unbound or cp.may_fail:
+            _global_replay(st, cp, fails, group)
+    except EscdbError as exc:
+        raise ExecutionError(f"count sub-query on {st.name!r} failed: {exc}") from exc
+    total, counts, offsets = exchange_counts(local, group)
+    qualified = decide_pushdown(rc, total, config)
+    cols = None
+    if qualified and config.materialize:
+        cols = []
+        for c, v, m in zip(proj, values, nulls):
+            v = v[:local].clone() if local < cap else v
+            m = (m[:local].clone() if local < cap else m) if m is not None else None
+            cols.append(Column(c.name, c.kind, v, m, c.dictionary))
+    return ShardedDecision(st.name, total, rc, Fraction(total, rc) if rc else Fraction(0), qualified,
+                           local, offsets[st.rank], counts, cols)
+
+
+def gather_to_rank0(cols: list, counts: list, group=None) -> list | None:
+    """Optional: assemble the global, order-preserving temp on rank 0 (rank-order concatenation
+    of the slices) — used by tests; the planner keeps temps sharded."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    out = []
+    for c in cols:
+        pieces = [torch.empty(counts[r], dtype=c.values.dtype, device=c.values.device) for r in range(world)]
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather(pieces, c.values.contiguous(), group=group) if len(set(counts)) == 1 else \
+                _ragged_gather(pieces, c.values, counts, group)
+        else:
+            _ragged_gather(pieces, c.values, counts, group)
+        if rank == 0:
+            out.append(torch.cat(pieces))
+    return out if rank == 0 else None
+
+
+def _ragged_gather(pieces, mine, counts, group):
+    """all_gather for unequal lengths: pad to the max count, then trim."""
+    m = max(counts) if counts else 0
+    dev = mine.device
+    padded = torch.zeros(m, dtype=mine.dtype, device=dev)
+    padded[: mine.numel()] = mine
+    bufs = [torch.empty(m, dtype=mine.dtype, device=dev) for _ in counts]
+    dist.all_gather(bufs, padded, group=group)
+    for r, b in enumerate(bufs):
+        pieces[r].copy_(b[: counts[r]])

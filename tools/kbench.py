@@ -1,0 +1,47 @@
+"""Kernel tuning micro-benchmark (not part of the product): device-generated tables, CUDA-event
+timing of the ESC kernels for a few predicate shapes.  Usage: python tools/kbench.py [rows]."""
+import json, os, statistics, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1901_01488_b200 import ColumnTable, count_star, executor, expr as ex
+from paper_1901_01488_b200.storage import Column, parse_kind
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 300_000_000
+dev = torch.device("cuda", 0)
+g = torch.Generator(device=dev); g.manual_seed(1)
+A = torch.randint(1, 1000, (n,), generator=g, device=dev, dtype=torch.int32)
+A[torch.rand(n, generator=g, device=dev) < 0.095] = 0   # config 4: A = x holds for ~9.5% (Zipf mode)
+B = torch.randint(-5, 1005, (n,), generator=g, device=dev, dtype=torch.int32)
+Cc = torch.randn(n, generator=g, device=dev, dtype=torch.float32)
+D = torch.randint(0, 1000, (n,), generator=g, device=dev, dtype=torch.int32)
+t = ColumnTable("t", [Column("A", parse_kind("INT32"), A), Column("B", parse_kind("INT32"), B),
+                      Column("C", parse_kind("FLOAT32"), Cc), Column("D", parse_kind("INT32"), D)])
+r = lambda c: ex.ColumnRef("t", c)
+preds = {
+    "notnull4": ex.And((ex.FoldedAtom(r("A"), True), ex.FoldedAtom(r("B"), True), ex.FoldedAtom(r("C"), True), ex.FoldedAtom(r("D"), True))),
+    "range1": ex.Range(r("A"), 100, 199),
+    "config4": ex.And((ex.Equality(r("A"), 0), ex.Range(r("C"), -0.5, 1.0),
+                       ex.Or((ex.Equality(r("D"), 17), ex.Comparison(r("D"), ">", 900))),
+                       ex.FnCall("b3d", (r("B"), r("D")), ">", 3.0, lambda b, d: (b * 3.0 + d) % 7.0))),
+}
+out = {}
+for name, p in preds.items():
+    width = {"notnull4": 16, "range1": 4, "config4": 16}[name]
+    for _ in range(2):
+        k = count_star(t, p)
+    executor.KERNEL_EVENTS = []
+    for _ in range(5):
+        count_star(t, p)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b, _ in executor.KERNEL_EVENTS)
+    res = {"count_ms": round(ms, 3), "count_GBps": round(n * width / ms / 1e6, 1)}
+    cap = max(k, 1)
+    executor.KERNEL_EVENTS = []
+    for _ in range(5):
+        executor.count_and_materialize(t, p, ["A"], cap)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b, _ in executor.KERNEL_EVENTS)
+    executor.KERNEL_EVENTS = None
+    res.update(compact_ms=round(ms, 3), compact_GBps=round((n * width + k * 4) / ms / 1e6, 1), k=k)
+    out[name] = res
+print(json.dumps({"rows": n, "env": {k: v for k, v in os.environ.items() if k.startswith("ESC_")}, "res": out}))
