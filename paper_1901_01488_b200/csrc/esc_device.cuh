@@ -10,7 +10,10 @@
 namespace esc {
 
 
-constexpr int kConsumerWarps = 16;
+#ifndef ESC_CONSUMER_WARPS
+#define ESC_CONSUMER_WARPS 8
+#endif
+constexpr int kConsumerWarps = ESC_CONSUMER_WARPS;
 constexpr int kChunkRows = 128;  // one warp chunk: 32 lanes x 4 consecutive rows
 constexpr int kMaxStages = 8;
 constexpr uint32_t kSmemBudget = 200 * 1024;  // dynamic smem for the stage ring
@@ -22,7 +25,8 @@ constexpr uint32_t kNoNulls = 0xFFFFFFFFu;
 
 template <bool COMPACT>
 struct Layout {
-  static constexpr int kFirstConsumer = COMPACT ? 2 : 1;
+  static constexpr int kWriters = COMPACT ? kMaxStages : 0;  // K2: one look-back / copy-out warp per ring slot
+  static constexpr int kFirstConsumer = 1 + kWriters;
   static constexpr int kThreads = (kFirstConsumer + kConsumerWarps) * 32;
 };
 
@@ -79,7 +83,8 @@ struct KParams {
   int32_t chunks;       // C
   int32_t tile_rows;    // T = kConsumerWarps * 128 * C
   int32_t stages;
-  uint32_t stage_bytes;
+  uint32_t stage_bytes;  // stage stride
+  uint32_t tma_bytes;    // bytes the bulk copies deliver per stage (expect_tx)
   uint32_t epoch;
   int32_t all_staged;   // every column the program reads is staged (fast evaluator usable)
   int64_t nrows;
@@ -90,6 +95,13 @@ struct KParams {
   unsigned long long* status;
   esc_result_t* result;
   esc_outputs_t outs;
+  // K2 fast tiles: every projection is compacted per warp into a stage region, then copied out
+  uint32_t proj_off[ESC_MAX_PROJ];   // stage offset of projection k's compacted values
+  uint32_t proj_noff[ESC_MAX_PROJ];  // stage offset of its compacted null bytes
+  uint8_t proj_mode[ESC_MAX_PROJ];   // values: 0 compact in place, 1 gather hits from HBM, 2 alias
+  uint8_t proj_nmode[ESC_MAX_PROJ];  // nulls:  0 in place, 1 gather, 2 alias, 3 none (write zeros)
+  int32_t all_fast;      // full tiles use the fast (writer copy-out) path
+  uint32_t rows_off;     // stage offset of the u16 row-index scratch (row-id outputs)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -585,74 +597,158 @@ __device__ __forceinline__ uint32_t valid_bits(int64_t grow0, int64_t nrows, int
 // ------------------------------------------------------------------------------------------
 // decoupled look-back (one warp)
 // ------------------------------------------------------------------------------------------
+// Relaxed loads suffice: the status word itself is the only datum read, and it carries its own
+// epoch/flag/value; relaxed (unlike acquire) loads of the window pipeline.
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ unsigned long long lookback_warp(unsigned long long* status, int64_t tile, unsigned long long agg,
                                             uint32_t epoch, int lane) {
   // the tile's aggregate (tile 0: its inclusive prefix) was published by the last consumer warp
   const unsigned long long tag = (unsigned long long)epoch << 48;
   if (tile == 0) return 0;
+  constexpr int J = 8;  // 8 x 32 predecessors in flight per round trip
   unsigned long long excl = 0;
   int64_t q = tile - 1;
   while (true) {
-    const int64_t idx = q - lane;
-    bool ok = true, pre = true;
-    unsigned long long val = 0;
-    if (idx >= 0) {
-      const unsigned long long w = ld_acquire(&status[idx]);
-      ok = (w >> 48) == epoch;
-      pre = ok && ((w >> kStatusValueBits) & 3ull) == kFlagPrefix;
-      val = w & kStatusValueMask;
-    }
-    const unsigned pm = __ballot_sync(0xFFFFFFFFu, pre);
-    const unsigned okm = __ballot_sync(0xFFFFFFFFu, ok);
-    const int first = pm ? __ffs(pm) - 1 : 31;
-    const unsigned need = first == 31 ? 0xFFFFFFFFu : ((1u << (first + 1)) - 1u);
-    if ((okm & need) != need) continue;  // a needed predecessor has not published: re-read
-    unsigned long long part = (lane <= first && idx >= 0) ? val : 0ull;
+    unsigned long long w[J];
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, d);
-    excl += part;
-    if (pm) break;
-    q -= 32;
+    for (int j = 0; j < J; ++j) {
+      const int64_t idx = q - 32 * j - lane;
+      w[j] = idx >= 0 ? ld_relaxed(&status[idx]) : 0ull;
+    }
+    int consumed = 0;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (done || consumed != j) break;
+      const int64_t idx = q - 32 * j - lane;
+      const bool ok = idx < 0 || (w[j] >> 48) == epoch;
+      const bool pre = idx < 0 || (ok && ((w[j] >> kStatusValueBits) & 3ull) == kFlagPrefix);
+      const unsigned pm = __ballot_sync(0xFFFFFFFFu, pre);
+      const unsigned okm = __ballot_sync(0xFFFFFFFFu, ok);
+      const int first = pm ? __ffs(pm) - 1 : 31;
+      const unsigned need = first == 31 ? 0xFFFFFFFFu : ((1u << (first + 1)) - 1u);
+      if ((okm & need) != need) break;  // a needed predecessor has not published: re-read from here
+      unsigned long long part = (lane <= first && idx >= 0) ? (w[j] & kStatusValueMask) : 0ull;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, d);
+      excl += part;
+      if (pm) done = true;
+      ++consumed;
+    }
+    if (done) break;
+    q -= 32 * consumed;
   }
   if (lane == 0) st_release(&status[tile], tag | (kFlagPrefix << kStatusValueBits) | (excl + agg));
   return excl;
 }
 
-// write this lane's hits of `chunk` starting at global position `pos`
-__device__ __forceinline__ void write_hits(const KParams& p, const RowRef& rr, uint32_t bits, int chunk,
-                                           unsigned long long pos) {
+// ---- scatter of one warp's hits (the warp's rows of a tile, ascending row order) -------------
+// Output order inside a warp segment is chunk-major, then lane, then row: a lane's hits of chunk c
+// start at chunk_base(c) + lane_excl(c) (both from the packed per-chunk scan).
+
+// one value column / null column, direct per-lane stores (non-staged columns, tail tiles)
+template <int C>
+__device__ __forceinline__ void scatter_direct(const KParams& p, const RowRef& rr, uint32_t bits, uint32_t excl,
+                                               uint32_t wtp, unsigned long long base, int k) {
   const esc_outputs_t& o = p.outs;
-  for (int j = 0; j < 4; ++j) {
-    const int bit = 4 * chunk + j;
-    if (!((bits >> bit) & 1u)) continue;
-    if ((int64_t)pos < o.capacity) {
-      for (int k = 0; k < o.n_proj; ++k) {
-        const KCol& col = p.cols[o.slot[k]];
+  const KCol& col = p.cols[o.slot[k]];
+  uint8_t* out = static_cast<uint8_t*>(o.out_values[k]);
+  uint8_t* onull = o.out_nulls[k];
+  uint32_t cb = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    unsigned long long pos = base + cb + ((excl >> (8 * c)) & 0xFFu);
+    cb += (wtp >> (8 * c)) & 0xFFu;
+    uint32_t m = (bits >> (4 * c)) & 0xFu;
+    while (m) {
+      const int bit = 4 * c + __ffs(m) - 1;
+      m &= m - 1;
+      if ((int64_t)pos < o.capacity) {
         const uint8_t* src = value_ptr(col, rr, bit);
-        uint8_t* dst = static_cast<uint8_t*>(o.out_values[k]) + (size_t)pos * col.width;
+        uint8_t* dst = out + (size_t)pos * col.width;
         switch (col.width) {
           case 1: *dst = *src; break;
           case 2: *reinterpret_cast<uint16_t*>(dst) = *reinterpret_cast<const uint16_t*>(src); break;
           case 4: *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(src); break;
-          default: *reinterpret_cast<uint64_t*>(dst) = *reinterpret_cast<const uint64_t*>(src); break;
+          default: *reinterpret_cast<unsigned long long*>(dst) = *reinterpret_cast<const unsigned long long*>(src); break;
         }
-        if (o.out_nulls[k] != nullptr) o.out_nulls[k][pos] = is_null(col, rr, bit) ? 1 : 0;
+        if (onull != nullptr) onull[pos] = is_null(col, rr, bit) ? 1 : 0;
       }
-      if (o.out_row_ids != nullptr) o.out_row_ids[pos] = phys_row(rr, logical_row(rr, bit));
+      ++pos;
     }
-    ++pos;
+  }
+}
+
+// hits of a column that is not staged: read just the hit rows from HBM into compacted slots
+template <typename T, int C>
+__device__ __forceinline__ void gather_compact(const uint8_t* data, int64_t grow0, uint8_t* seg, uint32_t bits,
+                                               uint32_t excl, uint32_t wtp) {
+  const T* src = reinterpret_cast<const T*>(data);
+  T* cs = reinterpret_cast<T*>(seg);
+  uint32_t cb = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);
+    cb += (wtp >> (8 * c)) & 0xFFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((bits >> (4 * c + j)) & 1u) cs[r++] = __ldg(src + grow0 + kChunkRows * c + j);
+  }
+}
+
+// phases 1+2 only: the warp's hits end up contiguous at the start of its segment
+template <typename T, int C>
+__device__ __forceinline__ void compact_inplace(uint8_t* seg, int lane, uint32_t bits, uint32_t excl, uint32_t wtp) {
+  T v[4 * C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    T t[4];
+    lds4<T>(seg + (size_t)(kChunkRows * c + 4 * lane) * sizeof(T), t);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[4 * c + j] = t[j];
+  }
+  __syncwarp();
+  T* cs = reinterpret_cast<T*>(seg);
+  uint32_t cb = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);
+    cb += (wtp >> (8 * c)) & 0xFFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((bits >> (4 * c + j)) & 1u) cs[r++] = v[4 * c + j];
   }
 }
 
 template <int C>
 __device__ __forceinline__ void scatter_tile(const KParams& p, const RowRef& rr, uint32_t bits, uint32_t incl,
-                                             uint32_t packed, uint32_t wtot_packed, unsigned long long warp_base) {
+                                             uint32_t packed, uint32_t wtp, unsigned long long base) {
+  const esc_outputs_t& o = p.outs;
   const uint32_t excl = incl - packed;
-  uint32_t chunk_base = 0;
+  uint32_t wtot = 0;
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if ((bits >> (4 * c)) & 0xFu) write_hits(p, rr, bits, c, warp_base + chunk_base + ((excl >> (8 * c)) & 0xFFu));
-    chunk_base += (wtot_packed >> (8 * c)) & 0xFFu;
+  for (int c = 0; c < C; ++c) wtot += (wtp >> (8 * c)) & 0xFFu;
+  if (wtot == 0) return;
+  for (int k = 0; k < o.n_proj; ++k) scatter_direct<C>(p, rr, bits, excl, wtp, base, k);
+  if (o.out_row_ids != nullptr) {
+    uint32_t cb = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      unsigned long long pos = base + cb + ((excl >> (8 * c)) & 0xFFu);
+      cb += (wtp >> (8 * c)) & 0xFFu;
+      uint32_t m = (bits >> (4 * c)) & 0xFu;
+      while (m) {
+        const int bit = 4 * c + __ffs(m) - 1;
+        m &= m - 1;
+        if ((int64_t)pos < o.capacity) o.out_row_ids[pos] = phys_row(rr, logical_row(rr, bit));
+        ++pos;
+      }
+    }
   }
 }
 
@@ -690,18 +786,23 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
   long long* tile_of = reinterpret_cast<long long*>(pref_bar + kMaxStages);
   unsigned long long* s_base = reinterpret_cast<unsigned long long*>(tile_of + kMaxStages);
   unsigned long long* s_red = s_base + kMaxStages;                                  // [kConsumerWarps]
-  uint32_t* s_wtot = reinterpret_cast<uint32_t*>(s_red + kConsumerWarps);           // [kMaxStages][16]
-  uint32_t* s_woff = s_wtot + kMaxStages * kConsumerWarps;                          // [kMaxStages][16]
+  uint32_t* s_wtot = reinterpret_cast<uint32_t*>(s_red + kConsumerWarps);           // [kMaxStages][NW]
+  uint32_t* s_woff = s_wtot + kMaxStages * kConsumerWarps;                          // [kMaxStages][NW]
   uint32_t* s_tsum = s_woff + kMaxStages * kConsumerWarps;                          // [kMaxStages]
+  uint32_t* s_writers_done = s_tsum + kMaxStages;                                   // [1]
+  unsigned long long* s_cta_count = reinterpret_cast<unsigned long long*>(s_writers_done + 2);  // [1]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  constexpr int kW = Layout<COMPACT>::kWriters;
 
   if (threadIdx.x < kMaxStages) s_tsum[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
+    *s_writers_done = 0;
+    *s_cta_count = 0;
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kConsumerWarps);
+      mbar_init(&empty_bar[s], kConsumerWarps + (COMPACT ? 1 : 0));
       mbar_init(&agg_bar[s], kConsumerWarps);
       mbar_init(&pref_bar[s], 1);
     }
@@ -713,26 +814,26 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
     // ===================== producer =====================
     if (lane == 0) {
       const uint64_t policy = evict_first_policy();
-      int64_t static_next = blockIdx.x;
+      // static round-robin schedule: round r of every CTA covers tiles [r*G, (r+1)*G), so a
+      // tile's look-back predecessors are evaluated concurrently in the same round (K2 is a
+      // cooperative launch: every CTA is resident, no look-back waits on an unscheduled CTA)
+      int64_t tile = blockIdx.x;
       int s = 0;
       uint32_t ph = 0;
+      int sentinels = 0;
       for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
-        int64_t tile;
-        if constexpr (COMPACT) {
-          tile = (int64_t)atomicAdd(&p.hdr->ticket, 1ull);
-        } else {
-          tile = static_next;
-          static_next += gridDim.x;
-        }
         mbar_wait(&empty_bar[s], ph ^ 1u);
         if (tile >= p.n_tiles) {
+          // K2: one end marker per ring slot (each slot has its own writer warp); consumers stop
+          // at the first
           tile_of[s] = -1;
           mbar_arrive(&full_bar[s]);
-          break;
+          if (++sentinels >= (kW > 0 ? S : 1)) break;
+          continue;
         }
         tile_of[s] = tile;
         if (tile < p.n_full_tiles) {
-          mbar_arrive_expect_tx(&full_bar[s], p.stage_bytes);
+          mbar_arrive_expect_tx(&full_bar[s], p.tma_bytes);
           uint8_t* dst = ring + (size_t)s * p.stage_bytes;
           const int64_t row0 = tile * p.tile_rows;
           for (int i = 0; i < p.ncols; ++i) {
@@ -746,17 +847,24 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
         } else {
           mbar_arrive(&full_bar[s]);
         }
+        tile += gridDim.x;
       }
     }
     return;
   }
 
-  if (COMPACT && warp == 1) {
-    // ===================== look-back warp (K2) =====================
+  if (COMPACT && warp <= kW) {
+    // ===================== writer warps (K2) =====================
+    // writer w owns ring slot w and meets its phases in order; per tile: warp offsets, decoupled
+    // look-back, then either the coalesced copy-out of the consumers' compacted rows (fast tiles)
+    // or handing the global base to the consumers (tail / selection tiles).  One writer per slot
+    // keeps up to S look-backs in flight per SM.
+    const int w = warp - 1;
     unsigned long long my_count = 0;
-    int s = 0;
-    uint32_t ph = 0;
-    for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+    if (w < S) {
+    for (int64_t k = w;; k += S) {
+      const int s = w;
+      const uint32_t ph = (uint32_t)((k / S) & 1);
       mbar_wait(&full_bar[s], ph);
       const int64_t tile = tile_of[s];
       if (tile < 0) break;
@@ -768,17 +876,70 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
         const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, sc, d);
         if (lane >= d) sc += t;
       }
-      if (lane < kConsumerWarps) s_woff[s * kConsumerWarps + lane] = sc - v;
+      const uint32_t woff = sc - v;
       const uint32_t total = __shfl_sync(0xFFFFFFFFu, sc, 31);
       const unsigned long long excl = lookback_warp(p.status, tile, total, p.epoch, lane);
       my_count += total;
+      const bool fast = tile < p.n_full_tiles && p.all_fast;
+      if (fast && total > 0) {
+        const esc_outputs_t& o = p.outs;
+        const uint8_t* stage = ring + (size_t)s * p.stage_bytes;
+        for (int w2 = 0; w2 < kConsumerWarps; ++w2) {
+          const uint32_t n = __shfl_sync(0xFFFFFFFFu, v, w2);
+          if (n == 0) continue;
+          const unsigned long long base = excl + __shfl_sync(0xFFFFFFFFu, woff, w2);
+          const int seg_row = w2 * kChunkRows * C;
+          const long long cap = o.capacity;
+          for (int kk = 0; kk < o.n_proj; ++kk) {
+            const KCol& col = p.cols[o.slot[kk]];
+            const uint8_t* src = stage + p.proj_off[kk] + (size_t)seg_row * col.width;
+            uint8_t* dst = static_cast<uint8_t*>(o.out_values[kk]);
+            switch (col.width) {
+              case 1:
+                for (uint32_t e = lane; e < n; e += 32) if ((long long)(base + e) < cap) dst[base + e] = src[e];
+                break;
+              case 2:
+                for (uint32_t e = lane; e < n; e += 32)
+                  if ((long long)(base + e) < cap) reinterpret_cast<uint16_t*>(dst)[base + e] = reinterpret_cast<const uint16_t*>(src)[e];
+                break;
+              case 4:
+                for (uint32_t e = lane; e < n; e += 32)
+                  if ((long long)(base + e) < cap) reinterpret_cast<uint32_t*>(dst)[base + e] = reinterpret_cast<const uint32_t*>(src)[e];
+                break;
+              default:
+                for (uint32_t e = lane; e < n; e += 32)
+                  if ((long long)(base + e) < cap)
+                    reinterpret_cast<unsigned long long*>(dst)[base + e] = reinterpret_cast<const unsigned long long*>(src)[e];
+                break;
+            }
+            if (o.out_nulls[kk] != nullptr) {
+              const uint8_t* nsrc = p.proj_nmode[kk] == 3 ? nullptr : stage + p.proj_noff[kk] + seg_row;
+              for (uint32_t e = lane; e < n; e += 32)
+                if ((long long)(base + e) < cap) o.out_nulls[kk][base + e] = nsrc ? nsrc[e] : 0;
+            }
+          }
+          if (o.out_row_ids != nullptr) {
+            const uint16_t* rs = reinterpret_cast<const uint16_t*>(stage + p.rows_off) + seg_row;
+            for (uint32_t e = lane; e < n; e += 32)
+              if ((long long)(base + e) < cap) o.out_row_ids[base + e] = tile * p.tile_rows + rs[e];
+          }
+        }
+      }
+      if (lane < kConsumerWarps) s_woff[s * kConsumerWarps + lane] = woff;
       __syncwarp();
       if (lane == 0) {
         s_base[s] = excl;
         mbar_arrive(&pref_bar[s]);
+        mbar_arrive(&empty_bar[s]);
       }
     }
-    if (lane == 0) finish_cta(p, my_count);
+    }
+    if (w < S && lane == 0) {
+      atomicAdd(s_cta_count, my_count);
+      __threadfence_block();
+      if (atomicAdd(s_writers_done, 1u) == (uint32_t)(S - 1))
+        finish_cta(p, *reinterpret_cast<volatile unsigned long long*>(s_cta_count));
+    }
     return;
   }
 
@@ -786,81 +947,109 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
   const int cw = warp - Layout<COMPACT>::kFirstConsumer;
   const int local0 = cw * (kChunkRows * C) + 4 * lane;
   unsigned long long my_count = 0;
-  // deferred (K2) state of the previous tile
-  bool have_prev = false;
-  int s_prev = 0;
-  uint32_t ph_prev = 0, bits_prev = 0, incl_prev = 0, packed_prev = 0, wtp_prev = 0;
-  RowRef rr_prev{};
-
   int s = 0;
   uint32_t ph = 0;
   for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
     mbar_wait(&full_bar[s], ph);
     const int64_t tile = tile_of[s];
-    RowRef rr{};
-    uint32_t bits = 0, incl = 0, packed = 0, wtp = 0;
-    if (tile >= 0) {
-      rr.stage = (tile < p.n_full_tiles) ? ring + (size_t)s * p.stage_bytes : nullptr;
-      rr.local0 = local0;
-      rr.grow0 = tile * p.tile_rows + local0;
-      rr.nrows = p.nrows;
-      rr.ids = p.row_ids;
-      if (rr.stage != nullptr && p.all_staged) {
-        bits = Pred::template eval<C>(p, rr, (4 * C == 32) ? 0xFFFFFFFFu : ((1u << (4 * C)) - 1u));
-      } else {
-        bits = eval_direct<C>(p, rr, valid_bits(rr.grow0, p.nrows, C));
-      }
-      if constexpr (!COMPACT) {
-        my_count += __popc(bits);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[s]);
-      } else {
-        // per-chunk lane counts in 8-bit fields: one warp scan ranks every chunk
-#pragma unroll
-        for (int c = 0; c < C; ++c) packed |= (uint32_t)__popc((bits >> (4 * c)) & 0xFu) << (8 * c);
-        incl = packed;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-          if (lane >= d) incl += t;
-        }
-        wtp = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        uint32_t wtot = 0;
-#pragma unroll
-        for (int c = 0; c < C; ++c) wtot += (wtp >> (8 * c)) & 0xFFu;
-        if (lane == 0) {
-          s_wtot[s * kConsumerWarps + cw] = wtot;
-          // the last warp to finish the tile publishes its aggregate right away, so successors'
-          // look-backs never wait for this CTA's look-back warp to reach the tile
-          const uint32_t now = atomicAdd(&s_tsum[s], (1u << 20) + wtot) + (1u << 20) + wtot;
-          if ((now >> 20) == kConsumerWarps) {
-            s_tsum[s] = 0;
-            const unsigned long long tag = (unsigned long long)p.epoch << 48;
-            const unsigned long long flag = tile == 0 ? kFlagPrefix : kFlagAggregate;
-            st_release(&p.status[tile], tag | (flag << kStatusValueBits) | (now & 0xFFFFFu));
-          }
-          mbar_arrive(&agg_bar[s]);
-        }
-      }
-    }
-    if constexpr (COMPACT) {
-      if (have_prev) {
-        mbar_wait(&pref_bar[s_prev], ph_prev);
-        const unsigned long long base = s_base[s_prev] + s_woff[s_prev * kConsumerWarps + cw];
-        scatter_tile<C>(p, rr_prev, bits_prev, incl_prev, packed_prev, wtp_prev, base);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[s_prev]);
-      }
-      have_prev = tile >= 0;
-      s_prev = s;
-      ph_prev = ph;
-      bits_prev = bits;
-      incl_prev = incl;
-      packed_prev = packed;
-      wtp_prev = wtp;
-      rr_prev = rr;
-    }
     if (tile < 0) break;
+    RowRef rr;
+    rr.stage = (tile < p.n_full_tiles) ? ring + (size_t)s * p.stage_bytes : nullptr;
+    rr.local0 = local0;
+    rr.grow0 = tile * p.tile_rows + local0;
+    rr.nrows = p.nrows;
+    rr.ids = p.row_ids;
+    uint32_t bits;
+    if (rr.stage != nullptr && p.all_staged) {
+      bits = Pred::template eval<C>(p, rr, (4 * C == 32) ? 0xFFFFFFFFu : ((1u << (4 * C)) - 1u));
+    } else {
+      bits = eval_direct<C>(p, rr, valid_bits(rr.grow0, p.nrows, C));
+    }
+    if constexpr (!COMPACT) {
+      my_count += __popc(bits);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    } else {
+      // per-chunk lane counts in 8-bit fields: one warp scan ranks every chunk
+      uint32_t packed = 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) packed |= (uint32_t)__popc((bits >> (4 * c)) & 0xFu) << (8 * c);
+      uint32_t incl = packed;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const uint32_t wtp = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const uint32_t excl = incl - packed;
+      uint32_t wtot = 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) wtot += (wtp >> (8 * c)) & 0xFFu;
+      const bool fast = rr.stage != nullptr && p.all_fast;
+      if (fast && wtot > 0) {
+        // compact this warp's hits inside its own smem segments; a writer warp copies them out
+        const int seg_row = local0 - 4 * lane;
+        const esc_outputs_t& o = p.outs;
+        uint8_t* stage = const_cast<uint8_t*>(rr.stage);
+        for (int kk = 0; kk < o.n_proj; ++kk) {
+          const KCol& col = p.cols[o.slot[kk]];
+          uint8_t* seg = stage + p.proj_off[kk] + (size_t)seg_row * col.width;
+          if (p.proj_mode[kk] == 0) {
+            switch (col.width) {
+              case 1: compact_inplace<uint8_t, C>(seg, lane, bits, excl, wtp); break;
+              case 2: compact_inplace<uint16_t, C>(seg, lane, bits, excl, wtp); break;
+              case 4: compact_inplace<uint32_t, C>(seg, lane, bits, excl, wtp); break;
+              default: compact_inplace<unsigned long long, C>(seg, lane, bits, excl, wtp); break;
+            }
+          } else if (p.proj_mode[kk] == 1) {
+            switch (col.width) {
+              case 1: gather_compact<uint8_t, C>(col.data, rr.grow0, seg, bits, excl, wtp); break;
+              case 2: gather_compact<uint16_t, C>(col.data, rr.grow0, seg, bits, excl, wtp); break;
+              case 4: gather_compact<uint32_t, C>(col.data, rr.grow0, seg, bits, excl, wtp); break;
+              default: gather_compact<unsigned long long, C>(col.data, rr.grow0, seg, bits, excl, wtp); break;
+            }
+          }
+          if (p.proj_nmode[kk] == 0)
+            compact_inplace<uint8_t, C>(stage + p.proj_noff[kk] + seg_row, lane, bits, excl, wtp);
+          else if (p.proj_nmode[kk] == 1)
+            gather_compact<uint8_t, C>(col.nulls, rr.grow0, stage + p.proj_noff[kk] + seg_row, bits, excl, wtp);
+        }
+        if (o.out_row_ids != nullptr) {
+          uint16_t* rs = reinterpret_cast<uint16_t*>(stage + p.rows_off) + seg_row;
+          uint32_t cb = 0;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);
+            cb += (wtp >> (8 * c)) & 0xFFu;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if ((bits >> (4 * c + j)) & 1u) rs[r++] = (uint16_t)(local0 + kChunkRows * c + j);
+          }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        s_wtot[s * kConsumerWarps + cw] = wtot;
+        // the last warp to finish the tile publishes its aggregate right away, so successors'
+        // look-backs never wait for this CTA's writer warp to reach the tile
+        const uint32_t now = atomicAdd(&s_tsum[s], (1u << 20) + wtot) + (1u << 20) + wtot;
+        if ((now >> 20) == kConsumerWarps) {
+          s_tsum[s] = 0;
+          const unsigned long long tag = (unsigned long long)p.epoch << 48;
+          const unsigned long long flag = tile == 0 ? kFlagPrefix : kFlagAggregate;
+          st_release(&p.status[tile], tag | (flag << kStatusValueBits) | (now & 0xFFFFFu));
+        }
+        mbar_arrive(&agg_bar[s]);
+      }
+      if (!fast) {
+        // tail / selection / non-staged projections: scatter directly once the base is known
+        mbar_wait(&pref_bar[s], ph);
+        const unsigned long long base = s_base[s] + s_woff[s * kConsumerWarps + cw];
+        if (wtot > 0) scatter_tile<C>(p, rr, bits, incl, packed, wtp, base);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
   }
 
   if constexpr (!COMPACT) {

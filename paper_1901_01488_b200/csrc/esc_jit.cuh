@@ -429,9 +429,10 @@ cudaKernel_t get_kernel(const KParams& kp, bool compact, size_t smem, std::strin
     e.log = "nvrtcCreateProgram failed";
   } else {
     nv.add_name(prog, inst.c_str());
+    const std::string warps = "-DESC_CONSUMER_WARPS=" + std::to_string(kConsumerWarps);
     const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-fmad=false", "-lineinfo",
-                          "--device-as-default-execution-space", "-DESC_JIT=1"};
-    const nvrtcResult rc = nv.compile(prog, 6, opts);
+                          "--device-as-default-execution-space", "-DESC_JIT=1", warps.c_str()};
+    const nvrtcResult rc = nv.compile(prog, 7, opts);
     size_t ls = 0;
     nv.log_size(prog, &ls);
     std::string log(ls, '\0');

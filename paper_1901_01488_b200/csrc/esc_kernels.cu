@@ -284,7 +284,8 @@ struct Geometry {
   int chunks = 1;
   int tile_rows = 0;
   int stages = 0;
-  uint32_t stage_bytes = 0;
+  uint32_t stage_bytes = 0;  // stage stride (TMA data + compaction regions)
+  uint32_t tma_bytes = 0;    // bytes the producer's bulk copies deliver per stage
 };
 
 uint64_t program_slots(const esc_program_t* prog) {
@@ -305,10 +306,13 @@ uint64_t program_slots(const esc_program_t* prog) {
   return m;
 }
 
-// Which columns are staged, and the tile geometry: the largest C whose stage ring still has
-// `min_stages` stages in the smem budget (K2 holds one extra stage for its deferred scatter).
+// Which columns are staged, the compaction regions, and the tile geometry: the largest C whose
+// stage ring still has `min_stages` stages in the smem budget.  For K2 (outs != nullptr) every
+// projection gets a per-stage region its warps compact hits into (in place for staged columns,
+// scratch filled by gathering only the hit rows otherwise) + a u16 row-index scratch for row-id
+// outputs; the stage count is a multiple of the writer-warp count.
 Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_t* cols, int32_t ncols,
-                       bool gather, int64_t nrows, int min_stages) {
+                       bool gather, int64_t nrows, int min_stages, const esc_outputs_t* outs) {
   Geometry g;
   const uint64_t used = program_slots(prog);
   uint32_t per_row = 0;
@@ -319,16 +323,40 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     c.nulls_staged = want && !gather && c.nulls != nullptr && (reinterpret_cast<uintptr_t>(c.nulls) % 16 == 0);
     per_row += (c.staged ? c.width : 0) + (c.nulls_staged ? 1 : 0);
   }
+  // compaction regions (bytes per row of scratch)
+  uint32_t scratch_row = 0;
+  const bool compact = outs != nullptr && !gather;
+  if (compact) {
+    for (int k = 0; k < outs->n_proj; ++k) {
+      int first = k;
+      for (int j = 0; j < k; ++j)
+        if (outs->slot[j] == outs->slot[k]) { first = j; break; }
+      const KCol& c = kp.cols[outs->slot[k]];
+      kp.proj_mode[k] = first != k ? 2 : (c.staged ? 0 : 1);
+      if (kp.proj_mode[k] == 1) scratch_row += c.width;
+      if (outs->out_nulls[k] == nullptr || c.nulls == nullptr) kp.proj_nmode[k] = 3;
+      else if (first != k) kp.proj_nmode[k] = 2;
+      else if (c.nulls_staged) kp.proj_nmode[k] = 0;
+      else { kp.proj_nmode[k] = 1; scratch_row += 1; }
+    }
+    if (outs->out_row_ids != nullptr) scratch_row += 2;
+  }
   int chunks = 4;
-  while (chunks > 1 && (uint64_t)kConsumerWarps * kChunkRows * chunks * per_row * min_stages > kSmemBudget)
+  while (chunks > 1 &&
+         (uint64_t)kConsumerWarps * kChunkRows * chunks * (per_row + scratch_row) * min_stages > kSmemBudget)
     chunks >>= 1;
   if (const char* e = getenv("ESC_CHUNKS")) {  // tuning override (experiments only)
     const int v = atoi(e);
     if (v == 1 || v == 2 || v == 4) chunks = v;
   }
   const int tile_rows = kConsumerWarps * kChunkRows * chunks;
+  bool fast = compact;
+  if (fast && (uint64_t)tile_rows * (per_row + scratch_row) * 2 > kSmemBudget) {
+    fast = false;  // compaction regions do not fit: consumers scatter directly (slow path)
+    scratch_row = 0;
+  }
   // if even C=1 cannot hold two stages, drop columns from staging (largest first)
-  while ((uint64_t)tile_rows * per_row * 2 > kSmemBudget) {
+  while ((uint64_t)tile_rows * (per_row + scratch_row) * 2 > kSmemBudget) {
     int best = -1;
     for (int i = 0; i < ncols; ++i)
       if (kp.cols[i].staged && (best < 0 || kp.cols[i].width > kp.cols[best].width)) best = i;
@@ -339,6 +367,7 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
       kp.cols[best].nulls_staged = 0;
       per_row -= 1;
     }
+    fast = false;
   }
   g.chunks = chunks;
   g.tile_rows = tile_rows;
@@ -348,10 +377,35 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     if (c.staged) { c.smem_off = off; off += (uint32_t)tile_rows * c.width; }
     if (c.nulls_staged) { c.smem_null_off = off; off += (uint32_t)tile_rows; }
   }
+  const uint32_t tma_bytes = off;  // what the producer's bulk copies fill per stage
+  if (fast) {
+    for (int k = 0; k < outs->n_proj; ++k) {
+      const KCol& c = kp.cols[outs->slot[k]];
+      int first = k;
+      for (int j = 0; j < k; ++j)
+        if (outs->slot[j] == outs->slot[k]) { first = j; break; }
+      if (kp.proj_mode[k] == 0) kp.proj_off[k] = c.smem_off;
+      else if (kp.proj_mode[k] == 1) { kp.proj_off[k] = off; off += (uint32_t)tile_rows * c.width; }
+      else kp.proj_off[k] = kp.proj_off[first];
+      if (kp.proj_nmode[k] == 0) kp.proj_noff[k] = c.smem_null_off;
+      else if (kp.proj_nmode[k] == 1) { kp.proj_noff[k] = off; off += (uint32_t)tile_rows; }
+      else if (kp.proj_nmode[k] == 2) kp.proj_noff[k] = kp.proj_noff[first];
+    }
+    if (outs->out_row_ids != nullptr) {
+      off = (off + 15u) & ~15u;
+      kp.rows_off = off;
+      off += (uint32_t)tile_rows * 2;
+    }
+    off = (off + 127u) & ~127u;
+  }
+  kp.all_fast = fast ? 1 : 0;
   g.stage_bytes = off;
-  if (off == 0 || nrows < tile_rows) {
+  g.tma_bytes = tma_bytes;
+  if (tma_bytes == 0 || nrows < tile_rows) {
     g.stages = 2;  // nothing staged (or no full tile): the ring only carries tile ids
     g.stage_bytes = 0;
+    g.tma_bytes = 0;
+    kp.all_fast = 0;
     for (int i = 0; i < ncols; ++i) kp.cols[i].staged = kp.cols[i].nulls_staged = 0;
   } else {
     g.stages = (int)(kSmemBudget / off);
@@ -362,11 +416,13 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     }
     if (g.stages < 1) g.stages = 1;
   }
+  if (outs != nullptr && g.stages < 2) g.stages = 2;  // K2 holds a stage for its writer warp
   return g;
 }
 
 int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
-                 const int64_t* row_ids, void* d_ws, size_t ws_bytes, esc_result_t* result, bool compact) {
+                 const int64_t* row_ids, void* d_ws, size_t ws_bytes, esc_result_t* result,
+                 const esc_outputs_t* outs) {
   if (ncols < 0 || ncols > ESC_MAX_COLS) return fail(ESC_ERR_INVALID, "ncols out of range");
   if (nrows < 0) return fail(ESC_ERR_INVALID, "negative nrows");
   if (nrows >= (1ll << kStatusValueBits)) return fail(ESC_ERR_INVALID, "nrows exceeds 2^46");
@@ -389,13 +445,23 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
   kp.ncols = ncols;
   kp.nrows = nrows;
   kp.row_ids = row_ids;
-  const Geometry g = plan_geometry(kp, prog, cols, ncols, row_ids != nullptr, nrows, 3);
+  if (outs != nullptr) {
+    if (outs->n_proj < 0 || outs->n_proj > ESC_MAX_PROJ) return fail(ESC_ERR_INVALID, "n_proj out of range");
+    if (outs->capacity < 0) return fail(ESC_ERR_INVALID, "negative capacity");
+    for (int k = 0; k < outs->n_proj; ++k) {
+      if (outs->slot[k] < 0 || outs->slot[k] >= ncols) return fail(ESC_ERR_INVALID, "projection slot out of range");
+      if (outs->out_values[k] == nullptr && outs->capacity > 0) return fail(ESC_ERR_INVALID, "null output buffer");
+    }
+    kp.outs = *outs;
+  }
+  const Geometry g = plan_geometry(kp, prog, cols, ncols, row_ids != nullptr, nrows, 3, outs);
   kp.chunks = g.chunks;
   kp.tile_rows = g.tile_rows;
   kp.stages = g.stages;
   kp.stage_bytes = g.stage_bytes;
+  kp.tma_bytes = g.tma_bytes;
   kp.n_tiles = (nrows + g.tile_rows - 1) / g.tile_rows;
-  kp.n_full_tiles = (g.stage_bytes == 0) ? 0 : nrows / g.tile_rows;
+  kp.n_full_tiles = (g.tma_bytes == 0) ? 0 : nrows / g.tile_rows;
   rc = lower_program(prog, kp);
   if (rc != ESC_OK) return rc;
   // smem offsets into the lowered instructions; fast evaluation needs every program column staged
@@ -443,8 +509,17 @@ int launch_c(const KParams& kp, cudaStream_t stream) {
       cudaKernel_t k = jit::get_kernel(kp, COMPACT, smem, &why);
       if (k != nullptr) {
         void* args[] = {const_cast<KParams*>(&kp)};
-        cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3((unsigned)grid),
-                                         dim3(Layout<COMPACT>::kThreads), args, smem, stream);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(Layout<COMPACT>::kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = COMPACT ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), args);
         if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("JIT kernel launch: ") + cudaGetErrorString(e));
         return ESC_OK;
       }
@@ -453,8 +528,14 @@ int launch_c(const KParams& kp, cudaStream_t stream) {
   auto kern = esc_scan_kernel<C, COMPACT, InterpPred>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  kern<<<(unsigned)grid, Layout<COMPACT>::kThreads, smem, stream>>>(kp);
-  e = cudaGetLastError();
+  if (COMPACT) {  // cooperative: all CTAs co-resident (the static-schedule look-back relies on it)
+    void* args[] = {const_cast<KParams*>(&kp)};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid),
+                                    dim3(Layout<COMPACT>::kThreads), args, smem, stream);
+  } else {
+    kern<<<(unsigned)grid, Layout<COMPACT>::kThreads, smem, stream>>>(kp);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return ESC_OK;
 }
@@ -496,7 +577,7 @@ int esc_workspace_init(void* d_ws, size_t ws_bytes, void* stream) {
 int esc_scan_count(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
                    const int64_t* d_row_ids, esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream) {
   static thread_local KParams kp;
-  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, false);
+  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, nullptr);
   if (rc != ESC_OK) return rc;
   return launch<false>(kp, static_cast<cudaStream_t>(stream));
 }
@@ -505,16 +586,9 @@ int esc_compact(const esc_program_t* prog, const esc_column_t* cols, int32_t nco
                 const int64_t* d_row_ids, const esc_outputs_t* outs, esc_result_t* result, void* d_ws,
                 size_t ws_bytes, void* stream) {
   static thread_local KParams kp;
-  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, true);
-  if (rc != ESC_OK) return rc;
   if (outs == nullptr) return fail(ESC_ERR_INVALID, "null outputs");
-  if (outs->n_proj < 0 || outs->n_proj > ESC_MAX_PROJ) return fail(ESC_ERR_INVALID, "n_proj out of range");
-  if (outs->capacity < 0) return fail(ESC_ERR_INVALID, "negative capacity");
-  for (int k = 0; k < outs->n_proj; ++k) {
-    if (outs->slot[k] < 0 || outs->slot[k] >= ncols) return fail(ESC_ERR_INVALID, "projection slot out of range");
-    if (outs->out_values[k] == nullptr && outs->capacity > 0) return fail(ESC_ERR_INVALID, "null output buffer");
-  }
-  kp.outs = *outs;
+  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, outs);
+  if (rc != ESC_OK) return rc;
   {
     std::lock_guard<std::mutex> g(g_epoch_mu);
     uint32_t& ep = g_epochs[d_ws];
@@ -618,7 +692,7 @@ int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t n
     kp.cols[i].dtype = cols[i].dtype;
     kp.cols[i].width = dtype_width(cols[i].dtype);
   }
-  return plan_geometry(kp, prog, cols, ncols, false, 1ll << 40, 3).tile_rows;
+  return plan_geometry(kp, prog, cols, ncols, false, 1ll << 40, 3, nullptr).tile_rows;
 }
 
 }  // extern "C"
