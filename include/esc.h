@@ -212,12 +212,42 @@ int esc_scan_count(const esc_program_t* prog, const esc_column_t* cols, int32_t 
                    int64_t nrows, const int64_t* d_row_ids, esc_result_t* result,
                    void* d_ws, size_t ws_bytes, void* stream);
 
-/* Fused predicate + exact count + order-preserving compaction of the projected columns
- * (single pass, decoupled look-back).  replaces executor.eval_predicate (executor.py:202-215)
- * and optimizer.materialize_pushdown (optimizer.py:180-194). */
+/* Predicate + exact count + order-preserving compaction of the projected columns (and/or the
+ * physical row ids of the hits).  replaces executor.eval_predicate (executor.py:202-215) and
+ * optimizer.materialize_pushdown (optimizer.py:180-194).  Runs esc_scan_select into the
+ * workspace, then esc_materialize_selection.  Rows beyond outs->capacity are counted, not
+ * written. */
 int esc_compact(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols,
                 int64_t nrows, const int64_t* d_row_ids, const esc_outputs_t* outs,
                 esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream);
+
+/* The same result in ONE pass over the predicate columns: tiles are ranked with a
+ * decoupled look-back over per-tile status words (a writer warp per smem stage) and copied
+ * out coalesced.  Bit-identical to esc_compact; on B200 the cross-CTA look-back latency makes it
+ * slower than the selection path for persistent grids, so it is not the default. */
+int esc_compact_onepass(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols,
+                        int64_t nrows, const int64_t* d_row_ids, const esc_outputs_t* outs,
+                        esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Upper bounds of the selection buffers esc_scan_select fills for `nrows` rows. */
+int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_tiles);
+
+/* The count sub-query that also RECORDS its selection: bit i of d_bitmap[i/32] = logical row i
+ * qualifies; d_tile_counts[t] = qualifying rows of tile t (of *tile_rows rows).  Costs N/8 bytes
+ * of writes on top of esc_scan_count; materialisation then never re-evaluates the predicate
+ * (the reference re-scans: optimizer.py:191). */
+int esc_scan_select(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols,
+                    int64_t nrows, const int64_t* d_row_ids, uint32_t* d_bitmap,
+                    uint32_t* d_tile_counts, int32_t* tile_rows, esc_result_t* result,
+                    void* d_ws, size_t ws_bytes, void* stream);
+
+/* Order-preserving compaction of the rows a selection marks: per-tile offsets by a scan of the
+ * tile counts, then every warp maps one row per lane of a bitmap word (contiguous reads of the
+ * projected columns' hit rows, contiguous writes).  cols[outs->slot[k]] is projection k. */
+int esc_materialize_selection(const uint32_t* d_bitmap, const uint32_t* d_tile_counts,
+                              int64_t nrows, int32_t tile_rows, const esc_column_t* cols,
+                              int32_t ncols, const int64_t* d_row_ids, const esc_outputs_t* outs,
+                              void* d_ws, size_t ws_bytes, void* stream);
 
 /* out[i] = col[idx[i]] (values and, when present, nulls).  replaces Column.take
  * (storage.py:176-184). */

@@ -93,6 +93,16 @@ _SIGNATURES = {
     "esc_compact": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32, C.c_int64,
                               C.c_void_p, C.POINTER(EscOutputs), C.c_void_p, C.c_void_p, C.c_size_t,
                               C.c_void_p]),
+    "esc_compact_onepass": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32, C.c_int64,
+                                      C.c_void_p, C.POINTER(EscOutputs), C.c_void_p, C.c_void_p, C.c_size_t,
+                                      C.c_void_p]),
+    "esc_selection_sizes": (C.c_int, [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "esc_scan_select": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32, C.c_int64, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p,
+                                  C.c_size_t, C.c_void_p]),
+    "esc_materialize_selection": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(EscColumn),
+                                            C.c_int32, C.c_void_p, C.POINTER(EscOutputs), C.c_void_p,
+                                            C.c_size_t, C.c_void_p]),
     "esc_gather": (C.c_int, [C.POINTER(EscColumn), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                              C.c_void_p]),
     "esc_last_error": (C.c_char_p, []),

@@ -101,6 +101,8 @@ struct KParams {
   uint8_t proj_mode[ESC_MAX_PROJ];   // values: 0 compact in place, 1 gather hits from HBM, 2 alias
   uint8_t proj_nmode[ESC_MAX_PROJ];  // nulls:  0 in place, 1 gather, 2 alias, 3 none (write zeros)
   int32_t all_fast;      // full tiles use the fast (writer copy-out) path
+  uint32_t* sel_bitmap;       // K1 selection output: bit i of word i/32 = logical row i qualifies
+  uint32_t* sel_tile_counts;  // K1 selection output: qualifying rows per tile
   uint32_t rows_off;     // stage offset of the u16 row-index scratch (row-id outputs)
 };
 
@@ -966,7 +968,30 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
       bits = eval_direct<C>(p, rr, valid_bits(rr.grow0, p.nrows, C));
     }
     if constexpr (!COMPACT) {
-      my_count += __popc(bits);
+      const uint32_t pc = __popc(bits);
+      my_count += pc;
+      if (p.sel_bitmap != nullptr) {
+        // 8 lanes x 4 rows of a chunk = one 32-row bitmap word (row-linear order)
+        const int64_t word0 = tile * (p.tile_rows / 32) + cw * (4 * C) + (lane >> 3);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          uint32_t v = ((bits >> (4 * c)) & 0xFu) << (4 * (lane & 7));
+          v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+          v |= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+          v |= __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+          if ((lane & 7) == 0) p.sel_bitmap[word0 + 4 * c] = v;
+        }
+        uint32_t wsum = pc;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) wsum += __shfl_xor_sync(0xFFFFFFFFu, wsum, d);
+        if (lane == 0) {
+          const uint32_t now = atomicAdd(&s_tsum[s], (1u << 20) + wsum) + (1u << 20) + wsum;
+          if ((now >> 20) == kConsumerWarps) {
+            s_tsum[s] = 0;
+            p.sel_tile_counts[tile] = now & 0xFFFFFu;
+          }
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     } else {
@@ -1062,6 +1087,211 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
       unsigned long long tot = 0;
       for (int w = 0; w < kConsumerWarps; ++w) tot += s_red[w];
       finish_cta(p, tot);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// selection -> order-preserving compaction (no cross-CTA dependency: offsets come from a scan of
+// the per-tile counts the scan kernel recorded)
+// ------------------------------------------------------------------------------------------
+constexpr int kScanThreads = 1024;
+constexpr int kScanSeg = 4 * kScanThreads;  // tiles per scan block
+
+// block-wide exclusive scan of one value per thread; returns the exclusive prefix, *total set
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* sh,
+                                                             unsigned long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    unsigned long long x = lane < nw ? sh[lane] : 0ull, y = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, y, d);
+      if (lane >= d) y += t;
+    }
+    if (lane < nw) sh[lane] = y - x;
+    if (lane == 31) sh[32] = y;
+  }
+  __syncthreads();
+  const unsigned long long r = sh[warp] + incl - v;
+  *total = sh[32];
+  __syncthreads();
+  return r;
+}
+
+// partial sums of kScanSeg-tile segments
+__global__ void __launch_bounds__(kScanThreads) tile_scan_partials(const uint32_t* __restrict__ counts, int64_t n,
+                                                                   unsigned long long* __restrict__ partial) {
+  __shared__ unsigned long long sh[33];
+  const int64_t base = (int64_t)blockIdx.x * kScanSeg + 4 * threadIdx.x;
+  unsigned long long v = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v += (base + j < n) ? counts[base + j] : 0u;
+  unsigned long long total;
+  block_excl_scan(v, sh, &total);
+  if (threadIdx.x == 0) partial[blockIdx.x] = total;
+}
+
+// exclusive offsets of every tile (carry from the earlier segments' partial sums)
+__global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* __restrict__ counts, int64_t n,
+                                                                const unsigned long long* __restrict__ partial,
+                                                                unsigned long long* __restrict__ offsets) {
+  __shared__ unsigned long long sh[33];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) {
+    unsigned long long c = 0;
+    for (unsigned b = 0; b < blockIdx.x; ++b) c += partial[b];
+    carry = c;
+  }
+  const int64_t base = (int64_t)blockIdx.x * kScanSeg + 4 * threadIdx.x;
+  uint32_t x[4];
+  unsigned long long v = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    x[j] = (base + j < n) ? counts[base + j] : 0u;
+    v += x[j];
+  }
+  unsigned long long total;
+  unsigned long long e = block_excl_scan(v, sh, &total) + carry;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (base + j < n) offsets[base + j] = e;
+    e += x[j];
+  }
+}
+
+struct SelParams {
+  const uint32_t* bitmap;
+  const uint32_t* tile_counts;
+  const unsigned long long* tile_offsets;
+  const int64_t* row_ids;  // logical -> physical rows (selection chaining) or nullptr
+  int64_t nrows;
+  int64_t n_tiles;
+  int32_t tile_rows;
+  int32_t n_proj;
+  KCol cols[ESC_MAX_PROJ];  // projected columns (data, nulls, width)
+  esc_outputs_t outs;
+};
+
+constexpr int kSelWarps = 8;
+
+template <typename T>
+__device__ __forceinline__ void sel_copy4(const KCol& col, uint8_t* out, const bool (&hit)[4],
+                                          const int64_t (&prow)[4], const unsigned long long (&pos)[4], long long cap) {
+  const T* src = reinterpret_cast<const T*>(col.data);
+  T* dst = reinterpret_cast<T*>(out);
+  T v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = hit[u] ? __ldg(src + prow[u]) : T(0);  // 4 loads in flight
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (hit[u] && (long long)pos[u] < cap) dst[pos[u]] = v[u];
+}
+
+// One tile per WARP (no block synchronisation): lane l loads bitmap word l of each 32-word
+// group; words are then walked four at a time, every word mapping one row per lane, so the
+// projected columns are read and the outputs written contiguously across the warp.
+__global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int W = p.tile_rows / 32;  // bitmap words per tile (a multiple of 32)
+  const long long cap = p.outs.capacity;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int64_t tile = gwarp; tile < p.n_tiles; tile += nwarps) {
+    if (p.tile_counts[tile] == 0) continue;
+    unsigned long long pos0 = p.tile_offsets[tile];
+    const int64_t wbase = tile * W;
+    for (int i0 = 0; i0 < W; i0 += 32) {
+      const uint32_t mine = p.bitmap[wbase + i0 + lane];
+      uint32_t nz = __ballot_sync(0xFFFFFFFFu, mine != 0);
+      if (nz == 0) continue;
+      if (__popc(nz) <= 8) {
+        // sparse: visit only the non-empty words
+        const uint32_t before = __popc(mine);
+        uint32_t excl = before;  // exclusive prefix of popc over words < lane
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, excl, d);
+          if (lane >= d) excl += t;
+        }
+        excl -= before;
+        const uint32_t group_total = __shfl_sync(0xFFFFFFFFu, excl + before, 31);
+        while (nz) {
+          const int i = __ffs(nz) - 1;
+          nz &= nz - 1;
+          const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, i);
+          const unsigned long long pos = pos0 + __shfl_sync(0xFFFFFFFFu, excl, i) + __popc(word & lt);
+          if (!((word >> lane) & 1u) || (long long)pos >= cap) continue;
+          const int64_t row = (wbase + i0 + i) * 32 + lane;
+          const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
+          for (int k = 0; k < p.n_proj; ++k) {
+            const KCol& col = p.cols[k];
+            const uint8_t* src = col.data + (size_t)prow * col.width;
+            uint8_t* dst = static_cast<uint8_t*>(p.outs.out_values[k]) + (size_t)pos * col.width;
+            switch (col.width) {
+              case 1: *dst = __ldg(src); break;
+              case 2: *reinterpret_cast<uint16_t*>(dst) = __ldg(reinterpret_cast<const uint16_t*>(src)); break;
+              case 4: *reinterpret_cast<uint32_t*>(dst) = __ldg(reinterpret_cast<const uint32_t*>(src)); break;
+              default:
+                *reinterpret_cast<unsigned long long*>(dst) = __ldg(reinterpret_cast<const unsigned long long*>(src));
+                break;
+            }
+            if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
+          }
+          if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
+        }
+        pos0 += group_total;
+        continue;
+      }
+#pragma unroll 1
+      for (int g = 0; g < 32; g += 4) {
+        uint32_t wd[4];
+        bool hit[4];
+        unsigned long long pos[4];
+        int64_t prow[4];
+        uint32_t any = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          wd[u] = __shfl_sync(0xFFFFFFFFu, mine, g + u);
+          any |= wd[u];
+          hit[u] = (wd[u] >> lane) & 1u;
+          pos[u] = pos0 + __popc(wd[u] & lt);
+          pos0 += __popc(wd[u]);
+          const int64_t row = (wbase + i0 + g + u) * 32 + lane;
+          prow[u] = (hit[u] && p.row_ids) ? __ldg(p.row_ids + row) : row;
+        }
+        if (any == 0) continue;
+        for (int k = 0; k < p.n_proj; ++k) {
+          const KCol& col = p.cols[k];
+          uint8_t* out = static_cast<uint8_t*>(p.outs.out_values[k]);
+          switch (col.width) {
+            case 1: sel_copy4<uint8_t>(col, out, hit, prow, pos, cap); break;
+            case 2: sel_copy4<uint16_t>(col, out, hit, prow, pos, cap); break;
+            case 4: sel_copy4<uint32_t>(col, out, hit, prow, pos, cap); break;
+            default: sel_copy4<unsigned long long>(col, out, hit, prow, pos, cap); break;
+          }
+          if (p.outs.out_nulls[k] != nullptr) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (hit[u] && (long long)pos[u] < cap) p.outs.out_nulls[k][pos[u]] = col.nulls ? __ldg(col.nulls + prow[u]) : 0;
+          }
+        }
+        if (p.outs.out_row_ids != nullptr) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (hit[u] && (long long)pos[u] < cap) p.outs.out_row_ids[pos[u]] = prow[u];
+        }
+      }
     }
   }
 }

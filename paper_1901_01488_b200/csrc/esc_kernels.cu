@@ -107,6 +107,30 @@ size_t status_words(int64_t nrows) {
   return (size_t)((nrows + t - 1) / t) + 1;
 }
 
+// Workspace layout: [header][tile status (one-pass K2)][tile offsets u64][scan partials u64]
+//                   [tile counts u32][selection bitmap u32]
+struct WsLayout {
+  size_t status, offsets, partials, counts, bitmap, total;
+  int64_t max_tiles, bitmap_words;
+};
+WsLayout ws_layout(int64_t nrows) {
+  WsLayout L;
+  if (nrows < 0) nrows = 0;
+  const int64_t t_min = (int64_t)kConsumerWarps * kChunkRows;        // smallest tile (C = 1)
+  const int64_t t_max = 4 * t_min;                                   // largest tile (C = 4)
+  L.max_tiles = (nrows + t_min - 1) / t_min + 1;
+  L.bitmap_words = ((nrows + t_max - 1) / t_max + 1) * (t_max / 32);  // covers every C's last tile
+  const int64_t segs = L.max_tiles / kScanSeg + 2;
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  L.status = sizeof(WsHeader);
+  L.offsets = up(L.status + status_words(nrows) * 8);
+  L.partials = up(L.offsets + (size_t)L.max_tiles * 8);
+  L.counts = up(L.partials + (size_t)segs * 8);
+  L.bitmap = up(L.counts + (size_t)L.max_tiles * 4);
+  L.total = up(L.bitmap + (size_t)L.bitmap_words * 4);
+  return L;
+}
+
 int validate_program(const esc_program_t* prog, int32_t ncols) {
   if (prog == nullptr) return fail(ESC_ERR_INVALID, "null program");
   if (prog->abi_version != ESC_ABI_VERSION) return fail(ESC_ERR_INVALID, "program ABI version mismatch");
@@ -556,9 +580,13 @@ int launch(const KParams& kp, cudaStream_t stream) {
 // ==========================================================================================
 extern "C" {
 
-size_t esc_workspace_bytes(int64_t nrows) {
-  if (nrows < 0) nrows = 0;
-  return sizeof(WsHeader) + status_words(nrows) * sizeof(unsigned long long);
+size_t esc_workspace_bytes(int64_t nrows) { return ws_layout(nrows).total; }
+
+int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_tiles) {
+  const WsLayout L = ws_layout(nrows);
+  if (bitmap_words) *bitmap_words = L.bitmap_words;
+  if (max_tiles) *max_tiles = L.max_tiles;
+  return ESC_OK;
 }
 
 int esc_workspace_init(void* d_ws, size_t ws_bytes, void* stream) {
@@ -582,9 +610,92 @@ int esc_scan_count(const esc_program_t* prog, const esc_column_t* cols, int32_t 
   return launch<false>(kp, static_cast<cudaStream_t>(stream));
 }
 
+int esc_scan_select(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
+                    const int64_t* d_row_ids, uint32_t* d_bitmap, uint32_t* d_tile_counts, int32_t* tile_rows,
+                    esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream) {
+  static thread_local KParams kp;
+  if (d_bitmap == nullptr || d_tile_counts == nullptr || tile_rows == nullptr)
+    return fail(ESC_ERR_INVALID, "null selection output");
+  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, nullptr);
+  if (rc != ESC_OK) return rc;
+  kp.sel_bitmap = d_bitmap;
+  kp.sel_tile_counts = d_tile_counts;
+  *tile_rows = kp.tile_rows;
+  return launch<false>(kp, static_cast<cudaStream_t>(stream));
+}
+
+int esc_materialize_selection(const uint32_t* d_bitmap, const uint32_t* d_tile_counts, int64_t nrows,
+                              int32_t tile_rows, const esc_column_t* cols, int32_t ncols, const int64_t* d_row_ids,
+                              const esc_outputs_t* outs, void* d_ws, size_t ws_bytes, void* stream) {
+  static thread_local SelParams sp;
+  if (d_bitmap == nullptr || d_tile_counts == nullptr || outs == nullptr)
+    return fail(ESC_ERR_INVALID, "null selection argument");
+  if (nrows < 0 || ncols < 0 || ncols > ESC_MAX_COLS) return fail(ESC_ERR_INVALID, "bad sizes");
+  if (tile_rows <= 0 || tile_rows % 1024 != 0) return fail(ESC_ERR_INVALID, "tile_rows must come from esc_scan_select");
+  if (outs->n_proj < 0 || outs->n_proj > ESC_MAX_PROJ || outs->capacity < 0)
+    return fail(ESC_ERR_INVALID, "bad outputs");
+  const WsLayout L = ws_layout(nrows);
+  if (d_ws == nullptr || ws_bytes < L.total) return fail(ESC_ERR_WORKSPACE, "workspace too small");
+  std::memset(&sp, 0, sizeof(sp));
+  sp.bitmap = d_bitmap;
+  sp.tile_counts = d_tile_counts;
+  sp.row_ids = d_row_ids;
+  sp.nrows = nrows;
+  sp.tile_rows = tile_rows;
+  sp.n_tiles = (nrows + tile_rows - 1) / tile_rows;
+  sp.n_proj = outs->n_proj;
+  for (int k = 0; k < outs->n_proj; ++k) {
+    if (outs->slot[k] < 0 || outs->slot[k] >= ncols) return fail(ESC_ERR_INVALID, "projection slot out of range");
+    const esc_column_t& c = cols[outs->slot[k]];
+    const int w = dtype_width(c.dtype);
+    if (w == 0) return fail(ESC_ERR_INVALID, "bad column dtype");
+    if (outs->out_values[k] == nullptr && outs->capacity > 0) return fail(ESC_ERR_INVALID, "null output buffer");
+    sp.cols[k].data = static_cast<const uint8_t*>(c.data);
+    sp.cols[k].nulls = c.nulls;
+    sp.cols[k].dtype = c.dtype;
+    sp.cols[k].width = w;
+  }
+  sp.outs = *outs;
+  if (sp.n_tiles == 0) return ESC_OK;
+  uint8_t* ws = static_cast<uint8_t*>(d_ws);
+  unsigned long long* offsets = reinterpret_cast<unsigned long long*>(ws + L.offsets);
+  unsigned long long* partials = reinterpret_cast<unsigned long long*>(ws + L.partials);
+  sp.tile_offsets = offsets;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned segs = (unsigned)((sp.n_tiles + kScanSeg - 1) / kScanSeg);
+  if (segs > 1) tile_scan_partials<<<segs, kScanThreads, 0, st>>>(d_tile_counts, sp.n_tiles, partials);
+  tile_scan_apply<<<segs, kScanThreads, 0, st>>>(d_tile_counts, sp.n_tiles, partials, offsets);
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  const int64_t want = (sp.n_tiles + kSelWarps - 1) / kSelWarps;  // one warp per tile
+  const int64_t grid = want < (int64_t)sms * 16 ? want : (int64_t)sms * 16;
+  sel_compact_kernel<<<(unsigned)grid, kSelWarps * 32, 0, st>>>(sp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("selection compaction launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
 int esc_compact(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
                 const int64_t* d_row_ids, const esc_outputs_t* outs, esc_result_t* result, void* d_ws,
                 size_t ws_bytes, void* stream) {
+  // K1 with selection outputs into the workspace, then the bitmap compaction (no look-back)
+  if (outs == nullptr) return fail(ESC_ERR_INVALID, "null outputs");
+  const WsLayout L = ws_layout(nrows);
+  if (d_ws == nullptr || ws_bytes < L.total) return fail(ESC_ERR_WORKSPACE, "workspace too small");
+  uint8_t* ws = static_cast<uint8_t*>(d_ws);
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(ws + L.bitmap);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.counts);
+  int32_t tile_rows = 0;
+  int rc = esc_scan_select(prog, cols, ncols, nrows, d_row_ids, bitmap, counts, &tile_rows, result, d_ws, ws_bytes,
+                           stream);
+  if (rc != ESC_OK) return rc;
+  return esc_materialize_selection(bitmap, counts, nrows, tile_rows, cols, ncols, d_row_ids, outs, d_ws, ws_bytes,
+                                   stream);
+}
+
+int esc_compact_onepass(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
+                        const int64_t* d_row_ids, const esc_outputs_t* outs, esc_result_t* result, void* d_ws,
+                        size_t ws_bytes, void* stream) {
   static thread_local KParams kp;
   if (outs == nullptr) return fail(ESC_ERR_INVALID, "null outputs");
   int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, outs);

@@ -113,10 +113,89 @@ def launch_count(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | 
     return ws.read_result(cp.n_udfs)
 
 
+@dataclass
+class Selection:
+    """What the count sub-query recorded on the device: a bitmap over the slice's logical rows
+    and the qualifying rows per tile — enough to materialise without re-evaluating."""
+
+    table: ColumnTable
+    count: int
+    bitmap: torch.Tensor
+    tile_counts: torch.Tensor
+    tile_rows: int
+    nrows: int
+    ids: torch.Tensor | None
+
+
+def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int):
+    """K1 + selection outputs; returns (count, [udf fail words], Selection)."""
+    lib = N.load_library()
+    stream = _stream(table.device)
+    ws = N.workspace(table.device, stream)
+    ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
+    words, tiles = C.c_int64(), C.c_int64()
+    lib.esc_selection_sizes(n, C.byref(words), C.byref(tiles))
+    bitmap = torch.empty(max(words.value, 1), dtype=torch.int32, device=table.device)
+    counts = torch.empty(max(tiles.value, 1), dtype=torch.int32, device=table.device)
+    tile_rows = C.c_int32()
+    cols = cp.column_array()
+    ev0 = _ev_start(stream)
+    N.check(lib.esc_scan_select(C.byref(cp.program), cols, cp.ncols, n,
+                                C.c_void_p(ids.data_ptr()) if ids is not None else None,
+                                C.c_void_p(bitmap.data_ptr()), C.c_void_p(counts.data_ptr()), C.byref(tile_rows),
+                                C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
+                                C.c_void_p(stream.cuda_stream)), "esc_scan_select")
+    _ev_end(stream, ev0, "select")
+    stream.synchronize()
+    count, fails = ws.read_result(cp.n_udfs)
+    return count, fails, Selection(table, count, bitmap, counts, int(tile_rows.value), n, ids)
+
+
+def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int, want_row_ids: bool):
+    """Order-preserving compaction of the selected rows of ``proj_cols`` (and/or their physical
+    row ids) into fresh buffers of ``capacity`` rows."""
+    lib = N.load_library()
+    table = sel.table
+    stream = _stream(table.device)
+    ws = N.workspace(table.device, stream)
+    ws_ptr, ws_bytes = ws.ensure(sel.nrows, stream.cuda_stream)
+    if len(proj_cols) > N.MAX_PROJ:
+        raise ExecutionError("too many columns for one compaction")
+    cols = (N.EscColumn * max(len(proj_cols), 1))()
+    outs = N.EscOutputs()
+    outs.n_proj = len(proj_cols)
+    outs.capacity = capacity
+    values, nulls = [], []
+    dev = table.device
+    for k, col in enumerate(proj_cols):
+        N.require_cuda(col.values, f"column {col.name!r}")
+        cols[k].data = col.values.data_ptr() if len(col) else None
+        cols[k].nulls = col.nulls.data_ptr() if col.nulls is not None and len(col) else None
+        cols[k].dtype = N.dtype_code(col.values)
+        v = torch.empty(capacity, dtype=col.values.dtype, device=dev)
+        m = torch.empty(capacity, dtype=torch.bool, device=dev) if col.nulls is not None else None
+        values.append(v)
+        nulls.append(m)
+        outs.slot[k] = k
+        outs.out_values[k] = v.data_ptr() if capacity else None
+        outs.out_nulls[k] = m.data_ptr() if m is not None and capacity else None
+    rows = torch.empty(capacity, dtype=torch.int64, device=dev) if want_row_ids else None
+    outs.out_row_ids = rows.data_ptr() if rows is not None and capacity else None
+    ev0 = _ev_start(stream)
+    N.check(lib.esc_materialize_selection(C.c_void_p(sel.bitmap.data_ptr()), C.c_void_p(sel.tile_counts.data_ptr()),
+                                          sel.nrows, sel.tile_rows, cols, len(proj_cols),
+                                          C.c_void_p(sel.ids.data_ptr()) if sel.ids is not None else None,
+                                          C.byref(outs), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
+                                          C.c_void_p(stream.cuda_stream)), "esc_materialize_selection")
+    _ev_end(stream, ev0, "materialize")
+    return values, nulls, rows
+
+
 def launch_compact(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int,
                    proj_cols: list, capacity: int, want_row_ids: bool, stage_proj: bool = False):
-    """K2: fused predicate + count + order-preserving compaction of ``proj_cols`` (and/or the
-    physical row ids) into fresh buffers of ``capacity`` rows."""
+    """Single-pass predicate + count + order-preserving compaction with decoupled look-back
+    (``esc_compact_onepass``) of ``proj_cols`` (and/or the physical row ids) into fresh buffers
+    of ``capacity`` rows.  Bit-identical to select + materialize; kept as the one-pass variant."""
     lib = N.load_library()
     stream = _stream(table.device)
     ws = N.workspace(table.device, stream)
@@ -150,10 +229,10 @@ def launch_compact(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor 
     rows = torch.empty(capacity, dtype=torch.int64, device=dev) if want_row_ids else None
     outs.out_row_ids = rows.data_ptr() if rows is not None and capacity else None
     ev0 = _ev_start(stream)
-    N.check(lib.esc_compact(C.byref(cp.program), cols, cp.ncols + len(extra), n,
+    N.check(lib.esc_compact_onepass(C.byref(cp.program), cols, cp.ncols + len(extra), n,
                             C.c_void_p(ids.data_ptr()) if ids is not None else None, C.byref(outs),
                             C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
-                            C.c_void_p(stream.cuda_stream)), "esc_compact")
+                            C.c_void_p(stream.cuda_stream)), "esc_compact_onepass")
     _ev_end(stream, ev0, "compact")
     stream.synchronize()
     count, fails = ws.read_result(cp.n_udfs)
@@ -228,6 +307,17 @@ def _count_with_errors(table, pred, selection=None) -> int:
     return count
 
 
+def select(table: ColumnTable, pred: ex.Expr, selection: RowSelection | None = None) -> Selection:
+    """The count sub-query that also records its selection on the device (one predicate pass);
+    raises the reference's UDF errors."""
+    cp = compile_predicate(table, pred)
+    ids, n = _row_ids(selection if selection is not None else RowSelection(table))
+    count, fails, sel = launch_select(cp, table, ids, n)
+    if cp.unbound or cp.may_fail:
+        raise_udf_errors(table, cp, fails, ids, n)
+    return sel
+
+
 def count_star(table: ColumnTable, pred: ex.Expr | None) -> int:
     """Exact number of rows satisfying ``pred`` (reference ``executor.py:218-224``); nothing is
     materialised — one fused scan over the predicate columns."""
@@ -244,62 +334,51 @@ def eval_predicate(table: ColumnTable, pred: ex.Expr | None,
         selection = RowSelection(table)
     if pred is None:
         return selection
-    cp = compile_predicate(table, pred)
-    ids, n = _row_ids(selection)
-    k = _count_with_errors(table, pred, selection)
-    count, _, _, _, rows = launch_compact(cp, table, ids, n, [], k, want_row_ids=True)
-    if count != k:
-        raise ExecutionError(f"internal: compaction counted {count} rows, scan counted {k}")
+    sel = select(table, pred, selection)
+    _, _, rows = launch_materialize_selection(sel, [], sel.count, want_row_ids=True)
     return RowSelection(table, rows)
+
+
+def materialize_selection(sel: Selection, needed, capacity: int | None = None) -> list[Column]:
+    """Columns ``needed`` of the rows a Selection marks, in row order (no predicate re-scan)."""
+    proj = [sel.table.column(name) for name in needed]
+    cap = sel.count if capacity is None else min(int(capacity), sel.count)
+    values, nulls, _ = launch_materialize_selection(sel, proj, cap, want_row_ids=False)
+    return [Column(c.name, c.kind, v, m, c.dictionary) for c, v, m in zip(proj, values, nulls)]
 
 
 def materialize(table: ColumnTable, pred: ex.Expr, needed, count: int | None = None,
                 stage_proj: bool | None = None) -> list[Column]:
-    """Qualifying rows of ``needed`` columns, in row order, as new device columns — the fused
-    equivalent of ``eval_predicate(...).to_indices()`` + ``Column.take`` per column
-    (reference ``optimizer.py:191-192``).  ``count`` (when the ESC count sub-query already
-    produced it) sizes the outputs and saves the sizing scan."""
-    cp = compile_predicate(table, pred)
-    ids, n = _row_ids(RowSelection(table))
-    if count is None:
-        count = _count_with_errors(table, pred)
-    proj = [table.column(name) for name in needed]
-    if stage_proj is None:
-        # stream projection-only columns through smem once hits are dense enough that nearly
-        # every 32-byte sector of those columns is touched anyway
-        stage_proj = n > 0 and count * 8 >= n
-    got, _, values, nulls, _ = launch_compact(cp, table, ids, n, proj, count, want_row_ids=False,
-                                              stage_proj=stage_proj)
-    if got != count:
-        raise ExecutionError(f"internal: compaction counted {got} rows, expected {count}")
-    return [Column(c.name, c.kind, v, m, c.dictionary) for c, v, m in zip(proj, values, nulls)]
+    """Qualifying rows of ``needed`` columns, in row order, as new device columns — the
+    equivalent of ``eval_predicate(...).to_indices()`` + ``Column.take`` per column (reference
+    ``optimizer.py:191-192``): one predicate pass recording the selection, one compaction pass
+    over the selection.  ``count`` / ``stage_proj`` are accepted for API stability."""
+    del count, stage_proj
+    return materialize_selection(select(table, pred), needed)
 
 
 def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: int):
-    """ONE fused pass: exact count + order-preserving compaction of ``needed`` bounded by
-    ``capacity`` rows.  Returns ``(count, columns)``; ``columns`` is None when the count
-    exceeds the capacity (the caller's push-down threshold rejected the table anyway).
+    """The ESC step: one predicate pass (exact count + selection bitmap), then — only when the
+    count fits ``capacity`` (the push-down threshold) — the compaction of ``needed`` from the
+    recorded selection.  Returns ``(count, columns or None)``."""
+    sel = select(table, pred)
+    if sel.count > capacity:
+        return sel.count, None
+    return sel.count, materialize_selection(sel, needed)
 
-    The planner uses this for the ESC sub-query: with ``capacity = floor(max_selectivity *
-    rows)`` every table the policy would push down is fully materialised by the same scan that
-    counts it, instead of count-then-rescan (reference ``optimizer.py:317-327``)."""
+
+def materialize_onepass(table: ColumnTable, pred: ex.Expr, needed, capacity: int | None = None):
+    """Single-pass variant (decoupled look-back kernel); same results as :func:`materialize`."""
     cp = compile_predicate(table, pred)
     ids, n = _row_ids(RowSelection(table))
-    capacity = max(0, min(int(capacity), n))
     proj = [table.column(name) for name in needed]
-    count, fails, values, nulls, _ = launch_compact(cp, table, ids, n, proj, capacity, want_row_ids=False)
+    cap = n if capacity is None else max(0, min(int(capacity), n))
+    count, fails, values, nulls, _ = launch_compact(cp, table, ids, n, proj, cap, want_row_ids=False)
     if cp.unbound or cp.may_fail:
         raise_udf_errors(table, cp, fails, ids, n)
-    if count > capacity:
-        return count, None
-    out = []
-    for c, v, m in zip(proj, values, nulls):
-        if count < capacity:
-            # keep the temp table compact: copy the hits out of the capacity-sized buffer
-            v = v[:count].clone()
-            m = m[:count].clone() if m is not None else None
-        out.append(Column(c.name, c.kind, v, m, c.dictionary))
-    return count, out
+    k = min(count, cap)
+    return count, [Column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
+                   for c, v, m in zip(proj, values, nulls)]
 
 
 def take_column(col: Column, indices) -> Column:

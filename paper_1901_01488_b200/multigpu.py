@@ -13,7 +13,6 @@ table data crosses NVLink; the sharded temp stays where it was produced.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 from fractions import Fraction
 
@@ -128,11 +127,9 @@ def sharded_esc_subquery(st: ShardedTable, predicate, needed, config: EscConfig,
     n = st.local.row_count
     try:
         if fused:
-            cap = min(n, math.floor(Fraction(config.max_selectivity) * rc))
-            proj = [st.local.column(c) for c in needed]
-            local, fails, values, nulls, _ = executor.launch_compact(cp, st.local, None, n, proj, cap, False)
+            local, fails, sel = executor.launch_select(cp, st.local, None, n)
         else:
-            (local, fails), values, nulls, proj, cap = executor.launch_count(cp, st.local, None, n), [], [], [], 0
+            (local, fails), sel = executor.launch_count(cp, st.local, None, n), None
         if cp.unbound or cp.may_fail:
             _global_replay(st, cp, fails, group)
     except EscdbError as exc:
@@ -140,12 +137,10 @@ def sharded_esc_subquery(st: ShardedTable, predicate, needed, config: EscConfig,
     total, counts, offsets = exchange_counts(local, group)
     qualified = decide_pushdown(rc, total, config)
     cols = None
-    if qualified and config.materialize:
-        cols = []
-        for c, v, m in zip(proj, values, nulls):
-            v = v[:local].clone() if local < cap else v
-            m = (m[:local].clone() if local < cap else m) if m is not None else None
-            cols.append(Column(c.name, c.kind, v, m, c.dictionary))
+    if qualified and config.materialize and sel is not None:
+        # every rank compacts its own slice from the selection it recorded; concatenated in rank
+        # order the slices are the global, order-preserving temp (offset = this rank's position)
+        cols = executor.materialize_selection(sel, list(needed))
     return ShardedDecision(st.name, total, rc, Fraction(total, rc) if rc else Fraction(0), qualified,
                            local, offsets[st.rank], counts, cols)
 

@@ -233,3 +233,35 @@ def test_jit_udf_integer_lowering_and_errors(mixed, jit_always):
              ["fn", "rmod", [["a", None], ["b", None]], ">", 1.0]]
     for j in cases:
         assert _device(count_star, t, _pred(j)) == _oracle(O.count_star, ot, j, UDFS), j
+
+
+def test_onepass_lookback_kernel_matches(mixed):
+    """The single-pass decoupled look-back kernel (esc_compact_onepass) is bit-identical."""
+    from paper_1901_01488_b200 import executor
+
+    arrays, t, ot = mixed
+    corpus = Corpus(arrays, random.Random(31), udfs=("mixy", "lin"))
+    names = ["id", "a", "tag", "f", "val"]
+    for _ in range(25):
+        j = corpus.pred()
+        want = O.materialize(ot, j, names, UDFS)
+        count, cols = executor.materialize_onepass(t, _pred(j), names)
+        assert count == len(want["id"].values), j
+        for c in cols:
+            v, m = c.to_numpy()
+            assert np.array_equal(v, want[c.name].values) and np.array_equal(m, want[c.name].nulls), (j, c.name)
+
+
+def test_selection_reuse(mixed):
+    """select() records the selection once; materialising from it equals re-evaluating."""
+    from paper_1901_01488_b200 import executor
+
+    arrays, t, ot = mixed
+    j = ["or", [["cmp", ["a", None], "<", 100], ["eq", ["tag", None], 2]]]
+    sel = executor.select(t, _pred(j))
+    assert sel.count == O.count_star(ot, j)
+    (a1,) = executor.materialize_selection(sel, ["a"])
+    (a2,) = executor.materialize_selection(sel, ["a"], capacity=7)
+    want = O.materialize(ot, j, ["a"])["a"].values
+    assert np.array_equal(a1.to_numpy()[0], want)
+    assert np.array_equal(a2.to_numpy()[0], want[:7])

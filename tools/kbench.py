@@ -40,8 +40,17 @@ for name, p in preds.items():
     for _ in range(5):
         executor.count_and_materialize(t, p, ["A"], cap)
     torch.cuda.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b, _ in executor.KERNEL_EVENTS)
+    ev = executor.KERNEL_EVENTS
+    ms = sum(a.elapsed_time(b) for a, b, _ in ev) / 5   # select + materialize per step
+    res["select_ms"] = round(statistics.median(a.elapsed_time(b) for a, b, kk in ev if kk == "select"), 3)
     executor.KERNEL_EVENTS = None
     res.update(compact_ms=round(ms, 3), compact_GBps=round((n * width + k * 4) / ms / 1e6, 1), k=k)
+    executor.KERNEL_EVENTS = []
+    for _ in range(5):
+        executor.materialize_onepass(t, p, ["A"], cap)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b, _ in executor.KERNEL_EVENTS)
+    executor.KERNEL_EVENTS = None
+    res.update(onepass_ms=round(ms, 3))
     out[name] = res
 print(json.dumps({"rows": n, "env": {k: v for k, v in os.environ.items() if k.startswith("ESC_")}, "res": out}))
