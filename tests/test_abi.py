@@ -1,0 +1,83 @@
+"""The C ABI library: loads without a GPU, exports every entry point include/esc.h declares, struct
+layouts agree with the ctypes binding, and argument validation fails loudly (no device needed)."""
+
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    text = open(os.path.join(ROOT, "include", "esc.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(esc_[a-z_0-9]+)\s*\(", text, flags=re.M)))
+
+
+def test_every_declared_symbol_is_exported(native_lib):
+    names = _declared_functions()
+    assert len(names) >= 14, names
+    for name in names:
+        assert hasattr(native_lib, name), f"{name} declared in esc.h but not exported"
+    from paper_1901_01488_b200 import _native as N
+
+    assert set(names) == set(N.EXPORTED_SYMBOLS), "ctypes binding and header disagree"
+
+
+def test_struct_layouts_match(native_lib):
+    from paper_1901_01488_b200 import _native as N
+
+    for i, st in enumerate(N.STRUCTS):
+        assert native_lib.esc_struct_size(i) == C.sizeof(st), st.__name__
+    assert native_lib.esc_struct_size(99) == -1
+    assert C.sizeof(N.EscInstr) == 32 and C.sizeof(N.EscUdfOp) == 16
+
+
+def test_version_and_device_queries(native_lib):
+    assert native_lib.esc_abi_version() == 1
+    assert native_lib.esc_device_sm_count() >= 0  # 0 without a GPU
+
+
+def test_workspace_sizes_grow_with_rows(native_lib):
+    small = native_lib.esc_workspace_bytes(0)
+    big = native_lib.esc_workspace_bytes(600_000_000)
+    assert small >= 128 and big > small
+    w, t = C.c_int64(), C.c_int64()
+    assert native_lib.esc_selection_sizes(600_000_000, C.byref(w), C.byref(t)) == 0
+    assert w.value * 32 >= 600_000_000 and t.value >= 600_000_000 // 4096
+
+
+def test_invalid_arguments_are_reported(native_lib):
+    from paper_1901_01488_b200 import _native as N
+
+    res = N.EscResult()
+    ws = (C.c_uint8 * 4096)()
+    rc = native_lib.esc_scan_count(None, None, 0, 10, None, C.byref(res), ws, 4096, None)
+    assert rc == 1 and b"null program" in native_lib.esc_last_error()
+    prog = N.EscProgram()
+    prog.abi_version = 7
+    rc = native_lib.esc_scan_count(C.byref(prog), None, 0, 10, None, C.byref(res), ws, 4096, None)
+    assert rc == 1 and b"ABI version" in native_lib.esc_last_error()
+    prog.abi_version = 1
+    prog.n_instrs = 1
+    prog.instrs[0].op = N.OP_PUSH
+    rc = native_lib.esc_scan_count(C.byref(prog), None, 0, 10, None, C.byref(res), ws, 4096, None)
+    assert rc == 1 and b"PUSH/POP" in native_lib.esc_last_error()
+    assert native_lib.esc_set_jit(5, 0) == 1
+    stats = (C.c_int64 * 5)()
+    assert native_lib.esc_jit_stats(stats) == 0
+
+
+def test_kernels_refuse_cpu_tensors():
+    """No CPU fallback: a CPU-resident table is rejected before any launch."""
+    import numpy as np
+
+    from paper_1901_01488_b200 import ColumnTable, count_star, expr as ex
+    from paper_1901_01488_b200.errors import NativeUnavailable
+    from paper_1901_01488_b200.storage import KIND_INT32, Column
+
+    t = ColumnTable("t", [Column("a", KIND_INT32, np.arange(10, dtype=np.int32), device="cpu")])
+    with pytest.raises(NativeUnavailable):
+        count_star(t, ex.Comparison(ex.ColumnRef("t", "a"), "<", 5))

@@ -1,0 +1,68 @@
+"""UDF tracing: the recorded program reproduces CPython float semantics (checked with the host
+reference evaluator), and untraceable UDFs are refused loudly."""
+
+import math
+import random
+
+import pytest
+
+from paper_1901_01488_b200 import _native as N
+from paper_1901_01488_b200.errors import UnsupportedUdf
+from paper_1901_01488_b200.udf import FAIL_MESSAGES, trace
+
+CASES = [
+    lambda b, d: (b * 3.0 + d) % 7.0,
+    lambda x, y: (x * 7.0 + y) % 13.0,
+    lambda x, y: (x - y) // 3.0,
+    lambda x, y: -abs(x) + y / 2.5,
+    lambda x, y: x ** 2 - 10 * y,
+    lambda x, y: (x + 1) % -3.0,
+    lambda x, y: +x - (-y) * 0.1,
+    lambda x, y: 7 - x // -2,
+    lambda x, y: 2.0,
+]
+
+
+@pytest.mark.parametrize("fn", CASES)
+def test_traced_program_equals_python(fn):
+    prog = trace(fn, 2)
+    rng = random.Random(7)
+    vals = [0.0, -0.0, 1.0, -1.0, 7.0, -9.0, 13.5, -2.25, 1e15, -3e-7, 2.0**53]
+    for _ in range(300):
+        x, y = rng.choice(vals + [rng.uniform(-1e4, 1e4)]), rng.choice(vals + [rng.uniform(-1e4, 1e4)])
+        want = fn(x, y)
+        got = prog.evaluate([x, y])
+        assert (math.isnan(want) and math.isnan(got)) or (want == got and math.copysign(1, want) == math.copysign(1, got)), (x, y)
+
+
+def test_cpython_floored_semantics():
+    assert trace(lambda x, y: x % y, 2).evaluate([-9.0, 7.0]) == 5.0
+    assert math.copysign(1, trace(lambda x, y: x % y, 2).evaluate([7.0, -7.0])) == -1.0
+
+
+def test_may_fail_flags():
+    assert not trace(lambda x: x % 7.0, 1).may_fail
+    assert trace(lambda x, y: x % y, 2).may_fail
+    assert trace(lambda x: x / 0.0, 1).may_fail
+    assert trace(lambda x: x ** 2, 1).may_fail
+
+
+@pytest.mark.parametrize("fn,msg", [
+    (lambda x: x if x > 0 else -x, "control flow"),
+    (lambda x: math.sqrt(x), "float()"),
+    (lambda x: x ** 3, "\\*\\* 3"),
+    (lambda x: "s", "returns str"),
+    (lambda x: round(x), "float()"),
+])
+def test_untraceable_udfs_are_refused(fn, msg):
+    with pytest.raises(UnsupportedUdf, match=msg):
+        trace(fn, 1, "f")
+
+
+def test_failure_messages_are_cpythons():
+    assert FAIL_MESSAGES[N.FAIL_DIV] == "float division by zero"
+    assert FAIL_MESSAGES[N.FAIL_FLOORDIV] == "float floor division by zero"
+    try:
+        1.0 % 0.0
+    except ZeroDivisionError as e:
+        assert FAIL_MESSAGES[N.FAIL_MOD] == str(e)
