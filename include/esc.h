@@ -229,23 +229,42 @@ int esc_compact_onepass(const esc_program_t* prog, const esc_column_t* cols, int
                         int64_t nrows, const int64_t* d_row_ids, const esc_outputs_t* outs,
                         esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream);
 
-/* Upper bounds of the selection buffers esc_scan_select fills for `nrows` rows. */
-int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_tiles);
+/* A selection recorded by esc_scan_select (device buffers owned by the caller).
+ *  - bitmap: bit i of word i/32 = logical row i qualifies (row-linear);
+ *  - seg_counts: hits per warp segment of seg_rows rows (set by the scan), OR-ed with
+ *    ESC_SEG_CAPTURED when the segment was sparse enough (<= seg_rows/32 hits) for the scan to
+ *    CAPTURE the hits' projected values into cap_values (cap_per_seg slots per segment), so the
+ *    materialisation copies them instead of gathering rows from HBM again. */
+#define ESC_SEG_CAPTURED 0x80000000u
+typedef struct {
+  uint32_t* bitmap;
+  uint32_t* seg_counts;
+  int32_t seg_rows;     /* out: rows per segment                                  */
+  int32_t cap_per_seg;  /* out: capture slots per segment (seg_rows / 32)         */
+  int32_t n_cap;        /* in: captured projections (0 = none)                     */
+  int32_t pad;
+  int32_t cap_slot[ESC_MAX_PROJ];   /* in: column slot (of the scan's cols) per capture */
+  void* cap_values[ESC_MAX_PROJ];   /* in: esc_selection_sizes().cap_entries values each */
+  uint8_t* cap_nulls[ESC_MAX_PROJ]; /* in: null bytes per capture, or NULL                */
+} esc_selection_t;
 
-/* The count sub-query that also RECORDS its selection: bit i of d_bitmap[i/32] = logical row i
- * qualifies; d_tile_counts[t] = qualifying rows of tile t (of *tile_rows rows).  Costs N/8 bytes
- * of writes on top of esc_scan_count; materialisation then never re-evaluates the predicate
- * (the reference re-scans: optimizer.py:191). */
+/* Upper bounds of the selection buffers for `nrows` rows: bitmap words, segments (seg_counts
+ * entries) and capture entries (per captured column). */
+int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_segments, int64_t* cap_entries);
+
+/* The count sub-query that also RECORDS its selection (bitmap + segment counts, and the
+ * projected values of sparse segments' hits).  Costs N/8 bytes of bitmap writes on top of
+ * esc_scan_count; materialisation then never re-evaluates the predicate (the reference re-scans:
+ * optimizer.py:191). */
 int esc_scan_select(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols,
-                    int64_t nrows, const int64_t* d_row_ids, uint32_t* d_bitmap,
-                    uint32_t* d_tile_counts, int32_t* tile_rows, esc_result_t* result,
-                    void* d_ws, size_t ws_bytes, void* stream);
+                    int64_t nrows, const int64_t* d_row_ids, esc_selection_t* sel,
+                    esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream);
 
-/* Order-preserving compaction of the rows a selection marks: per-tile offsets by a scan of the
- * tile counts, then every warp maps one row per lane of a bitmap word (contiguous reads of the
- * projected columns' hit rows, contiguous writes).  cols[outs->slot[k]] is projection k. */
-int esc_materialize_selection(const uint32_t* d_bitmap, const uint32_t* d_tile_counts,
-                              int64_t nrows, int32_t tile_rows, const esc_column_t* cols,
+/* Order-preserving compaction of the rows a selection marks: per-segment offsets by a scan of
+ * the segment counts; captured segments are copied from the capture buffers, the others
+ * gathered through the bitmap (one row per lane of a word: contiguous reads and writes).
+ * cols[outs->slot[k]] is projection k (cols as given to esc_scan_select). */
+int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const esc_column_t* cols,
                               int32_t ncols, const int64_t* d_row_ids, const esc_outputs_t* outs,
                               void* d_ws, size_t ws_bytes, void* stream);
 
@@ -268,7 +287,7 @@ int esc_set_jit(int mode, int64_t min_rows);
  * NVRTC available (0/1). */
 int esc_jit_stats(int64_t* out);
 /* sizeof() of the ABI structs, for binding checks: 0 program, 1 instr, 2 udf, 3 udf_op,
- * 4 column, 5 result, 6 outputs; -1 for an unknown id. */
+ * 4 column, 5 result, 6 outputs, 7 selection; -1 for an unknown id. */
 int esc_struct_size(int which);
 /* Tile geometry the kernels use for a program over these columns (for roofline accounting). */
 int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols);

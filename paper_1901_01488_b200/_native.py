@@ -82,7 +82,15 @@ class EscOutputs(C.Structure):
                 ("out_row_ids", C.c_void_p), ("capacity", C.c_int64)]
 
 
-STRUCTS = [EscProgram, EscInstr, EscUdf, EscUdfOp, EscColumn, EscResult, EscOutputs]
+class EscSelection(C.Structure):
+    _fields_ = [("bitmap", C.c_void_p), ("seg_counts", C.c_void_p), ("seg_rows", C.c_int32),
+                ("cap_per_seg", C.c_int32), ("n_cap", C.c_int32), ("pad", C.c_int32),
+                ("cap_slot", C.c_int32 * MAX_PROJ), ("cap_values", C.c_void_p * MAX_PROJ),
+                ("cap_nulls", C.c_void_p * MAX_PROJ)]
+
+
+SEG_CAPTURED = 0x80000000
+STRUCTS = [EscProgram, EscInstr, EscUdf, EscUdfOp, EscColumn, EscResult, EscOutputs, EscSelection]
 
 # every symbol include/esc.h declares, with its ctypes signature
 _SIGNATURES = {
@@ -96,13 +104,13 @@ _SIGNATURES = {
     "esc_compact_onepass": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32, C.c_int64,
                                       C.c_void_p, C.POINTER(EscOutputs), C.c_void_p, C.c_void_p, C.c_size_t,
                                       C.c_void_p]),
-    "esc_selection_sizes": (C.c_int, [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "esc_selection_sizes": (C.c_int, [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64)]),
     "esc_scan_select": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32, C.c_int64, C.c_void_p,
-                                  C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p,
-                                  C.c_size_t, C.c_void_p]),
-    "esc_materialize_selection": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(EscColumn),
-                                            C.c_int32, C.c_void_p, C.POINTER(EscOutputs), C.c_void_p,
-                                            C.c_size_t, C.c_void_p]),
+                                  C.POINTER(EscSelection), C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "esc_materialize_selection": (C.c_int, [C.POINTER(EscSelection), C.c_int64, C.POINTER(EscColumn), C.c_int32,
+                                            C.c_void_p, C.POINTER(EscOutputs), C.c_void_p, C.c_size_t,
+                                            C.c_void_p]),
     "esc_gather": (C.c_int, [C.POINTER(EscColumn), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                              C.c_void_p]),
     "esc_last_error": (C.c_char_p, []),

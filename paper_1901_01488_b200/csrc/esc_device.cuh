@@ -101,8 +101,8 @@ struct KParams {
   uint8_t proj_mode[ESC_MAX_PROJ];   // values: 0 compact in place, 1 gather hits from HBM, 2 alias
   uint8_t proj_nmode[ESC_MAX_PROJ];  // nulls:  0 in place, 1 gather, 2 alias, 3 none (write zeros)
   int32_t all_fast;      // full tiles use the fast (writer copy-out) path
-  uint32_t* sel_bitmap;       // K1 selection output: bit i of word i/32 = logical row i qualifies
-  uint32_t* sel_tile_counts;  // K1 selection output: qualifying rows per tile
+  int32_t sel_on;             // K1 records the selection into `sel`
+  esc_selection_t sel;
   uint32_t rows_off;     // stage offset of the u16 row-index scratch (row-id outputs)
 };
 
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
     if constexpr (!COMPACT) {
       const uint32_t pc = __popc(bits);
       my_count += pc;
-      if (p.sel_bitmap != nullptr) {
+      if (p.sel_on) {
         // 8 lanes x 4 rows of a chunk = one 32-row bitmap word (row-linear order)
         const int64_t word0 = tile * (p.tile_rows / 32) + cw * (4 * C) + (lane >> 3);
 #pragma unroll
@@ -979,18 +979,59 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
           v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
           v |= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
           v |= __shfl_xor_sync(0xFFFFFFFFu, v, 4);
-          if ((lane & 7) == 0) p.sel_bitmap[word0 + 4 * c] = v;
+          if ((lane & 7) == 0) p.sel.bitmap[word0 + 4 * c] = v;
         }
-        uint32_t wsum = pc;
+        const int64_t seg = tile * kConsumerWarps + cw;
+        const uint32_t pc = __popc(bits);
+        uint32_t wtot = pc, flag = 0;
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) wsum += __shfl_xor_sync(0xFFFFFFFFu, wsum, d);
-        if (lane == 0) {
-          const uint32_t now = atomicAdd(&s_tsum[s], (1u << 20) + wsum) + (1u << 20) + wsum;
-          if ((now >> 20) == kConsumerWarps) {
-            s_tsum[s] = 0;
-            p.sel_tile_counts[tile] = now & 0xFFFFFu;
+        for (int d = 16; d > 0; d >>= 1) wtot += __shfl_xor_sync(0xFFFFFFFFu, wtot, d);
+        if (p.sel.n_cap > 0 && wtot > 0 && wtot <= (uint32_t)(4 * C)) {
+          // very sparse segment: capture the hits' projected values now, while they sit in smem
+          // (warp-local ranks: per-chunk lane counts in 8-bit fields, one scan ranks every chunk)
+          flag = ESC_SEG_CAPTURED;
+          uint32_t packed = 0;
+#pragma unroll
+          for (int c = 0; c < C; ++c) packed |= (uint32_t)__popc((bits >> (4 * c)) & 0xFu) << (8 * c);
+          uint32_t incl = packed;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += t;
+          }
+          const uint32_t wtp = __shfl_sync(0xFFFFFFFFu, incl, 31);
+          const uint32_t excl = incl - packed;
+          if (bits) {
+            for (int k = 0; k < p.sel.n_cap; ++k) {
+              const KCol& col = p.cols[p.sel.cap_slot[k]];
+              uint8_t* dst = static_cast<uint8_t*>(p.sel.cap_values[k]) + (size_t)seg * p.sel.cap_per_seg * col.width;
+              uint8_t* dn = p.sel.cap_nulls[k] ? p.sel.cap_nulls[k] + (size_t)seg * p.sel.cap_per_seg : nullptr;
+              uint32_t cb = 0;
+#pragma unroll
+              for (int c = 0; c < C; ++c) {
+                uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);
+                cb += (wtp >> (8 * c)) & 0xFFu;
+                uint32_t m = (bits >> (4 * c)) & 0xFu;
+                while (m) {
+                  const int bit = 4 * c + __ffs(m) - 1;
+                  m &= m - 1;
+                  const uint8_t* src = value_ptr(col, rr, bit);
+                  switch (col.width) {
+                    case 1: dst[r] = *src; break;
+                    case 2: reinterpret_cast<uint16_t*>(dst)[r] = *reinterpret_cast<const uint16_t*>(src); break;
+                    case 4: reinterpret_cast<uint32_t*>(dst)[r] = *reinterpret_cast<const uint32_t*>(src); break;
+                    default:
+                      reinterpret_cast<unsigned long long*>(dst)[r] = *reinterpret_cast<const unsigned long long*>(src);
+                      break;
+                  }
+                  if (dn) dn[r] = is_null(col, rr, bit) ? 1 : 0;
+                  ++r;
+                }
+              }
+            }
           }
         }
+        if (lane == 0) p.sel.seg_counts[seg] = wtot | flag;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
@@ -1135,7 +1176,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_partials(const uint32_
   const int64_t base = (int64_t)blockIdx.x * kScanSeg + 4 * threadIdx.x;
   unsigned long long v = 0;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) v += (base + j < n) ? counts[base + j] : 0u;
+  for (int j = 0; j < 4; ++j) v += (base + j < n) ? (counts[base + j] & ~ESC_SEG_CAPTURED) : 0u;
   unsigned long long total;
   block_excl_scan(v, sh, &total);
   if (threadIdx.x == 0) partial[blockIdx.x] = total;
@@ -1157,7 +1198,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* 
   unsigned long long v = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    x[j] = (base + j < n) ? counts[base + j] : 0u;
+    x[j] = (base + j < n) ? (counts[base + j] & ~ESC_SEG_CAPTURED) : 0u;
     v += x[j];
   }
   unsigned long long total;
@@ -1171,126 +1212,151 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* 
 
 struct SelParams {
   const uint32_t* bitmap;
-  const uint32_t* tile_counts;
-  const unsigned long long* tile_offsets;
+  const uint32_t* seg_counts;            // | ESC_SEG_CAPTURED
+  const unsigned long long* seg_offsets;
   const int64_t* row_ids;  // logical -> physical rows (selection chaining) or nullptr
   int64_t nrows;
-  int64_t n_tiles;
-  int32_t tile_rows;
+  int64_t n_segs;
+  int32_t seg_rows;
+  int32_t cap_per_seg;
   int32_t n_proj;
+  int32_t need_bitmap_captured;  // captured segments still need the bitmap (row ids / uncaptured columns)
   KCol cols[ESC_MAX_PROJ];  // projected columns (data, nulls, width)
+  int32_t cap_index[ESC_MAX_PROJ];      // capture holding projection k, -1 = gather it
+  const void* cap_values[ESC_MAX_PROJ];
+  const uint8_t* cap_nulls[ESC_MAX_PROJ];
   esc_outputs_t outs;
 };
 
 constexpr int kSelWarps = 8;
 
-template <typename T>
-__device__ __forceinline__ void sel_copy4(const KCol& col, uint8_t* out, const bool (&hit)[4],
-                                          const int64_t (&prow)[4], const unsigned long long (&pos)[4], long long cap) {
-  const T* src = reinterpret_cast<const T*>(col.data);
-  T* dst = reinterpret_cast<T*>(out);
-  T v[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) v[u] = hit[u] ? __ldg(src + prow[u]) : T(0);  // 4 loads in flight
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-    if (hit[u] && (long long)pos[u] < cap) dst[pos[u]] = v[u];
+__device__ __forceinline__ unsigned long long ld_bits(const KCol& col, int64_t row) {
+  switch (col.width) {
+    case 1: return __ldg(col.data + row);
+    case 2: return __ldg(reinterpret_cast<const uint16_t*>(col.data) + row);
+    case 4: return __ldg(reinterpret_cast<const uint32_t*>(col.data) + row);
+    default: return __ldg(reinterpret_cast<const unsigned long long*>(col.data) + row);
+  }
+}
+__device__ __forceinline__ void st_bits(int width, void* out, unsigned long long pos, unsigned long long v) {
+  switch (width) {
+    case 1: static_cast<uint8_t*>(out)[pos] = (uint8_t)v; break;
+    case 2: static_cast<uint16_t*>(out)[pos] = (uint16_t)v; break;
+    case 4: static_cast<uint32_t*>(out)[pos] = (uint32_t)v; break;
+    default: static_cast<unsigned long long*>(out)[pos] = v; break;
+  }
 }
 
-// One tile per WARP (no block synchronisation): lane l loads bitmap word l of each 32-word
-// group; words are then walked four at a time, every word mapping one row per lane, so the
-// projected columns are read and the outputs written contiguously across the warp.
+template <typename T>
+__device__ __forceinline__ void copy_run(const void* src, void* dst, uint32_t n, unsigned long long base,
+                                         long long cap, int lane) {
+  const T* s = static_cast<const T*>(src);
+  T* d = static_cast<T*>(dst);
+  for (uint32_t e = lane; e < n; e += 32)
+    if ((long long)(base + e) < cap) d[base + e] = s[e];
+}
+
+// One warp per segment (seg_rows = 128*C rows = 4*C <= 16 bitmap words).  Captured segments:
+// coalesced copy of the hits the scan captured.  Other segments (and row ids): every bitmap word
+// maps one row per lane, so the gathers of the projected columns and the output writes are both
+// contiguous across the warp.
 __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int W = p.tile_rows / 32;  // bitmap words per tile (a multiple of 32)
+  const int W = p.seg_rows / 32;  // words per segment (<= 32)
   const long long cap = p.outs.capacity;
   const uint32_t lt = (1u << lane) - 1u;
-  for (int64_t tile = gwarp; tile < p.n_tiles; tile += nwarps) {
-    if (p.tile_counts[tile] == 0) continue;
-    unsigned long long pos0 = p.tile_offsets[tile];
-    const int64_t wbase = tile * W;
-    for (int i0 = 0; i0 < W; i0 += 32) {
-      const uint32_t mine = p.bitmap[wbase + i0 + lane];
-      uint32_t nz = __ballot_sync(0xFFFFFFFFu, mine != 0);
-      if (nz == 0) continue;
-      if (__popc(nz) <= 8) {
-        // sparse: visit only the non-empty words
-        const uint32_t before = __popc(mine);
-        uint32_t excl = before;  // exclusive prefix of popc over words < lane
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, excl, d);
-          if (lane >= d) excl += t;
+  const uint32_t sparse_max = (uint32_t)W;  // <= one hit per 32 rows on average: one lane per segment
+  // a warp takes 32 consecutive segments: sparse ones are handled one per LANE (32 independent
+  // gathers in flight per warp), dense ones cooperatively, one row per lane of each word
+  for (int64_t seg0 = gwarp * 32; seg0 < p.n_segs; seg0 += nwarps * 32) {
+    const int64_t myseg = seg0 + lane;
+    const uint32_t raw = myseg < p.n_segs ? p.seg_counts[myseg] : 0u;
+    const uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
+    const bool captured = (raw & ESC_SEG_CAPTURED) != 0;
+    const unsigned long long myoff = cnt ? p.seg_offsets[myseg] : 0ull;
+    // ---- captured segments: coalesced copy of the hits the scan captured ----
+    uint32_t cap_mask = __ballot_sync(0xFFFFFFFFu, captured && cnt > 0);
+    while (cap_mask) {
+      const int l = __ffs(cap_mask) - 1;
+      cap_mask &= cap_mask - 1;
+      const int64_t seg = seg0 + l;
+      const uint32_t n = __shfl_sync(0xFFFFFFFFu, cnt, l);
+      const unsigned long long base = __shfl_sync(0xFFFFFFFFu, myoff, l);
+      for (int k = 0; k < p.n_proj; ++k) {
+        const int ci = p.cap_index[k];
+        if (ci < 0) continue;
+        const int w = p.cols[k].width;
+        const uint8_t* src = static_cast<const uint8_t*>(p.cap_values[ci]) + (size_t)seg * p.cap_per_seg * w;
+        switch (w) {
+          case 1: copy_run<uint8_t>(src, p.outs.out_values[k], n, base, cap, lane); break;
+          case 2: copy_run<uint16_t>(src, p.outs.out_values[k], n, base, cap, lane); break;
+          case 4: copy_run<uint32_t>(src, p.outs.out_values[k], n, base, cap, lane); break;
+          default: copy_run<unsigned long long>(src, p.outs.out_values[k], n, base, cap, lane); break;
         }
-        excl -= before;
-        const uint32_t group_total = __shfl_sync(0xFFFFFFFFu, excl + before, 31);
-        while (nz) {
-          const int i = __ffs(nz) - 1;
-          nz &= nz - 1;
-          const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, i);
-          const unsigned long long pos = pos0 + __shfl_sync(0xFFFFFFFFu, excl, i) + __popc(word & lt);
-          if (!((word >> lane) & 1u) || (long long)pos >= cap) continue;
-          const int64_t row = (wbase + i0 + i) * 32 + lane;
-          const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
-          for (int k = 0; k < p.n_proj; ++k) {
-            const KCol& col = p.cols[k];
-            const uint8_t* src = col.data + (size_t)prow * col.width;
-            uint8_t* dst = static_cast<uint8_t*>(p.outs.out_values[k]) + (size_t)pos * col.width;
-            switch (col.width) {
-              case 1: *dst = __ldg(src); break;
-              case 2: *reinterpret_cast<uint16_t*>(dst) = __ldg(reinterpret_cast<const uint16_t*>(src)); break;
-              case 4: *reinterpret_cast<uint32_t*>(dst) = __ldg(reinterpret_cast<const uint32_t*>(src)); break;
-              default:
-                *reinterpret_cast<unsigned long long*>(dst) = __ldg(reinterpret_cast<const unsigned long long*>(src));
-                break;
-            }
-            if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
-          }
-          if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
+        if (p.outs.out_nulls[k] != nullptr) {
+          const uint8_t* ns = p.cap_nulls[ci] ? p.cap_nulls[ci] + (size_t)seg * p.cap_per_seg : nullptr;
+          for (uint32_t e = lane; e < n; e += 32)
+            if ((long long)(base + e) < cap) p.outs.out_nulls[k][base + e] = ns ? ns[e] : 0;
         }
-        pos0 += group_total;
-        continue;
       }
-#pragma unroll 1
-      for (int g = 0; g < 32; g += 4) {
-        uint32_t wd[4];
-        bool hit[4];
-        unsigned long long pos[4];
-        int64_t prow[4];
-        uint32_t any = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          wd[u] = __shfl_sync(0xFFFFFFFFu, mine, g + u);
-          any |= wd[u];
-          hit[u] = (wd[u] >> lane) & 1u;
-          pos[u] = pos0 + __popc(wd[u] & lt);
-          pos0 += __popc(wd[u]);
-          const int64_t row = (wbase + i0 + g + u) * 32 + lane;
-          prow[u] = (hit[u] && p.row_ids) ? __ldg(p.row_ids + row) : row;
+    }
+    const bool bitmap_work = cnt > 0 && (!captured || p.need_bitmap_captured);
+    // ---- sparse segments: one lane walks its segment's words ----
+    if (bitmap_work && cnt <= sparse_max) {
+      unsigned long long pos = myoff;
+      for (int i = 0; i < W; ++i) {
+        uint32_t word = p.bitmap[myseg * W + i];
+        while (word) {
+          const int b = __ffs(word) - 1;
+          word &= word - 1;
+          if ((long long)pos < cap) {
+            const int64_t row = (myseg * W + i) * 32 + b;
+            const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
+            for (int k = 0; k < p.n_proj; ++k) {
+              if (captured && p.cap_index[k] >= 0) continue;
+              const KCol& col = p.cols[k];
+              st_bits(col.width, p.outs.out_values[k], pos, ld_bits(col, prow));
+              if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
+            }
+            if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
+          }
+          ++pos;
         }
-        if (any == 0) continue;
+      }
+    }
+    // ---- dense segments: the whole warp, one row per lane of each word ----
+    uint32_t dense = __ballot_sync(0xFFFFFFFFu, bitmap_work && cnt > sparse_max);
+    while (dense) {
+      const int l = __ffs(dense) - 1;
+      dense &= dense - 1;
+      const int64_t seg = seg0 + l;
+      const bool seg_captured = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, l) != 0;
+      const unsigned long long base = __shfl_sync(0xFFFFFFFFu, myoff, l);
+      const uint32_t mine = lane < W ? p.bitmap[seg * W + lane] : 0u;
+      const uint32_t pc = __popc(mine);
+      uint32_t excl = pc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, excl, d);
+        if (lane >= d) excl += t;
+      }
+      excl -= pc;
+      for (int i = 0; i < W; ++i) {
+        const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, i);
+        if (word == 0) continue;
+        const unsigned long long pos = base + __shfl_sync(0xFFFFFFFFu, excl, i) + __popc(word & lt);
+        if (!((word >> lane) & 1u) || (long long)pos >= cap) continue;
+        const int64_t row = (seg * W + i) * 32 + lane;
+        const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
         for (int k = 0; k < p.n_proj; ++k) {
+          if (seg_captured && p.cap_index[k] >= 0) continue;
           const KCol& col = p.cols[k];
-          uint8_t* out = static_cast<uint8_t*>(p.outs.out_values[k]);
-          switch (col.width) {
-            case 1: sel_copy4<uint8_t>(col, out, hit, prow, pos, cap); break;
-            case 2: sel_copy4<uint16_t>(col, out, hit, prow, pos, cap); break;
-            case 4: sel_copy4<uint32_t>(col, out, hit, prow, pos, cap); break;
-            default: sel_copy4<unsigned long long>(col, out, hit, prow, pos, cap); break;
-          }
-          if (p.outs.out_nulls[k] != nullptr) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (hit[u] && (long long)pos[u] < cap) p.outs.out_nulls[k][pos[u]] = col.nulls ? __ldg(col.nulls + prow[u]) : 0;
-          }
+          st_bits(col.width, p.outs.out_values[k], pos, ld_bits(col, prow));
+          if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
         }
-        if (p.outs.out_row_ids != nullptr) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (hit[u] && (long long)pos[u] < cap) p.outs.out_row_ids[pos[u]] = prow[u];
-        }
+        if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
       }
     }
   }

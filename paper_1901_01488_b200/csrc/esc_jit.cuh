@@ -85,7 +85,30 @@ struct Entry {
   std::string log;
 };
 std::mutex g_mu;
-std::unordered_map<std::string, Entry> g_cache;
+std::unordered_map<std::string, Entry> g_cache;        // generated source -> module
+std::unordered_map<std::string, std::string> g_shape;  // shape bytes -> generated source (fast path)
+
+// Everything the generated evaluator bakes in (opcodes, flags, smem offsets, dtypes, UDF
+// programs) — but not the query constants, which it reads from the kernel parameters.
+std::string shape_key(const KParams& kp, bool compact) {
+  std::string k;
+  k.reserve(64 + sizeof(KInstr) * kp.n_ins + sizeof(kp.udfs) + sizeof(kp.udf_ops) + 16 * kp.ncols);
+  const int hdr[4] = {kp.chunks, compact ? 1 : 0, kp.n_ins, kp.ncols};
+  k.append(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+  for (int i = 0; i < kp.n_ins; ++i) {
+    KInstr K = kp.ins[i];
+    K.lo.i = K.hi.i = 0;
+    k.append(reinterpret_cast<const char*>(&K), sizeof(K));
+  }
+  k.append(reinterpret_cast<const char*>(kp.udfs), sizeof(kp.udfs));
+  k.append(reinterpret_cast<const char*>(kp.udf_ops), sizeof(kp.udf_ops));
+  for (int i = 0; i < kp.ncols; ++i) {
+    const KCol& c = kp.cols[i];
+    const uint32_t v[4] = {(uint32_t)c.dtype, c.smem_off, c.smem_null_off, c.nulls != nullptr ? 1u : 0u};
+    k.append(reinterpret_cast<const char*>(v), sizeof(v));
+  }
+  return k;
+}
 
 // ---- code generation -------------------------------------------------------------------------
 const char* ctype_of(int dtype) {
@@ -399,13 +422,19 @@ cudaKernel_t get_kernel(const KParams& kp, bool compact, size_t smem, std::strin
     *why = nv.why;
     return nullptr;
   }
-  std::ostringstream pred;
-  if (!gen_pred(kp, kp.chunks, pred)) return nullptr;
   const std::string inst = "esc::esc_scan_kernel<" + std::to_string(kp.chunks) + ", " + (compact ? "true" : "false") +
                            ", esc::JitPred>";
-  const std::string src = std::string("#include \"esc_device.cuh\"\nnamespace esc {\n") + pred.str() + "}\n";
-  const std::string key = inst + "\n" + src;
   std::lock_guard<std::mutex> g(g_mu);
+  const std::string shape = shape_key(kp, compact);
+  auto sh = g_shape.find(shape);
+  if (sh == g_shape.end()) {
+    std::ostringstream pred;
+    if (!gen_pred(kp, kp.chunks, pred)) return nullptr;
+    const std::string src = std::string("#include \"esc_device.cuh\"\nnamespace esc {\n") + pred.str() + "}\n";
+    sh = g_shape.emplace(shape, inst + "\n" + src).first;
+  }
+  const std::string& key = sh->second;
+  const std::string src = key.substr(key.find('\n') + 1);
   auto it = g_cache.find(key);
   if (it != g_cache.end()) {
     if (!it->second.ok) {

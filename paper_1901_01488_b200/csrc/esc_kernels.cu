@@ -107,8 +107,8 @@ size_t status_words(int64_t nrows) {
   return (size_t)((nrows + t - 1) / t) + 1;
 }
 
-// Workspace layout: [header][tile status (one-pass K2)][tile offsets u64][scan partials u64]
-//                   [tile counts u32][selection bitmap u32]
+// Workspace layout: [header][tile status (one-pass K2)][segment offsets u64][scan partials u64]
+//                   [segment counts u32][selection bitmap u32]
 struct WsLayout {
   size_t status, offsets, partials, counts, bitmap, total;
   int64_t max_tiles, bitmap_words;
@@ -118,7 +118,7 @@ WsLayout ws_layout(int64_t nrows) {
   if (nrows < 0) nrows = 0;
   const int64_t t_min = (int64_t)kConsumerWarps * kChunkRows;        // smallest tile (C = 1)
   const int64_t t_max = 4 * t_min;                                   // largest tile (C = 4)
-  L.max_tiles = (nrows + t_min - 1) / t_min + 1;
+  L.max_tiles = ((nrows + t_min - 1) / t_min + 1) * kConsumerWarps;  // warp segments
   L.bitmap_words = ((nrows + t_max - 1) / t_max + 1) * (t_max / 32);  // covers every C's last tile
   const int64_t segs = L.max_tiles / kScanSeg + 2;
   auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -582,10 +582,11 @@ extern "C" {
 
 size_t esc_workspace_bytes(int64_t nrows) { return ws_layout(nrows).total; }
 
-int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_tiles) {
+int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_segments, int64_t* cap_entries) {
   const WsLayout L = ws_layout(nrows);
   if (bitmap_words) *bitmap_words = L.bitmap_words;
-  if (max_tiles) *max_tiles = L.max_tiles;
+  if (max_segments) *max_segments = L.max_tiles;
+  if (cap_entries) *cap_entries = (nrows < 0 ? 0 : nrows) / 8 + 16 * 4 * (int64_t)kConsumerWarps * 2;
   return ESC_OK;
 }
 
@@ -611,39 +612,49 @@ int esc_scan_count(const esc_program_t* prog, const esc_column_t* cols, int32_t 
 }
 
 int esc_scan_select(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
-                    const int64_t* d_row_ids, uint32_t* d_bitmap, uint32_t* d_tile_counts, int32_t* tile_rows,
-                    esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream) {
+                    const int64_t* d_row_ids, esc_selection_t* sel, esc_result_t* result, void* d_ws,
+                    size_t ws_bytes, void* stream) {
   static thread_local KParams kp;
-  if (d_bitmap == nullptr || d_tile_counts == nullptr || tile_rows == nullptr)
+  if (sel == nullptr || sel->bitmap == nullptr || sel->seg_counts == nullptr)
     return fail(ESC_ERR_INVALID, "null selection output");
+  if (sel->n_cap < 0 || sel->n_cap > ESC_MAX_PROJ) return fail(ESC_ERR_INVALID, "n_cap out of range");
+  for (int k = 0; k < sel->n_cap; ++k)
+    if (sel->cap_slot[k] < 0 || sel->cap_slot[k] >= ncols || sel->cap_values[k] == nullptr)
+      return fail(ESC_ERR_INVALID, "bad capture slot / buffer");
   int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, nullptr);
   if (rc != ESC_OK) return rc;
-  kp.sel_bitmap = d_bitmap;
-  kp.sel_tile_counts = d_tile_counts;
-  *tile_rows = kp.tile_rows;
+  sel->seg_rows = kChunkRows * kp.chunks;
+  sel->cap_per_seg = 4 * kp.chunks;  // segments with <= 4*C hits (~3% of 128*C rows) are captured
+  kp.sel_on = 1;
+  kp.sel = *sel;
   return launch<false>(kp, static_cast<cudaStream_t>(stream));
 }
 
-int esc_materialize_selection(const uint32_t* d_bitmap, const uint32_t* d_tile_counts, int64_t nrows,
-                              int32_t tile_rows, const esc_column_t* cols, int32_t ncols, const int64_t* d_row_ids,
-                              const esc_outputs_t* outs, void* d_ws, size_t ws_bytes, void* stream) {
+int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const esc_column_t* cols, int32_t ncols,
+                              const int64_t* d_row_ids, const esc_outputs_t* outs, void* d_ws, size_t ws_bytes,
+                              void* stream) {
   static thread_local SelParams sp;
-  if (d_bitmap == nullptr || d_tile_counts == nullptr || outs == nullptr)
+  if (sel == nullptr || sel->bitmap == nullptr || sel->seg_counts == nullptr || outs == nullptr)
     return fail(ESC_ERR_INVALID, "null selection argument");
   if (nrows < 0 || ncols < 0 || ncols > ESC_MAX_COLS) return fail(ESC_ERR_INVALID, "bad sizes");
-  if (tile_rows <= 0 || tile_rows % 1024 != 0) return fail(ESC_ERR_INVALID, "tile_rows must come from esc_scan_select");
+  if (sel->seg_rows <= 0 || sel->seg_rows % 128 != 0 || sel->seg_rows > 1024)
+    return fail(ESC_ERR_INVALID, "selection was not filled by esc_scan_select");
   if (outs->n_proj < 0 || outs->n_proj > ESC_MAX_PROJ || outs->capacity < 0)
     return fail(ESC_ERR_INVALID, "bad outputs");
   const WsLayout L = ws_layout(nrows);
   if (d_ws == nullptr || ws_bytes < L.total) return fail(ESC_ERR_WORKSPACE, "workspace too small");
   std::memset(&sp, 0, sizeof(sp));
-  sp.bitmap = d_bitmap;
-  sp.tile_counts = d_tile_counts;
+  sp.bitmap = sel->bitmap;
+  sp.seg_counts = sel->seg_counts;
   sp.row_ids = d_row_ids;
   sp.nrows = nrows;
-  sp.tile_rows = tile_rows;
-  sp.n_tiles = (nrows + tile_rows - 1) / tile_rows;
+  sp.seg_rows = sel->seg_rows;
+  sp.cap_per_seg = sel->cap_per_seg;
+  // segments cover whole tiles: tile = kConsumerWarps segments
+  const int64_t tile_rows = (int64_t)sel->seg_rows * kConsumerWarps;
+  sp.n_segs = ((nrows + tile_rows - 1) / tile_rows) * kConsumerWarps;
   sp.n_proj = outs->n_proj;
+  sp.need_bitmap_captured = outs->out_row_ids != nullptr;
   for (int k = 0; k < outs->n_proj; ++k) {
     if (outs->slot[k] < 0 || outs->slot[k] >= ncols) return fail(ESC_ERR_INVALID, "projection slot out of range");
     const esc_column_t& c = cols[outs->slot[k]];
@@ -654,20 +665,30 @@ int esc_materialize_selection(const uint32_t* d_bitmap, const uint32_t* d_tile_c
     sp.cols[k].nulls = c.nulls;
     sp.cols[k].dtype = c.dtype;
     sp.cols[k].width = w;
+    sp.cap_index[k] = -1;
+    for (int j = 0; j < sel->n_cap; ++j)
+      if (sel->cap_slot[j] == outs->slot[k] && (outs->out_nulls[k] == nullptr || c.nulls == nullptr ||
+                                                sel->cap_nulls[j] != nullptr)) {
+        sp.cap_index[k] = j;
+        sp.cap_values[j] = sel->cap_values[j];
+        sp.cap_nulls[j] = sel->cap_nulls[j];
+        break;
+      }
+    if (sp.cap_index[k] < 0) sp.need_bitmap_captured = 1;
   }
   sp.outs = *outs;
-  if (sp.n_tiles == 0) return ESC_OK;
+  if (sp.n_segs == 0) return ESC_OK;
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
   unsigned long long* offsets = reinterpret_cast<unsigned long long*>(ws + L.offsets);
   unsigned long long* partials = reinterpret_cast<unsigned long long*>(ws + L.partials);
-  sp.tile_offsets = offsets;
+  sp.seg_offsets = offsets;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const unsigned segs = (unsigned)((sp.n_tiles + kScanSeg - 1) / kScanSeg);
-  if (segs > 1) tile_scan_partials<<<segs, kScanThreads, 0, st>>>(d_tile_counts, sp.n_tiles, partials);
-  tile_scan_apply<<<segs, kScanThreads, 0, st>>>(d_tile_counts, sp.n_tiles, partials, offsets);
+  const unsigned segs = (unsigned)((sp.n_segs + kScanSeg - 1) / kScanSeg);
+  if (segs > 1) tile_scan_partials<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials);
+  tile_scan_apply<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, offsets);
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
-  const int64_t want = (sp.n_tiles + kSelWarps - 1) / kSelWarps;  // one warp per tile
+  const int64_t want = (sp.n_segs + 32 * kSelWarps - 1) / (32 * kSelWarps);  // 32 segments per warp
   const int64_t grid = want < (int64_t)sms * 16 ? want : (int64_t)sms * 16;
   sel_compact_kernel<<<(unsigned)grid, kSelWarps * 32, 0, st>>>(sp);
   cudaError_t e = cudaGetLastError();
@@ -683,14 +704,13 @@ int esc_compact(const esc_program_t* prog, const esc_column_t* cols, int32_t nco
   const WsLayout L = ws_layout(nrows);
   if (d_ws == nullptr || ws_bytes < L.total) return fail(ESC_ERR_WORKSPACE, "workspace too small");
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
-  uint32_t* bitmap = reinterpret_cast<uint32_t*>(ws + L.bitmap);
-  uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.counts);
-  int32_t tile_rows = 0;
-  int rc = esc_scan_select(prog, cols, ncols, nrows, d_row_ids, bitmap, counts, &tile_rows, result, d_ws, ws_bytes,
-                           stream);
+  esc_selection_t sel;
+  std::memset(&sel, 0, sizeof(sel));
+  sel.bitmap = reinterpret_cast<uint32_t*>(ws + L.bitmap);
+  sel.seg_counts = reinterpret_cast<uint32_t*>(ws + L.counts);
+  int rc = esc_scan_select(prog, cols, ncols, nrows, d_row_ids, &sel, result, d_ws, ws_bytes, stream);
   if (rc != ESC_OK) return rc;
-  return esc_materialize_selection(bitmap, counts, nrows, tile_rows, cols, ncols, d_row_ids, outs, d_ws, ws_bytes,
-                                   stream);
+  return esc_materialize_selection(&sel, nrows, cols, ncols, d_row_ids, outs, d_ws, ws_bytes, stream);
 }
 
 int esc_compact_onepass(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
@@ -789,6 +809,7 @@ int esc_struct_size(int which) {
     case 4: return (int)sizeof(esc_column_t);
     case 5: return (int)sizeof(esc_result_t);
     case 6: return (int)sizeof(esc_outputs_t);
+    case 7: return (int)sizeof(esc_selection_t);
     default: return -1;
   }
 }

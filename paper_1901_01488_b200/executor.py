@@ -24,6 +24,7 @@ with exact device counts of the sibling prefixes and raises exactly when the ref
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import torch
@@ -115,40 +116,75 @@ def launch_count(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | 
 
 @dataclass
 class Selection:
-    """What the count sub-query recorded on the device: a bitmap over the slice's logical rows
-    and the qualifying rows per tile — enough to materialise without re-evaluating."""
+    """What the count sub-query recorded on the device: a bitmap over the slice's logical rows,
+    the hits per warp segment and — for sparse segments — the hits' values of the captured
+    projected columns; enough to materialise without re-evaluating (or, mostly, re-reading)."""
 
     table: ColumnTable
     count: int
-    bitmap: torch.Tensor
-    tile_counts: torch.Tensor
-    tile_rows: int
+    desc: object                 # N.EscSelection (device pointers)
+    buffers: list                # tensors owning the device memory behind ``desc``
+    captured: dict               # column name -> capture index
+    cols: object                 # the esc_column_t array the scan used (slots of ``captured``)
+    slot_of: dict                # column name -> slot in ``cols``
     nrows: int
     ids: torch.Tensor | None
 
 
-def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int):
-    """K1 + selection outputs; returns (count, [udf fail words], Selection)."""
+# Capture of sparse segments' hits inside the scan is opt-in (ESC_CAPTURE=1): in its generic
+# form it costs the scan more instructions than it saves the gather (DESIGN.md §4).
+_CAPTURE = os.environ.get("ESC_CAPTURE", "0") == "1"
+_CAPTURE_BYTES_LIMIT = 8 << 30
+
+
+def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int, capture=()):
+    """K1 + selection outputs (and capture of ``capture`` columns' sparse hits); returns
+    (count, [udf fail words], Selection)."""
     lib = N.load_library()
     stream = _stream(table.device)
     ws = N.workspace(table.device, stream)
     ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
-    words, tiles = C.c_int64(), C.c_int64()
-    lib.esc_selection_sizes(n, C.byref(words), C.byref(tiles))
-    bitmap = torch.empty(max(words.value, 1), dtype=torch.int32, device=table.device)
-    counts = torch.empty(max(tiles.value, 1), dtype=torch.int32, device=table.device)
-    tile_rows = C.c_int32()
-    cols = cp.column_array()
+    words, segs, cap_entries = C.c_int64(), C.c_int64(), C.c_int64()
+    lib.esc_selection_sizes(n, C.byref(words), C.byref(segs), C.byref(cap_entries))
+    dev = table.device
+    bitmap = torch.empty(max(words.value, 1), dtype=torch.int32, device=dev)
+    counts = torch.empty(max(segs.value, 1), dtype=torch.int32, device=dev)
+    desc = N.EscSelection()
+    desc.bitmap = bitmap.data_ptr()
+    desc.seg_counts = counts.data_ptr()
+    buffers = [bitmap, counts]
+    extra, slot_of = [], dict(cp.slot_of)
+    capture = [table.column(c) for c in dict.fromkeys(capture)] if _CAPTURE else []
+    if ids is not None or sum(c.values.element_size() for c in capture) * cap_entries.value > _CAPTURE_BYTES_LIMIT:
+        capture = []
+    captured = {}
+    for col in capture[: N.MAX_PROJ]:
+        if col.name not in slot_of:
+            if cp.ncols + len(extra) >= N.MAX_COLS:
+                break
+            slot_of[col.name] = cp.ncols + len(extra)
+            extra.append(col)
+        k = len(captured)
+        vals = torch.empty(max(cap_entries.value, 1), dtype=col.values.dtype, device=dev)
+        buffers.append(vals)
+        desc.cap_slot[k] = slot_of[col.name]
+        desc.cap_values[k] = vals.data_ptr()
+        if col.nulls is not None:
+            nb = torch.empty(max(cap_entries.value, 1), dtype=torch.uint8, device=dev)
+            buffers.append(nb)
+            desc.cap_nulls[k] = nb.data_ptr()
+        captured[col.name] = k
+    desc.n_cap = len(captured)
+    cols = cp.column_array(extra)
     ev0 = _ev_start(stream)
-    N.check(lib.esc_scan_select(C.byref(cp.program), cols, cp.ncols, n,
-                                C.c_void_p(ids.data_ptr()) if ids is not None else None,
-                                C.c_void_p(bitmap.data_ptr()), C.c_void_p(counts.data_ptr()), C.byref(tile_rows),
+    N.check(lib.esc_scan_select(C.byref(cp.program), cols, cp.ncols + len(extra), n,
+                                C.c_void_p(ids.data_ptr()) if ids is not None else None, C.byref(desc),
                                 C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
                                 C.c_void_p(stream.cuda_stream)), "esc_scan_select")
     _ev_end(stream, ev0, "select")
     stream.synchronize()
     count, fails = ws.read_result(cp.n_udfs)
-    return count, fails, Selection(table, count, bitmap, counts, int(tile_rows.value), n, ids)
+    return count, fails, Selection(table, count, desc, buffers, captured, cols, slot_of, n, ids)
 
 
 def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int, want_row_ids: bool):
@@ -161,29 +197,39 @@ def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int,
     ws_ptr, ws_bytes = ws.ensure(sel.nrows, stream.cuda_stream)
     if len(proj_cols) > N.MAX_PROJ:
         raise ExecutionError("too many columns for one compaction")
-    cols = (N.EscColumn * max(len(proj_cols), 1))()
+    # projections the scan did not see go after its slots
+    slot_of = dict(sel.slot_of)
+    nscan = len(sel.cols)
+    extra = []
+    for col in proj_cols:
+        if col.name not in slot_of:
+            slot_of[col.name] = nscan + len(extra)
+            extra.append(col)
+    cols = (N.EscColumn * max(nscan + len(extra), 1))()
+    for i in range(nscan):
+        cols[i] = sel.cols[i]
+    for j, col in enumerate(extra):
+        N.require_cuda(col.values, f"column {col.name!r}")
+        cols[nscan + j].data = col.values.data_ptr() if len(col) else None
+        cols[nscan + j].nulls = col.nulls.data_ptr() if col.nulls is not None and len(col) else None
+        cols[nscan + j].dtype = N.dtype_code(col.values)
     outs = N.EscOutputs()
     outs.n_proj = len(proj_cols)
     outs.capacity = capacity
     values, nulls = [], []
     dev = table.device
     for k, col in enumerate(proj_cols):
-        N.require_cuda(col.values, f"column {col.name!r}")
-        cols[k].data = col.values.data_ptr() if len(col) else None
-        cols[k].nulls = col.nulls.data_ptr() if col.nulls is not None and len(col) else None
-        cols[k].dtype = N.dtype_code(col.values)
         v = torch.empty(capacity, dtype=col.values.dtype, device=dev)
         m = torch.empty(capacity, dtype=torch.bool, device=dev) if col.nulls is not None else None
         values.append(v)
         nulls.append(m)
-        outs.slot[k] = k
+        outs.slot[k] = slot_of[col.name]
         outs.out_values[k] = v.data_ptr() if capacity else None
         outs.out_nulls[k] = m.data_ptr() if m is not None and capacity else None
     rows = torch.empty(capacity, dtype=torch.int64, device=dev) if want_row_ids else None
     outs.out_row_ids = rows.data_ptr() if rows is not None and capacity else None
     ev0 = _ev_start(stream)
-    N.check(lib.esc_materialize_selection(C.c_void_p(sel.bitmap.data_ptr()), C.c_void_p(sel.tile_counts.data_ptr()),
-                                          sel.nrows, sel.tile_rows, cols, len(proj_cols),
+    N.check(lib.esc_materialize_selection(C.byref(sel.desc), sel.nrows, cols, nscan + len(extra),
                                           C.c_void_p(sel.ids.data_ptr()) if sel.ids is not None else None,
                                           C.byref(outs), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
                                           C.c_void_p(stream.cuda_stream)), "esc_materialize_selection")
@@ -307,12 +353,13 @@ def _count_with_errors(table, pred, selection=None) -> int:
     return count
 
 
-def select(table: ColumnTable, pred: ex.Expr, selection: RowSelection | None = None) -> Selection:
-    """The count sub-query that also records its selection on the device (one predicate pass);
-    raises the reference's UDF errors."""
+def select(table: ColumnTable, pred: ex.Expr, selection: RowSelection | None = None, capture=()) -> Selection:
+    """The count sub-query that also records its selection on the device (one predicate pass;
+    sparse segments' hits of the ``capture`` columns are captured on the way); raises the
+    reference's UDF errors."""
     cp = compile_predicate(table, pred)
     ids, n = _row_ids(selection if selection is not None else RowSelection(table))
-    count, fails, sel = launch_select(cp, table, ids, n)
+    count, fails, sel = launch_select(cp, table, ids, n, capture)
     if cp.unbound or cp.may_fail:
         raise_udf_errors(table, cp, fails, ids, n)
     return sel
@@ -354,14 +401,14 @@ def materialize(table: ColumnTable, pred: ex.Expr, needed, count: int | None = N
     ``optimizer.py:191-192``): one predicate pass recording the selection, one compaction pass
     over the selection.  ``count`` / ``stage_proj`` are accepted for API stability."""
     del count, stage_proj
-    return materialize_selection(select(table, pred), needed)
+    return materialize_selection(select(table, pred, capture=needed), needed)
 
 
 def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: int):
     """The ESC step: one predicate pass (exact count + selection bitmap), then — only when the
     count fits ``capacity`` (the push-down threshold) — the compaction of ``needed`` from the
     recorded selection.  Returns ``(count, columns or None)``."""
-    sel = select(table, pred)
+    sel = select(table, pred, capture=needed)
     if sel.count > capacity:
         return sel.count, None
     return sel.count, materialize_selection(sel, needed)

@@ -127,7 +127,7 @@ def sharded_esc_subquery(st: ShardedTable, predicate, needed, config: EscConfig,
     n = st.local.row_count
     try:
         if fused:
-            local, fails, sel = executor.launch_select(cp, st.local, None, n)
+            local, fails, sel = executor.launch_select(cp, st.local, None, n, capture=needed)
         else:
             (local, fails), sel = executor.launch_count(cp, st.local, None, n), None
         if cp.unbound or cp.may_fail:

@@ -44,9 +44,9 @@ def test_workspace_sizes_grow_with_rows(native_lib):
     small = native_lib.esc_workspace_bytes(0)
     big = native_lib.esc_workspace_bytes(600_000_000)
     assert small >= 128 and big > small
-    w, t = C.c_int64(), C.c_int64()
-    assert native_lib.esc_selection_sizes(600_000_000, C.byref(w), C.byref(t)) == 0
-    assert w.value * 32 >= 600_000_000 and t.value >= 600_000_000 // 4096
+    w, t, c = C.c_int64(), C.c_int64(), C.c_int64()
+    assert native_lib.esc_selection_sizes(600_000_000, C.byref(w), C.byref(t), C.byref(c)) == 0
+    assert w.value * 32 >= 600_000_000 and t.value >= 600_000_000 // 512 and c.value >= 600_000_000 // 8
 
 
 def test_invalid_arguments_are_reported(native_lib):
