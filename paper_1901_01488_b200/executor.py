@@ -404,10 +404,19 @@ def materialize(table: ColumnTable, pred: ex.Expr, needed, count: int | None = N
     return materialize_selection(select(table, pred, capture=needed), needed)
 
 
+# below this many rows the fused ESC step is ONE launch of the one-pass look-back kernel (a few
+# tiles: the look-back is trivial and launch latency dominates); above, select + gather
+ONEPASS_MAX_ROWS = int(os.environ.get("ESC_ONEPASS_MAX_ROWS", str(1 << 21)))
+
+
 def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: int):
     """The ESC step: one predicate pass (exact count + selection bitmap), then — only when the
     count fits ``capacity`` (the push-down threshold) — the compaction of ``needed`` from the
-    recorded selection.  Returns ``(count, columns or None)``."""
+    recorded selection.  Small tables take the single-launch one-pass kernel with the output
+    bounded by ``capacity``.  Returns ``(count, columns or None)``."""
+    if table.row_count <= ONEPASS_MAX_ROWS:
+        count, cols = materialize_onepass(table, pred, needed, capacity)
+        return count, (cols if count <= capacity else None)
     sel = select(table, pred, capture=needed)
     if sel.count > capacity:
         return sel.count, None
@@ -424,8 +433,13 @@ def materialize_onepass(table: ColumnTable, pred: ex.Expr, needed, capacity: int
     if cp.unbound or cp.may_fail:
         raise_udf_errors(table, cp, fails, ids, n)
     k = min(count, cap)
-    return count, [Column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
-                   for c, v, m in zip(proj, values, nulls)]
+    out = []
+    for c, v, m in zip(proj, values, nulls):
+        if k < cap:  # keep temps compact: copy the hits out of the capacity-sized buffer
+            v = v[:k].clone()
+            m = m[:k].clone() if m is not None else None
+        out.append(Column(c.name, c.kind, v, m, c.dictionary))
+    return count, out
 
 
 def take_column(col: Column, indices) -> Column:
