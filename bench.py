@@ -523,6 +523,7 @@ def run_sweep(args, dev, peak):
             cat.register(t)
             cfg = optimizer.EscConfig(max_selectivity=1.0)
             count_star(t, p)
+            executor.materialize(t, p, wl.project)  # warm-up (JIT compile of the selection shape)
             tc = _time_kernels(lambda: count_star(t, p), 3, dev)
             cms = statistics.mean(x for x, k in tc if k == "count")
             k = count_star(t, p)

@@ -183,9 +183,14 @@ typedef struct {
 } esc_result_t;
 
 /* Output of a compaction: one destination per projected slot. */
+/* esc_outputs_t.flags */
+#define ESC_OUT_SKIP_OVER_CAPACITY 1 /* materialisation: do nothing when the selection's device
+                                        count (esc_selection_t.d_count) exceeds `capacity`, so a
+                                        caller can launch it before reading the count back */
+
 typedef struct {
   int32_t n_proj;
-  int32_t pad;
+  int32_t flags;                       /* ESC_OUT_*                                   */
   int32_t slot[ESC_MAX_PROJ];          /* column slot of each projected column        */
   void* out_values[ESC_MAX_PROJ];      /* device buffers, `capacity` values each      */
   uint8_t* out_nulls[ESC_MAX_PROJ];    /* device bool buffers or NULL                 */
@@ -246,6 +251,8 @@ typedef struct {
   int32_t cap_slot[ESC_MAX_PROJ];   /* in: column slot (of the scan's cols) per capture */
   void* cap_values[ESC_MAX_PROJ];   /* in: esc_selection_sizes().cap_entries values each */
   uint8_t* cap_nulls[ESC_MAX_PROJ]; /* in: null bytes per capture, or NULL                */
+  uint64_t* d_count;                /* in: optional device word; the scan stores the exact count
+                                       there when it completes (ESC_OUT_SKIP_OVER_CAPACITY) */
 } esc_selection_t;
 
 /* Upper bounds of the selection buffers for `nrows` rows: bitmap words, segments (seg_counts
@@ -286,6 +293,11 @@ int esc_set_jit(int mode, int64_t min_rows);
 /* out[0..4] = modules compiled, cache hits, compile failures, total compile microseconds,
  * NVRTC available (0/1). */
 int esc_jit_stats(int64_t* out);
+/* Streamed compaction of dense tiles in esc_materialize_selection: a tile of the selection is
+ * streamed through shared memory (instead of gathered row by row) when it holds at least
+ * tile_rows / div hits.  div <= 0 turns streaming off; default 32 (env ESC_STREAM_DIV).
+ * Returns the previous setting. */
+int esc_set_stream_div(int div);
 /* sizeof() of the ABI structs, for binding checks: 0 program, 1 instr, 2 udf, 3 udf_op,
  * 4 column, 5 result, 6 outputs, 7 selection; -1 for an unknown id. */
 int esc_struct_size(int which);

@@ -77,7 +77,7 @@ class EscResult(C.Structure):
 
 
 class EscOutputs(C.Structure):
-    _fields_ = [("n_proj", C.c_int32), ("pad", C.c_int32), ("slot", C.c_int32 * MAX_PROJ),
+    _fields_ = [("n_proj", C.c_int32), ("flags", C.c_int32), ("slot", C.c_int32 * MAX_PROJ),
                 ("out_values", C.c_void_p * MAX_PROJ), ("out_nulls", C.c_void_p * MAX_PROJ),
                 ("out_row_ids", C.c_void_p), ("capacity", C.c_int64)]
 
@@ -86,10 +86,11 @@ class EscSelection(C.Structure):
     _fields_ = [("bitmap", C.c_void_p), ("seg_counts", C.c_void_p), ("seg_rows", C.c_int32),
                 ("cap_per_seg", C.c_int32), ("n_cap", C.c_int32), ("pad", C.c_int32),
                 ("cap_slot", C.c_int32 * MAX_PROJ), ("cap_values", C.c_void_p * MAX_PROJ),
-                ("cap_nulls", C.c_void_p * MAX_PROJ)]
+                ("cap_nulls", C.c_void_p * MAX_PROJ), ("d_count", C.c_void_p)]
 
 
 SEG_CAPTURED = 0x80000000
+OUT_SKIP_OVER_CAPACITY = 1
 STRUCTS = [EscProgram, EscInstr, EscUdf, EscUdfOp, EscColumn, EscResult, EscOutputs, EscSelection]
 
 # every symbol include/esc.h declares, with its ctypes signature
@@ -120,6 +121,7 @@ _SIGNATURES = {
     "esc_tile_rows": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32]),
     "esc_set_jit": (C.c_int, [C.c_int, C.c_int64]),
     "esc_jit_stats": (C.c_int, [C.POINTER(C.c_int64)]),
+    "esc_set_stream_div": (C.c_int, [C.c_int]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -157,6 +159,12 @@ def load_library(path: str = LIB_PATH):
 def set_jit(mode: int, min_rows: int = -1):
     """0 = interpreter only, 1 = JIT scans of >= min_rows rows, 2 = always JIT."""
     check(load_library().esc_set_jit(int(mode), int(min_rows)), "esc_set_jit")
+
+
+def set_stream_div(div: int) -> int:
+    """Dense-tile rule of the selection compaction (tile streamed when hits >= rows/div; <= 0 off);
+    returns the previous setting."""
+    return int(load_library().esc_set_stream_div(int(div)))
 
 
 def jit_stats() -> dict:
@@ -197,6 +205,10 @@ class _Workspace:
         self.result = torch.zeros(C.sizeof(EscResult), dtype=torch.uint8, pin_memory=True)
         # device-side result block (for NCCL reductions of counts)
         self.dresult = torch.zeros(C.sizeof(EscResult), dtype=torch.uint8, device=device)
+        # device copy of the last selection count (queued compactions check it on the device)
+        self.dcount = torch.zeros(1, dtype=torch.int64, device=device)
+        # reusable selection buffers of the queued ESC step (executor.launch_select(scratch=True))
+        self.scratch: dict = {}
 
     def ensure(self, nrows: int, stream_ptr: int) -> tuple[int, int]:
         lib = load_library()

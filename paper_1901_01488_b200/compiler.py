@@ -64,7 +64,25 @@ class CompiledPredicate:
         return len(self.columns)
 
     def column_array(self, extra=()):
-        """ctypes esc_column_t[] of the slots (+ projection-only columns appended)."""
+        """ctypes esc_column_t[] of the slots (+ projection-only columns appended); cached (the
+        columns are immutable, so their device pointers are too) — callers must not mutate it."""
+        key = tuple(id(c) for c in extra)
+        cache = self.col_array if isinstance(self.col_array, dict) else {}
+        arr = cache.get(key)
+        if arr is None:
+            arr = cache[key] = self._build_column_array(extra)
+            self.col_array = cache
+        return arr
+
+    def tile_rows(self) -> int:
+        """Tile geometry the scan kernels use for this program (cached)."""
+        tr = getattr(self, "_tile_rows", None)
+        if tr is None:
+            tr = self._tile_rows = int(N.load_library().esc_tile_rows(C.byref(self.program), self.column_array(),
+                                                                      self.ncols))
+        return tr
+
+    def _build_column_array(self, extra=()):
         cols = list(self.columns) + list(extra)
         arr = (N.EscColumn * max(len(cols), 1))()
         for i, col in enumerate(cols):

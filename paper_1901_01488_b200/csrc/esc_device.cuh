@@ -15,7 +15,8 @@ namespace esc {
 #endif
 constexpr int kConsumerWarps = ESC_CONSUMER_WARPS;
 constexpr int kChunkRows = 128;  // one warp chunk: 32 lanes x 4 consecutive rows
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;  // narrow tiles (one 4-byte column: 16 KB) need many in flight
+constexpr int kMaxWriters = 8;  // K2 one-pass: one writer warp per ring slot, so <= 8 stages
 constexpr uint32_t kSmemBudget = 200 * 1024;  // dynamic smem for the stage ring
 constexpr int kStatusValueBits = 46;
 constexpr unsigned long long kStatusValueMask = (1ull << kStatusValueBits) - 1;
@@ -25,7 +26,7 @@ constexpr uint32_t kNoNulls = 0xFFFFFFFFu;
 
 template <bool COMPACT>
 struct Layout {
-  static constexpr int kWriters = COMPACT ? kMaxStages : 0;  // K2: one look-back / copy-out warp per ring slot
+  static constexpr int kWriters = COMPACT ? kMaxWriters : 0;  // K2: one look-back / copy-out warp per ring slot
   static constexpr int kFirstConsumer = 1 + kWriters;
   static constexpr int kThreads = (kFirstConsumer + kConsumerWarps) * 32;
 };
@@ -580,12 +581,52 @@ __device__ __noinline__ uint32_t eval_direct(const KParams& p, const RowRef& rr,
   return eval_program<C, false>(p, rr, valid);
 }
 
+// Scan-time capture of a sparse warp segment's hits (esc_selection_t): the hit rows' values of
+// every captured column are copied from the staged tile into the segment's capture slots, in row
+// order.  `excl`/`wtp`: the lane's exclusive / the warp's total per-chunk hit counts (8-bit fields).
+template <int C>
+__device__ __noinline__ void capture_generic(const KParams& p, const RowRef& rr, uint32_t bits, uint32_t excl,
+                                             uint32_t wtp, int64_t seg) {
+  for (int k = 0; k < p.sel.n_cap; ++k) {
+    const KCol& col = p.cols[p.sel.cap_slot[k]];
+    uint8_t* dst = static_cast<uint8_t*>(p.sel.cap_values[k]) + (size_t)seg * p.sel.cap_per_seg * col.width;
+    uint8_t* dn = p.sel.cap_nulls[k] ? p.sel.cap_nulls[k] + (size_t)seg * p.sel.cap_per_seg : nullptr;
+    uint32_t cb = 0;
+    for (int c = 0; c < C; ++c) {
+      uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);
+      cb += (wtp >> (8 * c)) & 0xFFu;
+      uint32_t m = (bits >> (4 * c)) & 0xFu;
+      while (m) {
+        const int bit = 4 * c + __ffs(m) - 1;
+        m &= m - 1;
+        const uint8_t* src = value_ptr(col, rr, bit);
+        switch (col.width) {
+          case 1: dst[r] = *src; break;
+          case 2: reinterpret_cast<uint16_t*>(dst)[r] = *reinterpret_cast<const uint16_t*>(src); break;
+          case 4: reinterpret_cast<uint32_t*>(dst)[r] = *reinterpret_cast<const uint32_t*>(src); break;
+          default:
+            reinterpret_cast<unsigned long long*>(dst)[r] = *reinterpret_cast<const unsigned long long*>(src);
+            break;
+        }
+        if (dn) dn[r] = is_null(col, rr, bit) ? 1 : 0;
+        ++r;
+      }
+    }
+  }
+}
+
 // Predicate evaluator of the ahead-of-time kernels: the opcode interpreter over a staged tile.
-// The JIT tier substitutes a generated straight-line evaluator with the same signature.
+// The JIT tier substitutes a generated straight-line evaluator (and a capture with the captured
+// columns' widths and smem offsets baked in) with the same signatures.
 struct InterpPred {
   template <int C>
   static __device__ __forceinline__ uint32_t eval(const KParams& p, const RowRef& rr, uint32_t valid) {
     return eval_program<C, true>(p, rr, valid);
+  }
+  template <int C>
+  static __device__ __forceinline__ void capture(const KParams& p, const RowRef& rr, uint32_t bits, uint32_t excl,
+                                                 uint32_t wtp, int64_t seg) {
+    capture_generic<C>(p, rr, bits, excl, wtp, seg);
   }
 };
 
@@ -762,6 +803,7 @@ __device__ __forceinline__ void finish_cta(const KParams& p, unsigned long long 
     __threadfence();
     volatile WsHeader* h = p.hdr;
     p.result->count = h->count;
+    if (p.sel_on && p.sel.d_count != nullptr) *p.sel.d_count = h->count;
     for (int i = 0; i < ESC_MAX_UDFS; ++i) {
       p.result->udf_fail[i] = h->fail[i];
       h->fail[i] = ~0ull;
@@ -986,7 +1028,7 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
         uint32_t wtot = pc, flag = 0;
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) wtot += __shfl_xor_sync(0xFFFFFFFFu, wtot, d);
-        if (p.sel.n_cap > 0 && wtot > 0 && wtot <= (uint32_t)(4 * C)) {
+        if (C <= 4 && p.sel.n_cap > 0 && wtot > 0 && wtot <= (uint32_t)(4 * C)) {  // 8-bit chunk fields: C <= 4
           // very sparse segment: capture the hits' projected values now, while they sit in smem
           // (warp-local ranks: per-chunk lane counts in 8-bit fields, one scan ranks every chunk)
           flag = ESC_SEG_CAPTURED;
@@ -1001,35 +1043,7 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
           }
           const uint32_t wtp = __shfl_sync(0xFFFFFFFFu, incl, 31);
           const uint32_t excl = incl - packed;
-          if (bits) {
-            for (int k = 0; k < p.sel.n_cap; ++k) {
-              const KCol& col = p.cols[p.sel.cap_slot[k]];
-              uint8_t* dst = static_cast<uint8_t*>(p.sel.cap_values[k]) + (size_t)seg * p.sel.cap_per_seg * col.width;
-              uint8_t* dn = p.sel.cap_nulls[k] ? p.sel.cap_nulls[k] + (size_t)seg * p.sel.cap_per_seg : nullptr;
-              uint32_t cb = 0;
-#pragma unroll
-              for (int c = 0; c < C; ++c) {
-                uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);
-                cb += (wtp >> (8 * c)) & 0xFFu;
-                uint32_t m = (bits >> (4 * c)) & 0xFu;
-                while (m) {
-                  const int bit = 4 * c + __ffs(m) - 1;
-                  m &= m - 1;
-                  const uint8_t* src = value_ptr(col, rr, bit);
-                  switch (col.width) {
-                    case 1: dst[r] = *src; break;
-                    case 2: reinterpret_cast<uint16_t*>(dst)[r] = *reinterpret_cast<const uint16_t*>(src); break;
-                    case 4: reinterpret_cast<uint32_t*>(dst)[r] = *reinterpret_cast<const uint32_t*>(src); break;
-                    default:
-                      reinterpret_cast<unsigned long long*>(dst)[r] = *reinterpret_cast<const unsigned long long*>(src);
-                      break;
-                  }
-                  if (dn) dn[r] = is_null(col, rr, bit) ? 1 : 0;
-                  ++r;
-                }
-              }
-            }
-          }
+          if (bits) Pred::template capture<C>(p, rr, bits, excl, wtp, seg);
         }
         if (lane == 0) p.sel.seg_counts[seg] = wtot | flag;
       }
@@ -1137,7 +1151,25 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
 // the per-tile counts the scan kernel recorded)
 // ------------------------------------------------------------------------------------------
 constexpr int kScanThreads = 1024;
-constexpr int kScanSeg = 4 * kScanThreads;  // tiles per scan block
+constexpr int kScanSeg = 4 * kScanThreads;  // segments per scan block
+
+// Streamed compaction of dense tiles (sel_stream_kernel): a "stream tile" is `segs_per_tile`
+// consecutive warp segments of the selection.  Dense tiles (>= dense_min hits) are streamed whole
+// through shared memory by TMA; every other segment is compacted by sel_compact_kernel.  Both
+// kernels and the scan that lists the dense tiles apply the same rule to the same counts.
+struct DenseRule {
+  uint32_t dense_min;      // hits that make a stream tile dense (0xFFFFFFFF: streaming off)
+  int32_t segs_per_tile;   // 2, 4 or 8
+  int64_t n_tiles;         // stream tiles over the selection's rows (the last may be partial)
+  uint32_t* dense_list;    // out: dense tile ids (unordered; output positions come from offsets)
+  uint32_t* n_dense;       // out: number of dense tiles
+  const unsigned long long* skip_count;  // ESC_OUT_SKIP_OVER_CAPACITY: the selection's count ...
+  long long skip_capacity;               // ... and the capacity it must not exceed
+};
+
+__device__ __forceinline__ bool skip_materialize(const DenseRule& r) {
+  return r.skip_count != nullptr && (long long)*r.skip_count > r.skip_capacity;
+}
 
 // block-wide exclusive scan of one value per thread; returns the exclusive prefix, *total set
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* sh,
@@ -1169,10 +1201,16 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
   return r;
 }
 
-// partial sums of kScanSeg-tile segments
+// partial sums of kScanSeg-segment blocks (block 0 also resets the dense-tile counter)
 __global__ void __launch_bounds__(kScanThreads) tile_scan_partials(const uint32_t* __restrict__ counts, int64_t n,
-                                                                   unsigned long long* __restrict__ partial) {
+                                                                   unsigned long long* __restrict__ partial,
+                                                                   uint32_t* __restrict__ n_dense,
+                                                                   const unsigned long long* skip_count,
+                                                                   long long skip_capacity) {
+  const bool skip = skip_count != nullptr && (long long)*skip_count > skip_capacity;
   __shared__ unsigned long long sh[33];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_dense = 0;
+  if (skip) return;
   const int64_t base = (int64_t)blockIdx.x * kScanSeg + 4 * threadIdx.x;
   unsigned long long v = 0;
 #pragma unroll
@@ -1182,16 +1220,21 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_partials(const uint32_
   if (threadIdx.x == 0) partial[blockIdx.x] = total;
 }
 
-// exclusive offsets of every tile (carry from the earlier segments' partial sums)
+// exclusive offsets of every segment (carry from the earlier blocks' partial sums), and the list
+// of dense stream tiles
 __global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* __restrict__ counts, int64_t n,
                                                                 const unsigned long long* __restrict__ partial,
-                                                                unsigned long long* __restrict__ offsets) {
+                                                                unsigned long long* __restrict__ offsets,
+                                                                const DenseRule rule) {
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long carry;
-  if (threadIdx.x == 0) {
+  if (skip_materialize(rule)) return;
+  if (threadIdx.x < 32) {  // one warp sums the earlier blocks' partials (independent loads in flight)
     unsigned long long c = 0;
-    for (unsigned b = 0; b < blockIdx.x; ++b) c += partial[b];
-    carry = c;
+    for (unsigned b = threadIdx.x; b < blockIdx.x; b += 32) c += partial[b];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
+    if (threadIdx.x == 0) carry = c;
   }
   const int64_t base = (int64_t)blockIdx.x * kScanSeg + 4 * threadIdx.x;
   uint32_t x[4];
@@ -1202,12 +1245,39 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* 
     v += x[j];
   }
   unsigned long long total;
-  unsigned long long e = block_excl_scan(v, sh, &total) + carry;
+  unsigned long long e = block_excl_scan(v, sh, &total);  // its barriers also publish `carry`
+  e += carry;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (base + j < n) offsets[base + j] = e;
     e += x[j];
   }
+  if (rule.dense_min == 0xFFFFFFFFu) return;
+  // dense stream tiles among this thread's 4 segments (8-segment tiles: thread pairs)
+  const uint32_t pair = (uint32_t)v + __shfl_xor_sync(0xFFFFFFFFu, (uint32_t)v, 1);
+  bool d0 = false, d1 = false;
+  int64_t t0 = -1, t1 = -1;
+  if (rule.segs_per_tile == 8) {
+    if ((threadIdx.x & 1) == 0) { t0 = base / 8; d0 = pair >= rule.dense_min; }
+  } else if (rule.segs_per_tile == 4) {
+    t0 = base / 4; d0 = v >= rule.dense_min;
+  } else {
+    t0 = base / 2; d0 = x[0] + x[1] >= rule.dense_min;
+    t1 = t0 + 1;   d1 = x[2] + x[3] >= rule.dense_min;
+  }
+  d0 = d0 && t0 >= 0 && t0 < rule.n_tiles;
+  d1 = d1 && t1 >= 0 && t1 < rule.n_tiles;
+  // warp-aggregated append
+  const int lane = threadIdx.x & 31;
+  const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, d0), m1 = __ballot_sync(0xFFFFFFFFu, d1);
+  const uint32_t tot = __popc(m0) + __popc(m1);
+  if (tot == 0) return;
+  uint32_t slot0 = 0;
+  if (lane == 0) slot0 = atomicAdd(rule.n_dense, tot);
+  slot0 = __shfl_sync(0xFFFFFFFFu, slot0, 0);
+  const uint32_t lt = (1u << lane) - 1u;
+  if (d0) rule.dense_list[slot0 + __popc(m0 & lt)] = (uint32_t)t0;
+  if (d1) rule.dense_list[slot0 + __popc(m0) + __popc(m1 & lt)] = (uint32_t)t1;
 }
 
 struct SelParams {
@@ -1226,6 +1296,7 @@ struct SelParams {
   const void* cap_values[ESC_MAX_PROJ];
   const uint8_t* cap_nulls[ESC_MAX_PROJ];
   esc_outputs_t outs;
+  DenseRule rule;  // segments of dense stream tiles belong to sel_stream_kernel
 };
 
 constexpr int kSelWarps = 8;
@@ -1246,20 +1317,33 @@ __device__ __forceinline__ void st_bits(int width, void* out, unsigned long long
     default: static_cast<unsigned long long*>(out)[pos] = v; break;
   }
 }
-
-template <typename T>
-__device__ __forceinline__ void copy_run(const void* src, void* dst, uint32_t n, unsigned long long base,
-                                         long long cap, int lane) {
-  const T* s = static_cast<const T*>(src);
-  T* d = static_cast<T*>(dst);
-  for (uint32_t e = lane; e < n; e += 32)
-    if ((long long)(base + e) < cap) d[base + e] = s[e];
+__device__ __forceinline__ unsigned long long ld_w(int width, const void* src, uint32_t e) {
+  switch (width) {
+    case 1: return static_cast<const uint8_t*>(src)[e];
+    case 2: return static_cast<const uint16_t*>(src)[e];
+    case 4: return static_cast<const uint32_t*>(src)[e];
+    default: return static_cast<const unsigned long long*>(src)[e];
+  }
 }
 
-// One warp per segment (seg_rows = 128*C rows = 4*C <= 16 bitmap words).  Captured segments:
-// coalesced copy of the hits the scan captured.  Other segments (and row ids): every bitmap word
-// maps one row per lane, so the gathers of the projected columns and the output writes are both
-// contiguous across the warp.
+// 4 rows of one column: loads first (independent, in flight together), then the stores
+template <typename T>
+__device__ __forceinline__ void gather4(const uint8_t* data, void* out, const bool (&hit)[4], const int64_t (&prow)[4],
+                                        const unsigned long long (&pos)[4]) {
+  const T* src = reinterpret_cast<const T*>(data);
+  T v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = hit[j] ? __ldg(src + prow[j]) : (T)0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<T*>(out)[pos[j]] = v[j];
+}
+
+// One warp per 32 consecutive segments (seg_rows = 128*C rows = 4*C <= 32 bitmap words each):
+//  - captured segments: each LANE copies its own segment's captured hits (<= 4*C per column);
+//  - sparse segments (<= one hit per 32 rows): each lane walks its segment's words, so a warp
+//    keeps 32 independent gathers in flight;
+//  - dense segments: the whole warp, one row per lane of each word (contiguous reads/writes).
+// Segments of dense stream tiles are skipped (sel_stream_kernel writes them).
 __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1267,38 +1351,33 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
   const int W = p.seg_rows / 32;  // words per segment (<= 32)
   const long long cap = p.outs.capacity;
   const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t sparse_max = (uint32_t)W;  // <= one hit per 32 rows on average: one lane per segment
-  // a warp takes 32 consecutive segments: sparse ones are handled one per LANE (32 independent
-  // gathers in flight per warp), dense ones cooperatively, one row per lane of each word
+  const uint32_t sparse_max = (uint32_t)W;
+  if (skip_materialize(p.rule)) return;
   for (int64_t seg0 = gwarp * 32; seg0 < p.n_segs; seg0 += nwarps * 32) {
     const int64_t myseg = seg0 + lane;
     const uint32_t raw = myseg < p.n_segs ? p.seg_counts[myseg] : 0u;
-    const uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
+    uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
+    if (p.rule.dense_min != 0xFFFFFFFFu) {
+      uint32_t ts = cnt;  // hits of my stream tile (segments_per_tile consecutive lanes)
+      for (int d = 1; d < p.rule.segs_per_tile; d <<= 1) ts += __shfl_xor_sync(0xFFFFFFFFu, ts, d);
+      if (ts >= p.rule.dense_min && myseg / p.rule.segs_per_tile < p.rule.n_tiles) cnt = 0;
+    }
     const bool captured = (raw & ESC_SEG_CAPTURED) != 0;
     const unsigned long long myoff = cnt ? p.seg_offsets[myseg] : 0ull;
-    // ---- captured segments: coalesced copy of the hits the scan captured ----
-    uint32_t cap_mask = __ballot_sync(0xFFFFFFFFu, captured && cnt > 0);
-    while (cap_mask) {
-      const int l = __ffs(cap_mask) - 1;
-      cap_mask &= cap_mask - 1;
-      const int64_t seg = seg0 + l;
-      const uint32_t n = __shfl_sync(0xFFFFFFFFu, cnt, l);
-      const unsigned long long base = __shfl_sync(0xFFFFFFFFu, myoff, l);
+    // ---- captured segments: lane-parallel copies of the hits the scan captured ----
+    if (captured && cnt > 0) {
       for (int k = 0; k < p.n_proj; ++k) {
         const int ci = p.cap_index[k];
         if (ci < 0) continue;
         const int w = p.cols[k].width;
-        const uint8_t* src = static_cast<const uint8_t*>(p.cap_values[ci]) + (size_t)seg * p.cap_per_seg * w;
-        switch (w) {
-          case 1: copy_run<uint8_t>(src, p.outs.out_values[k], n, base, cap, lane); break;
-          case 2: copy_run<uint16_t>(src, p.outs.out_values[k], n, base, cap, lane); break;
-          case 4: copy_run<uint32_t>(src, p.outs.out_values[k], n, base, cap, lane); break;
-          default: copy_run<unsigned long long>(src, p.outs.out_values[k], n, base, cap, lane); break;
-        }
+        const uint8_t* src = static_cast<const uint8_t*>(p.cap_values[ci]) + (size_t)myseg * p.cap_per_seg * w;
+        void* dst = p.outs.out_values[k];
+        for (uint32_t e = 0; e < cnt; ++e)
+          if ((long long)(myoff + e) < cap) st_bits(w, dst, myoff + e, ld_w(w, src, e));
         if (p.outs.out_nulls[k] != nullptr) {
-          const uint8_t* ns = p.cap_nulls[ci] ? p.cap_nulls[ci] + (size_t)seg * p.cap_per_seg : nullptr;
-          for (uint32_t e = lane; e < n; e += 32)
-            if ((long long)(base + e) < cap) p.outs.out_nulls[k][base + e] = ns ? ns[e] : 0;
+          const uint8_t* ns = p.cap_nulls[ci] ? p.cap_nulls[ci] + (size_t)myseg * p.cap_per_seg : nullptr;
+          for (uint32_t e = 0; e < cnt; ++e)
+            if ((long long)(myoff + e) < cap) p.outs.out_nulls[k][myoff + e] = ns ? ns[e] : 0;
         }
       }
     }
@@ -1343,22 +1422,233 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
         if (lane >= d) excl += t;
       }
       excl -= pc;
-      for (int i = 0; i < W; ++i) {
-        const uint32_t word = __shfl_sync(0xFFFFFFFFu, mine, i);
-        if (word == 0) continue;
-        const unsigned long long pos = base + __shfl_sync(0xFFFFFFFFu, excl, i) + __popc(word & lt);
-        if (!((word >> lane) & 1u) || (long long)pos >= cap) continue;
-        const int64_t row = (seg * W + i) * 32 + lane;
-        const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
+      // 4 words per batch: each column's loads are issued for all 4 rows before the stores
+      for (int i0 = 0; i0 < W; i0 += 4) {
+        bool hit[4];
+        unsigned long long pos[4];
+        int64_t prow[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + j < W ? i0 + j : 0;
+          const uint32_t word = i0 + j < W ? __shfl_sync(0xFFFFFFFFu, mine, i) : 0u;
+          pos[j] = base + __shfl_sync(0xFFFFFFFFu, excl, i) + __popc(word & lt);
+          hit[j] = ((word >> lane) & 1u) && (long long)pos[j] < cap;
+          const int64_t row = (seg * W + i) * 32 + lane;
+          prow[j] = (hit[j] && p.row_ids) ? __ldg(p.row_ids + row) : row;
+        }
         for (int k = 0; k < p.n_proj; ++k) {
           if (seg_captured && p.cap_index[k] >= 0) continue;
           const KCol& col = p.cols[k];
-          st_bits(col.width, p.outs.out_values[k], pos, ld_bits(col, prow));
-          if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
+          switch (col.width) {
+            case 1: gather4<uint8_t>(col.data, p.outs.out_values[k], hit, prow, pos); break;
+            case 2: gather4<uint16_t>(col.data, p.outs.out_values[k], hit, prow, pos); break;
+            case 4: gather4<uint32_t>(col.data, p.outs.out_values[k], hit, prow, pos); break;
+            default: gather4<unsigned long long>(col.data, p.outs.out_values[k], hit, prow, pos); break;
+          }
+          if (p.outs.out_nulls[k] != nullptr) {
+            uint8_t nb[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) nb[j] = (hit[j] && col.nulls) ? __ldg(col.nulls + prow[j]) : (uint8_t)0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) if (hit[j]) p.outs.out_nulls[k][pos[j]] = nb[j];
+          }
         }
-        if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
+        if (p.outs.out_row_ids != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) if (hit[j]) p.outs.out_row_ids[pos[j]] = prow[j];
+        }
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// streamed compaction of dense tiles: TMA stages the tile's bitmap words, segment offsets and
+// projected columns (+ null bytes) into a shared-memory ring; consumer warps write each hit
+// straight to its final position (contiguous across the lanes of a word).
+// ------------------------------------------------------------------------------------------
+struct StreamParams {
+  const uint32_t* bitmap;
+  const unsigned long long* seg_offsets;
+  const uint32_t* dense_list;
+  const uint32_t* n_dense;
+  int32_t seg_rows;        // 128*C
+  int32_t segs_per_tile;   // 2, 4, 8
+  int32_t tile_rows;       // seg_rows * segs_per_tile
+  int32_t stages;
+  uint32_t stage_bytes;
+  uint32_t tma_bytes;      // bytes the bulk copies of a full tile deliver
+  uint32_t meta_bytes;     // ... of the tail tile (bitmap words + offsets only)
+  int64_t n_full_tiles;    // tiles below this are staged whole; the tail tile reads HBM directly
+  uint32_t off_bitmap;     // stage offset of the tile's bitmap words
+  uint32_t off_offsets;    // stage offset of the tile's segment offsets
+  int32_t n_proj;
+  int32_t width[ESC_MAX_PROJ];
+  const uint8_t* data[ESC_MAX_PROJ];
+  const uint8_t* nulls[ESC_MAX_PROJ];  // staged null bytes when the output wants them, else nullptr
+  uint32_t off_val[ESC_MAX_PROJ];
+  uint32_t off_null[ESC_MAX_PROJ];
+  esc_outputs_t outs;
+};
+
+constexpr int kStreamConsumers = 16;
+
+// Write the hits of `nw` consecutive bitmap words (<= 4) of one warp segment: every lane owns one
+// row per word; the values of each column are loaded for all words first, then stored, so a lane
+// keeps up to 4 loads in flight.  `src(k, row)`: staged smem (tile-local row) or HBM (global row).
+template <bool STAGED>
+__device__ __forceinline__ void stream_words(const StreamParams& p, const uint8_t* st, int64_t row_base,
+                                             const uint32_t (&word)[4], const unsigned long long (&pos)[4],
+                                             int lr0, int lane) {
+  const long long cap = p.outs.capacity;
+  bool hit[4];
+  int lr[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    hit[j] = ((word[j] >> lane) & 1u) && (long long)pos[j] < cap;
+    lr[j] = lr0 + 32 * j + lane;
+  }
+  for (int k = 0; k < p.n_proj; ++k) {
+    const int w = p.width[k];
+    const uint8_t* base = STAGED ? st + p.off_val[k] : p.data[k] + (size_t)row_base * w;
+    void* out = p.outs.out_values[k];
+    if (w == 4) {
+      uint32_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? reinterpret_cast<const uint32_t*>(base)[lr[j]] : 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<uint32_t*>(out)[pos[j]] = v[j];
+    } else if (w == 8) {
+      unsigned long long v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? reinterpret_cast<const unsigned long long*>(base)[lr[j]] : 0ull;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<unsigned long long*>(out)[pos[j]] = v[j];
+    } else if (w == 2) {
+      uint16_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? reinterpret_cast<const uint16_t*>(base)[lr[j]] : (uint16_t)0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<uint16_t*>(out)[pos[j]] = v[j];
+    } else {
+      uint8_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? base[lr[j]] : (uint8_t)0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<uint8_t*>(out)[pos[j]] = v[j];
+    }
+    uint8_t* on = p.outs.out_nulls[k];
+    if (on != nullptr) {
+      const uint8_t* nb = p.nulls[k] == nullptr ? nullptr : (STAGED ? st + p.off_null[k] : p.nulls[k] + row_base);
+      uint8_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = (hit[j] && nb != nullptr) ? nb[lr[j]] : (uint8_t)0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (hit[j]) on[pos[j]] = v[j];
+    }
+  }
+  if (p.outs.out_row_ids != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) if (hit[j]) p.outs.out_row_ids[pos[j]] = row_base + lr[j];
+  }
+}
+
+__global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_kernel(const __grid_constant__ StreamParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int S = p.stages;
+  uint8_t* ring = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+  uint64_t* empty_bar = full_bar + kMaxStages;
+  long long* tile_of = reinterpret_cast<long long*>(empty_bar + kMaxStages);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kStreamConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t nd = *p.n_dense;
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t policy = evict_first_policy();
+      int s = 0;
+      uint32_t ph = 0;
+      for (uint32_t k = blockIdx.x;; k += gridDim.x, s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        if (k >= nd) {
+          tile_of[s] = -1;
+          mbar_arrive(&full_bar[s]);
+          break;
+        }
+        const int64_t tile = p.dense_list[k];
+        const bool full = tile < p.n_full_tiles;  // the tail tile's columns are read from HBM directly
+        tile_of[s] = tile;
+        uint8_t* dst = ring + (size_t)s * p.stage_bytes;
+        const int64_t row0 = tile * p.tile_rows;
+        mbar_arrive_expect_tx(&full_bar[s], full ? p.tma_bytes : p.meta_bytes);
+        bulk_g2s(dst + p.off_bitmap, p.bitmap + row0 / 32, (uint32_t)p.tile_rows / 8, &full_bar[s], policy);
+        bulk_g2s(dst + p.off_offsets, p.seg_offsets + tile * p.segs_per_tile, (uint32_t)p.segs_per_tile * 8,
+                 &full_bar[s], policy);
+        if (full) {
+          for (int k2 = 0; k2 < p.n_proj; ++k2) {
+            const int w = p.width[k2];
+            bulk_g2s(dst + p.off_val[k2], p.data[k2] + (size_t)row0 * w, (uint32_t)p.tile_rows * w, &full_bar[s],
+                     policy);
+            if (p.nulls[k2] != nullptr)
+              bulk_g2s(dst + p.off_null[k2], p.nulls[k2] + row0, (uint32_t)p.tile_rows, &full_bar[s], policy);
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  const int wps = kStreamConsumers / p.segs_per_tile;  // warps per segment (host: <= words per segment)
+  const int seg = cw / wps;
+  const int W = p.seg_rows / 32;
+  const int wpart = W / wps;                            // words this warp writes
+  const int w0 = (cw % wps) * wpart;
+  const uint32_t lt = (1u << lane) - 1u;
+  int s = 0;
+  uint32_t ph = 0;
+  for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
+    mbar_wait(&full_bar[s], ph);
+    const int64_t tile = tile_of[s];
+    if (tile < 0) break;
+    const uint8_t* st = ring + (size_t)s * p.stage_bytes;
+    const uint32_t* bm = reinterpret_cast<const uint32_t*>(st + p.off_bitmap) + seg * W;
+    const unsigned long long base = reinterpret_cast<const unsigned long long*>(st + p.off_offsets)[seg];
+    const uint32_t mine = lane < W ? bm[lane] : 0u;
+    const uint32_t pc = __popc(mine);
+    uint32_t excl = pc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, excl, d);
+      if (lane >= d) excl += t;
+    }
+    excl -= pc;
+    const bool full = tile < p.n_full_tiles;
+    const int64_t row_base = tile * p.tile_rows;
+    for (int i0 = w0; i0 < w0 + wpart; i0 += 4) {
+      uint32_t word[4];
+      unsigned long long pos[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = i0 + j;
+        const bool in = i < w0 + wpart;
+        word[j] = __shfl_sync(0xFFFFFFFFu, mine, in ? i : 0);
+        if (!in) word[j] = 0;
+        pos[j] = base + __shfl_sync(0xFFFFFFFFu, excl, in ? i : 0) + __popc(word[j] & lt);
+      }
+      const int lr0 = seg * p.seg_rows + 32 * i0;
+      if (full) stream_words<true>(p, st, row_base, word, pos, lr0, lane);
+      else stream_words<false>(p, st, row_base, word, pos, lr0, lane);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
   }
 }
 

@@ -85,8 +85,8 @@ struct Entry {
   std::string log;
 };
 std::mutex g_mu;
-std::unordered_map<std::string, Entry> g_cache;        // generated source -> module
-std::unordered_map<std::string, std::string> g_shape;  // shape bytes -> generated source (fast path)
+std::unordered_map<std::string, Entry> g_cache;   // generated source -> module
+std::unordered_map<std::string, Entry*> g_shape;  // shape bytes -> its module (fast path: no codegen)
 
 // Everything the generated evaluator bakes in (opcodes, flags, smem offsets, dtypes, UDF
 // programs) — but not the query constants, which it reads from the kernel parameters.
@@ -104,7 +104,15 @@ std::string shape_key(const KParams& kp, bool compact) {
   k.append(reinterpret_cast<const char*>(kp.udf_ops), sizeof(kp.udf_ops));
   for (int i = 0; i < kp.ncols; ++i) {
     const KCol& c = kp.cols[i];
-    const uint32_t v[4] = {(uint32_t)c.dtype, c.smem_off, c.smem_null_off, c.nulls != nullptr ? 1u : 0u};
+    const uint32_t v[6] = {(uint32_t)c.dtype, c.smem_off, c.smem_null_off, c.nulls != nullptr ? 1u : 0u,
+                           (uint32_t)c.staged, (uint32_t)c.nulls_staged};
+    k.append(reinterpret_cast<const char*>(v), sizeof(v));
+  }
+  // the scan-time capture is baked in too (which columns, where their nulls go)
+  const int ncap = kp.sel_on ? kp.sel.n_cap : 0;
+  k.append(reinterpret_cast<const char*>(&ncap), sizeof(ncap));
+  for (int j = 0; j < ncap; ++j) {
+    const int32_t v[2] = {kp.sel.cap_slot[j], kp.sel.cap_nulls[j] != nullptr ? 1 : 0};
     k.append(reinterpret_cast<const char*>(v), sizeof(v));
   }
   return k;
@@ -320,6 +328,48 @@ Val gen_udf_body(const KParams& kp, int ui, std::ostringstream& o, const std::st
   return stk.back();
 }
 
+// Scan-time capture with the captured columns' types and stage offsets baked in: staged tiles
+// copy each hit's values straight from shared memory; tail tiles keep the generic path.
+void gen_capture(const KParams& kp, std::ostringstream& o) {
+  o << "  template <int C>\n  static __device__ __forceinline__ void capture(const KParams& p, const RowRef& rr, "
+       "uint32_t bits, uint32_t excl, uint32_t wtp, int64_t seg) {\n";
+  const int ncap = kp.sel_on ? kp.sel.n_cap : 0;
+  if (ncap == 0) {
+    o << "    capture_generic<C>(p, rr, bits, excl, wtp, seg);\n  }\n";
+    return;
+  }
+  o << "    if (rr.stage == nullptr) { capture_generic<C>(p, rr, bits, excl, wtp, seg); return; }\n"
+    << "    const uint8_t* st = rr.stage;\n"
+    << "    const size_t base = (size_t)seg * (4 * C);\n";
+  for (int k = 0; k < ncap; ++k) {
+    const KCol& c = kp.cols[kp.sel.cap_slot[k]];
+    o << "    " << ctype_of(c.dtype) << "* cv" << k << " = static_cast<" << ctype_of(c.dtype) << "*>(p.sel.cap_values["
+      << k << "]) + base;\n";
+    if (kp.sel.cap_nulls[k] != nullptr) o << "    uint8_t* cn" << k << " = p.sel.cap_nulls[" << k << "] + base;\n";
+  }
+  o << "    uint32_t cb = 0;\n#pragma unroll\n    for (int c = 0; c < C; ++c) {\n"
+    << "      uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);\n      cb += (wtp >> (8 * c)) & 0xFFu;\n"
+    << "      uint32_t m = (bits >> (4 * c)) & 0xFu;\n      while (m) {\n"
+    << "        const int j = __ffs(m) - 1;\n        m &= m - 1;\n"
+    << "        const int lr = rr.local0 + " << kChunkRows << " * c + j;\n";
+  for (int k = 0; k < ncap; ++k) {
+    const int slot = kp.sel.cap_slot[k];
+    const KCol& c = kp.cols[slot];
+    if (c.staged)
+      o << "        cv" << k << "[r] = *reinterpret_cast<const " << ctype_of(c.dtype) << "*>(st + " << c.smem_off
+        << "u + (size_t)lr * " << c.width << ");\n";
+    else
+      o << "        cv" << k << "[r] = *reinterpret_cast<const " << ctype_of(c.dtype) << "*>(value_ptr(p.cols[" << slot
+        << "], rr, 4 * c + j));\n";
+    if (kp.sel.cap_nulls[k] != nullptr) {
+      if (c.nulls == nullptr) o << "        cn" << k << "[r] = 0;\n";
+      else if (c.nulls_staged) o << "        cn" << k << "[r] = st[" << c.smem_null_off << "u + lr];\n";
+      else o << "        cn" << k << "[r] = is_null(p.cols[" << slot << "], rr, 4 * c + j) ? 1 : 0;\n";
+    }
+  }
+  o << "        ++r;\n      }\n    }\n  }\n";
+}
+
 // The generated evaluator.  Returns false when the program uses something the generator does
 // not specialise (the caller then keeps the interpreter).
 bool gen_pred(const KParams& kp, int C, std::ostringstream& o) {
@@ -410,7 +460,9 @@ bool gen_pred(const KParams& kp, int C, std::ostringstream& o) {
     if (K.neg) o << "      r = ~r;\n";
     o << "      " << acc << " " << comb_stmt(K.combine) << " r;\n    }\n";
   }
-  o << "    return acc0 & valid;\n  }\n};\n";
+  o << "    return acc0 & valid;\n  }\n";
+  gen_capture(kp, o);
+  o << "};\n";
   (void)C;
   return true;
 }
@@ -426,28 +478,29 @@ cudaKernel_t get_kernel(const KParams& kp, bool compact, size_t smem, std::strin
                            ", esc::JitPred>";
   std::lock_guard<std::mutex> g(g_mu);
   const std::string shape = shape_key(kp, compact);
-  auto sh = g_shape.find(shape);
-  if (sh == g_shape.end()) {
-    std::ostringstream pred;
-    if (!gen_pred(kp, kp.chunks, pred)) return nullptr;
-    const std::string src = std::string("#include \"esc_device.cuh\"\nnamespace esc {\n") + pred.str() + "}\n";
-    sh = g_shape.emplace(shape, inst + "\n" + src).first;
-  }
-  const std::string& key = sh->second;
-  const std::string src = key.substr(key.find('\n') + 1);
-  auto it = g_cache.find(key);
-  if (it != g_cache.end()) {
-    if (!it->second.ok) {
-      *why = it->second.log;
+  auto serve = [&](Entry& en) -> cudaKernel_t {
+    if (!en.ok) {
+      *why = en.log;
       return nullptr;
     }
-    if (it->second.smem_configured < (int)smem) {
-      if (cudaFuncSetAttribute(reinterpret_cast<const void*>(it->second.kernel),
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess)
-        it->second.smem_configured = (int)smem;
+    if (en.smem_configured < (int)smem) {
+      if (cudaFuncSetAttribute(reinterpret_cast<const void*>(en.kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) == cudaSuccess)
+        en.smem_configured = (int)smem;
     }
     ++g_hits;
-    return it->second.kernel;
+    return en.kernel;
+  };
+  auto sh = g_shape.find(shape);
+  if (sh != g_shape.end()) return serve(*sh->second);
+  std::ostringstream pred;
+  if (!gen_pred(kp, kp.chunks, pred)) return nullptr;
+  const std::string src = std::string("#include \"esc_device.cuh\"\nnamespace esc {\n") + pred.str() + "}\n";
+  const std::string key = inst + "\n" + src;
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) {
+    g_shape.emplace(shape, &it->second);
+    return serve(it->second);
   }
   Entry e;
   const auto t0 = std::chrono::steady_clock::now();
@@ -494,6 +547,7 @@ cudaKernel_t get_kernel(const KParams& kp, bool compact, size_t smem, std::strin
   if (e.ok) ++g_compiled;
   else ++g_failures;
   auto& slot = g_cache[key] = e;
+  g_shape.emplace(shape, &slot);
   if (!slot.ok) {
     *why = slot.log;
     return nullptr;

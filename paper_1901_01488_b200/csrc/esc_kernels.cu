@@ -108,16 +108,16 @@ size_t status_words(int64_t nrows) {
 }
 
 // Workspace layout: [header][tile status (one-pass K2)][segment offsets u64][scan partials u64]
-//                   [segment counts u32][selection bitmap u32]
+//                   [segment counts u32][selection bitmap u32][dense-tile counter + list u32]
 struct WsLayout {
-  size_t status, offsets, partials, counts, bitmap, total;
+  size_t status, offsets, partials, counts, bitmap, dense, total;
   int64_t max_tiles, bitmap_words;
 };
 WsLayout ws_layout(int64_t nrows) {
   WsLayout L;
   if (nrows < 0) nrows = 0;
   const int64_t t_min = (int64_t)kConsumerWarps * kChunkRows;        // smallest tile (C = 1)
-  const int64_t t_max = 4 * t_min;                                   // largest tile (C = 4)
+  const int64_t t_max = 8 * t_min;                                   // largest tile (C = 8)
   L.max_tiles = ((nrows + t_min - 1) / t_min + 1) * kConsumerWarps;  // warp segments
   L.bitmap_words = ((nrows + t_max - 1) / t_max + 1) * (t_max / 32);  // covers every C's last tile
   const int64_t segs = L.max_tiles / kScanSeg + 2;
@@ -127,7 +127,8 @@ WsLayout ws_layout(int64_t nrows) {
   L.partials = up(L.offsets + (size_t)L.max_tiles * 8);
   L.counts = up(L.partials + (size_t)segs * 8);
   L.bitmap = up(L.counts + (size_t)L.max_tiles * 4);
-  L.total = up(L.bitmap + (size_t)L.bitmap_words * 4);
+  L.dense = up(L.bitmap + (size_t)L.bitmap_words * 4);
+  L.total = up(L.dense + 256 + (size_t)L.max_tiles * 4);
   return L;
 }
 
@@ -365,13 +366,15 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     }
     if (outs->out_row_ids != nullptr) scratch_row += 2;
   }
-  int chunks = 4;
+  // C = 8 (32 rows per lane) only for count/selection scans: narrow tables need big tiles to
+  // stream at full bandwidth; the one-pass compaction packs per-chunk counts in 8-bit fields
+  int chunks = compact || outs != nullptr ? 4 : 8;
   while (chunks > 1 &&
          (uint64_t)kConsumerWarps * kChunkRows * chunks * (per_row + scratch_row) * min_stages > kSmemBudget)
     chunks >>= 1;
   if (const char* e = getenv("ESC_CHUNKS")) {  // tuning override (experiments only)
     const int v = atoi(e);
-    if (v == 1 || v == 2 || v == 4) chunks = v;
+    if (v == 1 || v == 2 || v == 4 || (v == 8 && outs == nullptr)) chunks = v;
   }
   const int tile_rows = kConsumerWarps * kChunkRows * chunks;
   bool fast = compact;
@@ -440,6 +443,7 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     }
     if (g.stages < 1) g.stages = 1;
   }
+  if (outs != nullptr && g.stages > kMaxWriters) g.stages = kMaxWriters;  // one writer warp per slot
   if (outs != nullptr && g.stages < 2) g.stages = 2;  // K2 holds a stage for its writer warp
   return g;
 }
@@ -515,7 +519,8 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
 size_t smem_bytes_for(const KParams& kp) {
   return (size_t)kp.stages * kp.stage_bytes + 4 * kMaxStages * sizeof(uint64_t) + kMaxStages * sizeof(long long) +
          kMaxStages * sizeof(unsigned long long) + kConsumerWarps * sizeof(unsigned long long) +
-         2 * kMaxStages * kConsumerWarps * sizeof(uint32_t) + kMaxStages * sizeof(uint32_t);
+         2 * kMaxStages * kConsumerWarps * sizeof(uint32_t) + kMaxStages * sizeof(uint32_t) +
+         2 * sizeof(uint32_t) + sizeof(unsigned long long);  // s_writers_done[2], s_cta_count
 }
 
 template <int C, bool COMPACT>
@@ -567,10 +572,101 @@ int launch_c(const KParams& kp, cudaStream_t stream) {
 template <bool COMPACT>
 int launch(const KParams& kp, cudaStream_t stream) {
   switch (kp.chunks) {
+    case 8:
+      if constexpr (!COMPACT) return launch_c<8, false>(kp, stream);
+      return fail(ESC_ERR_INVALID, "internal: C=8 tiles are for count/selection scans only");
     case 4: return launch_c<4, COMPACT>(kp, stream);
     case 2: return launch_c<2, COMPACT>(kp, stream);
     default: return launch_c<1, COMPACT>(kp, stream);
   }
+}
+
+// ---- streamed compaction of dense tiles ------------------------------------------------------
+// A stream tile is dense when it holds at least tile_rows / ESC_STREAM_DIV hits (default 32: one
+// hit per bitmap word on average, ~3% selectivity): from there on, reading the tile's projected
+// columns whole through TMA beats sector-granular gathers of the hit rows.
+std::atomic<int> g_stream_div{[] {
+  const char* e = getenv("ESC_STREAM_DIV");
+  return e ? atoi(e) : 32;
+}()};
+
+uint32_t stream_dense_min(int tile_rows) {
+  const int div = g_stream_div.load();
+  if (div <= 0) return 0xFFFFFFFFu;  // streaming off
+  const uint32_t m = (uint32_t)(tile_rows / div);
+  return m > 0 ? m : 1u;
+}
+
+// Stage layout of sel_stream_kernel; false when streaming does not apply (row-id chaining, an
+// unaligned column, nothing fits).  Tiles of 8 segments shrink to 4 or 2 until >= 3 stages fit.
+bool plan_stream(StreamParams& tp, const SelParams& sp, const esc_column_t* cols, const esc_outputs_t* outs,
+                 const esc_selection_t* sel, int64_t nrows, const int64_t* d_row_ids) {
+  std::memset(&tp, 0, sizeof(tp));
+  if (d_row_ids != nullptr || nrows <= 0) return false;
+  if (stream_dense_min(1 << 20) == 0xFFFFFFFFu) return false;
+  if (reinterpret_cast<uintptr_t>(sel->bitmap) % 16 != 0) return false;
+  uint32_t per_row = 0;
+  for (int k = 0; k < outs->n_proj; ++k) {
+    const esc_column_t& c = cols[outs->slot[k]];
+    const int w = dtype_width(c.dtype);
+    if (reinterpret_cast<uintptr_t>(c.data) % 16 != 0) return false;
+    const bool want_nulls = outs->out_nulls[k] != nullptr && c.nulls != nullptr;
+    if (want_nulls && reinterpret_cast<uintptr_t>(c.nulls) % 16 != 0) return false;
+    per_row += w + (want_nulls ? 1 : 0);
+  }
+  tp.seg_rows = sel->seg_rows;
+  int spt = kConsumerWarps;
+  auto stage_for = [&](int s) {
+    const uint32_t rows = (uint32_t)s * (uint32_t)tp.seg_rows;
+    uint32_t b = rows / 8;                 // bitmap words
+    b = (b + 15u) & ~15u;
+    b += 64;                               // <= 8 segment offsets
+    for (int k = 0; k < outs->n_proj; ++k) {
+      const esc_column_t& c = cols[outs->slot[k]];
+      b += rows * dtype_width(c.dtype);
+      if (outs->out_nulls[k] != nullptr && c.nulls != nullptr) b += rows;
+      b = (b + 15u) & ~15u;
+    }
+    return (b + 127u) & ~127u;
+  };
+  const int W = tp.seg_rows / 32;
+  auto warps_ok = [&](int s) { return kStreamConsumers / s <= W; };  // >= 1 word per consumer warp
+  while (spt > 2 && warps_ok(spt >> 1) && stage_for(spt) * 3 > kSmemBudget) spt >>= 1;
+  if (!warps_ok(spt) || stage_for(spt) * 2 > kSmemBudget) return false;
+  (void)per_row;
+  tp.segs_per_tile = spt;
+  tp.tile_rows = spt * tp.seg_rows;
+  const uint32_t rows = (uint32_t)tp.tile_rows;
+  uint32_t off = 0;
+  tp.off_bitmap = off;
+  off += (rows / 8 + 15u) & ~15u;
+  tp.off_offsets = off;
+  off += 64;
+  tp.tma_bytes = rows / 8 + (uint32_t)spt * 8;
+  tp.meta_bytes = tp.tma_bytes;
+  tp.n_proj = outs->n_proj;
+  for (int k = 0; k < outs->n_proj; ++k) {
+    const esc_column_t& c = cols[outs->slot[k]];
+    const int w = dtype_width(c.dtype);
+    tp.width[k] = w;
+    tp.data[k] = static_cast<const uint8_t*>(c.data);
+    tp.off_val[k] = off;
+    off += rows * w;
+    off = (off + 15u) & ~15u;
+    tp.tma_bytes += rows * w;
+    if (outs->out_nulls[k] != nullptr && c.nulls != nullptr) {
+      tp.nulls[k] = c.nulls;
+      tp.off_null[k] = off;
+      off += rows;
+      off = (off + 15u) & ~15u;
+      tp.tma_bytes += rows;
+    }
+  }
+  tp.stage_bytes = (off + 127u) & ~127u;
+  tp.stages = (int)(kSmemBudget / tp.stage_bytes);
+  if (tp.stages > kMaxStages) tp.stages = kMaxStages;
+  (void)sp;
+  return tp.stages >= 2;
 }
 
 }  // namespace
@@ -586,7 +682,8 @@ int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_segme
   const WsLayout L = ws_layout(nrows);
   if (bitmap_words) *bitmap_words = L.bitmap_words;
   if (max_segments) *max_segments = L.max_tiles;
-  if (cap_entries) *cap_entries = (nrows < 0 ? 0 : nrows) / 8 + 16 * 4 * (int64_t)kConsumerWarps * 2;
+  // capture slots: 4*C per segment of 128*C rows (C <= 4), i.e. n/32 plus the tail tile's slack
+  if (cap_entries) *cap_entries = (nrows < 0 ? 0 : nrows) / 32 + 4 * 4 * (int64_t)kConsumerWarps * 2;
   return ESC_OK;
 }
 
@@ -625,6 +722,7 @@ int esc_scan_select(const esc_program_t* prog, const esc_column_t* cols, int32_t
   if (rc != ESC_OK) return rc;
   sel->seg_rows = kChunkRows * kp.chunks;
   sel->cap_per_seg = 4 * kp.chunks;  // segments with <= 4*C hits (~3% of 128*C rows) are captured
+  if (kp.chunks > 4) sel->cap_per_seg = 0;  // (no capture with C = 8 tiles)
   kp.sel_on = 1;
   kp.sel = *sel;
   return launch<false>(kp, static_cast<cudaStream_t>(stream));
@@ -682,12 +780,51 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
   unsigned long long* offsets = reinterpret_cast<unsigned long long*>(ws + L.offsets);
   unsigned long long* partials = reinterpret_cast<unsigned long long*>(ws + L.partials);
   sp.seg_offsets = offsets;
+  // dense stream tiles (no row-id chaining: the staged tile must be the physical rows)
+  static thread_local StreamParams tp;
+  const bool streaming = plan_stream(tp, sp, cols, outs, sel, nrows, d_row_ids);
+  sp.rule.dense_min = 0xFFFFFFFFu;
+  sp.rule.segs_per_tile = 8;
+  sp.rule.n_tiles = 0;
+  sp.rule.n_dense = reinterpret_cast<uint32_t*>(ws + L.dense);
+  sp.rule.dense_list = reinterpret_cast<uint32_t*>(ws + L.dense + 256);
+  sp.rule.skip_count = nullptr;
+  sp.rule.skip_capacity = outs->capacity;
+  if (outs->flags & ESC_OUT_SKIP_OVER_CAPACITY) {
+    if (sel->d_count == nullptr) return fail(ESC_ERR_INVALID, "ESC_OUT_SKIP_OVER_CAPACITY needs sel->d_count");
+    sp.rule.skip_count = reinterpret_cast<const unsigned long long*>(sel->d_count);
+  }
+  if (streaming) {
+    sp.rule.dense_min = stream_dense_min(tp.tile_rows);
+    sp.rule.segs_per_tile = tp.segs_per_tile;
+    sp.rule.n_tiles = (nrows + tp.tile_rows - 1) / tp.tile_rows;
+    tp.n_full_tiles = nrows / tp.tile_rows;
+    tp.dense_list = sp.rule.dense_list;
+    tp.n_dense = sp.rule.n_dense;
+    tp.bitmap = sel->bitmap;
+    tp.seg_offsets = offsets;
+    tp.outs = *outs;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const unsigned segs = (unsigned)((sp.n_segs + kScanSeg - 1) / kScanSeg);
-  if (segs > 1) tile_scan_partials<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials);
-  tile_scan_apply<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, offsets);
+  tile_scan_partials<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, sp.rule.n_dense,
+                                                     sp.rule.skip_count, sp.rule.skip_capacity);
+  tile_scan_apply<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, offsets, sp.rule);
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  if (streaming) {
+    const size_t smem = (size_t)tp.stages * tp.stage_bytes + 2 * kMaxStages * sizeof(uint64_t) +
+                        kMaxStages * sizeof(long long);
+    static thread_local int configured = 0;
+    if (configured < (int)smem) {
+      cudaError_t e = cudaFuncSetAttribute(sel_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      configured = (int)smem;
+    }
+    int64_t tiles = sp.rule.n_tiles;
+    const unsigned grid = (unsigned)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
+    sel_stream_kernel<<<grid, (1 + kStreamConsumers) * 32, smem, st>>>(tp);
+  }
   const int64_t want = (sp.n_segs + 32 * kSelWarps - 1) / (32 * kSelWarps);  // 32 segments per warp
   const int64_t grid = want < (int64_t)sms * 16 ? want : (int64_t)sms * 16;
   sel_compact_kernel<<<(unsigned)grid, kSelWarps * 32, 0, st>>>(sp);
@@ -798,6 +935,12 @@ int esc_jit_stats(int64_t* out) {
   out[3] = jit::g_compile_us.load();
   out[4] = jit::nvrtc().ok ? 1 : 0;
   return ESC_OK;
+}
+
+int esc_set_stream_div(int div) {
+  const int prev = g_stream_div.load();
+  g_stream_div = div;
+  return prev;
 }
 
 int esc_struct_size(int which) {

@@ -131,65 +131,96 @@ class Selection:
     ids: torch.Tensor | None
 
 
-# Capture of sparse segments' hits inside the scan is opt-in (ESC_CAPTURE=1): in its generic
-# form it costs the scan more instructions than it saves the gather.
-_CAPTURE = os.environ.get("ESC_CAPTURE", "0") == "1"
+# Scan-time capture of sparse segments' hits (ESC_CAPTURE=0 turns it off): the scan copies the
+# hits' values of the projected PREDICATE columns — already staged in shared memory — into
+# per-segment slots, so the materialisation copies them instead of re-gathering rows from HBM
+# (DESIGN.md §4).  Projection-only columns are never captured: reading them would put HBM
+# gathers inside the scan.
+_CAPTURE = os.environ.get("ESC_CAPTURE", "1") == "1"
 _CAPTURE_BYTES_LIMIT = 8 << 30
 
 
-def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int, capture=()):
+def set_capture(on: bool) -> bool:
+    """Turn scan-time capture on/off; returns the previous setting (tests, tuning)."""
+    global _CAPTURE
+    prev, _CAPTURE = _CAPTURE, bool(on)
+    return prev
+
+
+def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int, capture=(),
+                  sync: bool = True, d_count: torch.Tensor | None = None, scratch: bool = False):
     """K1 + selection outputs (and capture of ``capture`` columns' sparse hits); returns
-    (count, [udf fail words], Selection)."""
+    (count, [udf fail words], Selection).  ``sync=False`` returns right after the launch with
+    count/fails None (read them with :func:`finish_select`); ``d_count`` (device int64[1])
+    receives the exact count on the device.  ``scratch``: the selection buffers are the
+    workspace's (reused by the next scratch selection on this stream: consume it first)."""
     lib = N.load_library()
     stream = _stream(table.device)
     ws = N.workspace(table.device, stream)
     ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
-    words, segs, cap_entries = C.c_int64(), C.c_int64(), C.c_int64()
-    lib.esc_selection_sizes(n, C.byref(words), C.byref(segs), C.byref(cap_entries))
-    dev = table.device
-    bitmap = torch.empty(max(words.value, 1), dtype=torch.int32, device=dev)
-    counts = torch.empty(max(segs.value, 1), dtype=torch.int32, device=dev)
+    slot_of = cp.slot_of
+    capture = [table.column(c) for c in dict.fromkeys(capture) if c in slot_of] if _CAPTURE else []
+    if capture and (ids is not None or cp.tile_rows() > 4096):
+        capture = []  # no capture through row-id chains or with 32-row-per-lane (narrow) tiles
+    capture = capture[: N.MAX_PROJ]
+    key = (n, tuple((c.values.dtype, c.nulls is not None) for c in capture))
+    hit = ws.scratch.get(key) if scratch else None
+    if hit is None:
+        words, segs, cap_entries = C.c_int64(), C.c_int64(), C.c_int64()
+        lib.esc_selection_sizes(n, C.byref(words), C.byref(segs), C.byref(cap_entries))
+        if sum(c.values.element_size() for c in capture) * cap_entries.value > _CAPTURE_BYTES_LIMIT:
+            capture, key = [], (n, ())
+        dev = table.device
+        buffers = [torch.empty(max(words.value, 1), dtype=torch.int32, device=dev),
+                   torch.empty(max(segs.value, 1), dtype=torch.int32, device=dev)]
+        for col in capture:
+            buffers.append(torch.empty(max(cap_entries.value, 1), dtype=col.values.dtype, device=dev))
+            buffers.append(torch.empty(max(cap_entries.value, 1), dtype=torch.uint8, device=dev)
+                           if col.nulls is not None else None)
+        if scratch:
+            ws.scratch = {key: buffers}  # one live scratch selection per stream
+    else:
+        buffers = hit
     desc = N.EscSelection()
-    desc.bitmap = bitmap.data_ptr()
-    desc.seg_counts = counts.data_ptr()
-    buffers = [bitmap, counts]
-    extra, slot_of = [], dict(cp.slot_of)
-    capture = [table.column(c) for c in dict.fromkeys(capture)] if _CAPTURE else []
-    if ids is not None or sum(c.values.element_size() for c in capture) * cap_entries.value > _CAPTURE_BYTES_LIMIT:
-        capture = []
+    desc.bitmap = buffers[0].data_ptr()
+    desc.seg_counts = buffers[1].data_ptr()
     captured = {}
-    for col in capture[: N.MAX_PROJ]:
-        if col.name not in slot_of:
-            if cp.ncols + len(extra) >= N.MAX_COLS:
-                break
-            slot_of[col.name] = cp.ncols + len(extra)
-            extra.append(col)
-        k = len(captured)
-        vals = torch.empty(max(cap_entries.value, 1), dtype=col.values.dtype, device=dev)
-        buffers.append(vals)
+    for k, col in enumerate(capture):
         desc.cap_slot[k] = slot_of[col.name]
-        desc.cap_values[k] = vals.data_ptr()
-        if col.nulls is not None:
-            nb = torch.empty(max(cap_entries.value, 1), dtype=torch.uint8, device=dev)
-            buffers.append(nb)
-            desc.cap_nulls[k] = nb.data_ptr()
+        desc.cap_values[k] = buffers[2 + 2 * k].data_ptr()
+        nb = buffers[3 + 2 * k]
+        desc.cap_nulls[k] = nb.data_ptr() if nb is not None else None
         captured[col.name] = k
     desc.n_cap = len(captured)
-    cols = cp.column_array(extra)
+    desc.d_count = d_count.data_ptr() if d_count is not None else None
+    cols = cp.column_array()
     ev0 = _ev_start(stream)
-    N.check(lib.esc_scan_select(C.byref(cp.program), cols, cp.ncols + len(extra), n,
+    N.check(lib.esc_scan_select(C.byref(cp.program), cols, cp.ncols, n,
                                 C.c_void_p(ids.data_ptr()) if ids is not None else None, C.byref(desc),
                                 C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
                                 C.c_void_p(stream.cuda_stream)), "esc_scan_select")
     _ev_end(stream, ev0, "select")
+    sel = Selection(table, None, desc, [b for b in buffers if b is not None], captured, cols, dict(slot_of), n, ids)
+    if not sync:
+        return None, None, sel
+    count, fails = finish_select(sel, cp)
+    return count, fails, sel
+
+
+def finish_select(sel: Selection, cp: CompiledPredicate):
+    """Wait for the scan of ``sel`` (and whatever was queued behind it) and read its result."""
+    stream = _stream(sel.table.device)
     stream.synchronize()
-    count, fails = ws.read_result(cp.n_udfs)
-    return count, fails, Selection(table, count, desc, buffers, captured, cols, slot_of, n, ids)
+    count, fails = N.workspace(sel.table.device, stream).read_result(cp.n_udfs)
+    sel.count = count
+    return count, fails
 
 
-def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int, want_row_ids: bool):
+def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int, want_row_ids: bool,
+                                 skip_over_capacity: bool = False):
     """Order-preserving compaction of the selected rows of ``proj_cols`` (and/or their physical
-    row ids) into fresh buffers of ``capacity`` rows."""
+    row ids) into fresh buffers of ``capacity`` rows.  ``skip_over_capacity``: the launch may be
+    queued before the count is known; it does nothing when the count exceeds ``capacity``."""
     lib = N.load_library()
     table = sel.table
     stream = _stream(table.device)
@@ -216,6 +247,7 @@ def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int,
     outs = N.EscOutputs()
     outs.n_proj = len(proj_cols)
     outs.capacity = capacity
+    outs.flags = N.OUT_SKIP_OVER_CAPACITY if skip_over_capacity else 0
     values, nulls = [], []
     dev = table.device
     for k, col in enumerate(proj_cols):
@@ -257,8 +289,11 @@ def launch_compact(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor 
         raise ExecutionError("too many columns for one compaction")
     cols = cp.column_array(extra)
     if stage_proj:
+        staged = (N.EscColumn * len(cols))()
+        C.memmove(staged, cols, C.sizeof(staged))
         for k in range(cp.ncols, cp.ncols + len(extra)):
-            cols[k].flags |= N.COL_STAGE
+            staged[k].flags |= N.COL_STAGE
+        cols = staged
     outs = N.EscOutputs()
     outs.n_proj = len(proj_cols)
     outs.capacity = capacity
@@ -408,19 +443,45 @@ def materialize(table: ColumnTable, pred: ex.Expr, needed, count: int | None = N
 # tiles: the look-back is trivial and launch latency dominates); above, select + gather
 ONEPASS_MAX_ROWS = int(os.environ.get("ESC_ONEPASS_MAX_ROWS", str(1 << 21)))
 
+# the compaction is queued behind the scan (one host round trip per table) when its
+# capacity-sized output buffers stay below this many bytes
+SPECULATE_BYTES = int(os.environ.get("ESC_SPECULATE_BYTES", str(4 << 30)))
+
 
 def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: int):
     """The ESC step: one predicate pass (exact count + selection bitmap), then — only when the
     count fits ``capacity`` (the push-down threshold) — the compaction of ``needed`` from the
-    recorded selection.  Small tables take the single-launch one-pass kernel with the output
-    bounded by ``capacity``.  Returns ``(count, columns or None)``."""
+    recorded selection.  The compaction is queued right behind the scan and checks the count
+    on the device (it does nothing for a table that does not qualify), so the host waits once;
+    the qualifying rows are then trimmed out of the ``capacity``-row buffers.  Small tables take
+    the single-launch one-pass kernel with the output bounded by ``capacity``.  Returns
+    ``(count, columns or None)``."""
     if table.row_count <= ONEPASS_MAX_ROWS:
         count, cols = materialize_onepass(table, pred, needed, capacity)
         return count, (cols if count <= capacity else None)
-    sel = select(table, pred, capture=needed)
-    if sel.count > capacity:
-        return sel.count, None
-    return sel.count, materialize_selection(sel, needed)
+    proj = [table.column(name) for name in needed]
+    row_bytes = sum(c.values.element_size() + (1 if c.nulls is not None else 0) for c in proj)
+    if not (0 < capacity and capacity * max(row_bytes, 1) <= SPECULATE_BYTES):
+        sel = select(table, pred, capture=needed)
+        if sel.count > capacity:
+            return sel.count, None
+        return sel.count, materialize_selection(sel, needed)
+    cp = compile_predicate(table, pred)
+    n = table.row_count
+    ws = N.workspace(table.device, _stream(table.device))
+    _, _, sel = launch_select(cp, table, None, n, capture=needed, sync=False, d_count=ws.dcount, scratch=True)
+    values, nulls, _ = launch_materialize_selection(sel, proj, capacity, want_row_ids=False,
+                                                    skip_over_capacity=True)
+    count, fails = finish_select(sel, cp)
+    if cp.unbound or cp.may_fail:
+        raise_udf_errors(table, cp, fails, None, n)
+    if count > capacity:
+        return count, None
+    out = []
+    for c, v, m in zip(proj, values, nulls):  # trim (stream-ordered copies; the big buffers recycle)
+        out.append(Column(c.name, c.kind, v[:count].clone(), m[:count].clone() if m is not None else None,
+                          c.dictionary))
+    return count, out
 
 
 def materialize_onepass(table: ColumnTable, pred: ex.Expr, needed, capacity: int | None = None):

@@ -46,7 +46,7 @@ def test_workspace_sizes_grow_with_rows(native_lib):
     assert small >= 128 and big > small
     w, t, c = C.c_int64(), C.c_int64(), C.c_int64()
     assert native_lib.esc_selection_sizes(600_000_000, C.byref(w), C.byref(t), C.byref(c)) == 0
-    assert w.value * 32 >= 600_000_000 and t.value >= 600_000_000 // 512 and c.value >= 600_000_000 // 8
+    assert w.value * 32 >= 600_000_000 and t.value >= 600_000_000 // 512 and c.value >= 600_000_000 // 32
 
 
 def test_invalid_arguments_are_reported(native_lib):

@@ -265,3 +265,102 @@ def test_selection_reuse(mixed):
     want = O.materialize(ot, j, ["a"])["a"].values
     assert np.array_equal(a1.to_numpy()[0], want)
     assert np.array_equal(a2.to_numpy()[0], want[:7])
+
+
+# ---- scan-time capture and streamed compaction of dense tiles ---------------------------------
+@pytest.fixture(params=["off", "default", "always"])
+def stream_mode(request, cuda):
+    from paper_1901_01488_b200 import _native as N
+
+    div = {"off": 0, "default": 32, "always": 1 << 30}[request.param]
+    prev = N.set_stream_div(div)
+    yield request.param
+    N.set_stream_div(prev)
+
+
+@pytest.mark.parametrize("capture", [False, True])
+@pytest.mark.parametrize("jit", [0, 2])
+def test_capture_and_stream_paths(mixed, stream_mode, capture, jit):
+    """Every compaction route — captured sparse segments, lane gathers, warp gathers, TMA-streamed
+    dense tiles — yields the oracle's columns, null masks and row ids, in order."""
+    from paper_1901_01488_b200 import _native as N, eval_predicate, executor, materialize
+
+    arrays, t, ot = mixed
+    prev_cap = executor.set_capture(capture)
+    N.set_jit(jit, 0)
+    try:
+        corpus = Corpus(arrays, random.Random(4242 + jit), udfs=("mixy", "lin"))
+        names = ["id", "a", "tag", "f", "val", "big"]
+        for i in range(12):
+            j = corpus.pred()
+            want = _oracle(O.materialize, ot, j, names, UDFS)
+            if want[0] != "ok":
+                continue
+            cols = materialize(t, _pred(j), names)
+            for c in cols:
+                v, m = c.to_numpy()
+                assert np.array_equal(v, want[1][c.name].values), (j, c.name)
+                assert np.array_equal(m, want[1][c.name].nulls), (j, c.name)
+            if i % 4 == 0:
+                got = eval_predicate(t, _pred(j)).to_indices().cpu().numpy()
+                assert np.array_equal(got, O.eval_predicate(ot, j, None, UDFS)), j
+    finally:
+        executor.set_capture(prev_cap)
+        N.set_jit(1, 1 << 22)
+
+
+def test_stream_selectivity_sweep(cuda, stream_mode):
+    """2.4M rows over every selectivity regime (sparse -> fully dense) and mixed widths: the
+    streamed dense tiles and the gathered sparse ones stitch together in row order."""
+    from paper_1901_01488_b200 import ColumnTable, count_star, eval_predicate, expr as ex, materialize
+    from paper_1901_01488_b200.storage import KIND_INT32, KIND_INT64, Column, parse_kind
+
+    n = 2_400_017
+    g = np.random.default_rng(11)
+    x = g.integers(0, 1_000_000, n).astype(np.int32)
+    y = g.integers(0, 1 << 40, n).astype(np.int64)
+    z = g.integers(-100, 100, n).astype(np.int8)
+    h = g.integers(-30000, 30000, n).astype(np.int16)
+    hn = g.random(n) < 0.1
+    t = ColumnTable("t", [Column("x", KIND_INT32, x, device=cuda), Column("y", KIND_INT64, y, device=cuda),
+                          Column("z", parse_kind("INT8"), z, device=cuda),
+                          Column("h", parse_kind("INT16"), np.where(hn, 0, h).astype(np.int16), hn, device=cuda)])
+    for hi in (99, 9_999, 29_999, 99_999, 499_999, 899_999, 999_999):
+        p = ex.Range(ex.ColumnRef("t", "x"), 0, hi)
+        want = np.flatnonzero(x <= hi)
+        assert count_star(t, p) == want.size
+        cx, cy, cz, ch = materialize(t, p, ["x", "y", "z", "h"])
+        assert np.array_equal(cx.values.cpu().numpy(), x[want])
+        assert np.array_equal(cy.values.cpu().numpy(), y[want])
+        assert np.array_equal(cz.values.cpu().numpy(), z[want])
+        hv, hm = ch.to_numpy()
+        assert np.array_equal(hm, hn[want])
+        assert np.array_equal(hv, np.where(hn, 0, h)[want])
+        got = eval_predicate(t, p).to_indices().cpu().numpy()
+        assert np.array_equal(got, want)
+
+
+def test_queued_compaction_checks_count_on_device(cuda):
+    """count_and_materialize queues the compaction behind the scan with a device-side capacity
+    check: a qualifying table is materialised exactly, an overflowing one yields no temp and its
+    (skipped) compaction leaves nothing behind; both match the oracle's counts."""
+    from paper_1901_01488_b200 import ColumnTable, executor, expr as ex
+    from paper_1901_01488_b200.storage import KIND_INT32, KIND_INT64, Column
+
+    n = 3_000_001
+    g = np.random.default_rng(17)
+    x = g.integers(0, 100_000, n).astype(np.int32)
+    y = g.integers(-(1 << 40), 1 << 40, n).astype(np.int64)
+    t = ColumnTable("t", [Column("x", KIND_INT32, x, device=cuda), Column("y", KIND_INT64, y, device=cuda)])
+    for hi in (9, 999, 19_999, 60_000):
+        p = ex.Range(ex.ColumnRef("t", "x"), 0, hi)
+        want = np.flatnonzero(x <= hi)
+        for cap in (want.size - 1, want.size, n // 5):
+            count, cols = executor.count_and_materialize(t, p, ["y", "x"], cap)
+            assert count == want.size
+            if want.size > cap:
+                assert cols is None
+                continue
+            cy, cx = cols
+            assert np.array_equal(cy.values.cpu().numpy(), y[want])
+            assert np.array_equal(cx.values.cpu().numpy(), x[want])
