@@ -280,6 +280,12 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
 int esc_gather(const esc_column_t* col, const int64_t* d_idx, int64_t n, void* out_values,
                uint8_t* out_nulls, void* stream);
 
+/* dst[i] <- src[i] (bytes[i] bytes) for n <= ESC_MAX_REGIONS device regions, in ONE launch: the
+ * trim of capacity-sized compaction outputs to their exact row counts (temp-table registration,
+ * storage.py:344-352, without one copy launch per column). */
+#define ESC_MAX_REGIONS 72
+int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const int64_t* bytes, void* stream);
+
 /* ---- misc ------------------------------------------------------------------------------- */
 
 const char* esc_last_error(void);
@@ -290,6 +296,9 @@ int esc_device_sm_count(void);
  * mode 0 = off (interpreter only), 1 = auto (scans of >= min_rows rows; default 2^22),
  * 2 = always; min_rows < 0 keeps the current threshold. */
 int esc_set_jit(int mode, int64_t min_rows);
+/* Compile the JIT tier's device sources (every kernel instantiation it emits, with a trivial
+ * evaluator) through NVRTC; needs no device.  ESC_OK, or ESC_ERR_UNSUPPORTED with the log. */
+int esc_jit_selftest(void);
 /* out[0..4] = modules compiled, cache hits, compile failures, total compile microseconds,
  * NVRTC available (0/1). */
 int esc_jit_stats(int64_t* out);

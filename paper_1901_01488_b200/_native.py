@@ -121,7 +121,9 @@ _SIGNATURES = {
     "esc_tile_rows": (C.c_int, [C.POINTER(EscProgram), C.POINTER(EscColumn), C.c_int32]),
     "esc_set_jit": (C.c_int, [C.c_int, C.c_int64]),
     "esc_jit_stats": (C.c_int, [C.POINTER(C.c_int64)]),
+    "esc_jit_selftest": (C.c_int, []),
     "esc_set_stream_div": (C.c_int, [C.c_int]),
+    "esc_copy_regions": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -207,7 +209,7 @@ class _Workspace:
         self.dresult = torch.zeros(C.sizeof(EscResult), dtype=torch.uint8, device=device)
         # device copy of the last selection count (queued compactions check it on the device)
         self.dcount = torch.zeros(1, dtype=torch.int64, device=device)
-        # reusable selection buffers of the queued ESC step (executor.launch_select(scratch=True))
+        # the queued ESC step's cached launch plan (executor._step_plan)
         self.scratch: dict = {}
 
     def ensure(self, nrows: int, stream_ptr: int) -> tuple[int, int]:

@@ -1652,6 +1652,31 @@ __global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_ker
   }
 }
 
+// ---- batched region copy (esc_copy_regions): blockIdx.y = region -----------------------------
+struct CopyRegions {
+  int32_t n;
+  uint8_t* dst[ESC_MAX_REGIONS];
+  const uint8_t* src[ESC_MAX_REGIONS];
+  long long bytes[ESC_MAX_REGIONS];
+};
+
+__global__ void __launch_bounds__(256) copy_regions_kernel(const __grid_constant__ CopyRegions p) {
+  const int r = blockIdx.y;
+  uint8_t* d = p.dst[r];
+  const uint8_t* s = p.src[r];
+  const long long nb = p.bytes[r];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (((reinterpret_cast<unsigned long long>(d) | reinterpret_cast<unsigned long long>(s)) & 15ull) == 0) {
+    const long long nv = nb >> 4;
+    for (long long i = t0; i < nv; i += stride)
+      reinterpret_cast<uint4*>(d)[i] = __ldg(reinterpret_cast<const uint4*>(s) + i);
+    for (long long i = (nv << 4) + t0; i < nb; i += stride) d[i] = s[i];
+  } else {
+    for (long long i = t0; i < nb; i += stride) d[i] = s[i];
+  }
+}
+
 // gather: out[i] = col[idx[i]]
 template <typename T>
 __global__ void gather_kernel(const T* __restrict__ src, const uint8_t* __restrict__ nulls,

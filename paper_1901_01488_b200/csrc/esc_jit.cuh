@@ -555,4 +555,39 @@ cudaKernel_t get_kernel(const KParams& kp, bool compact, size_t smem, std::strin
   return slot.kernel;
 }
 
+// Compile the embedded device sources with a trivial evaluator for every kernel instantiation
+// the JIT tier emits (no device needed: NVRTC only).  Returns "" on success, else the log.
+std::string selftest() {
+  Nvrtc& nv = nvrtc();
+  if (!nv.ok) return nv.why.empty() ? "NVRTC unavailable" : nv.why;
+  const char* src =
+      "#include \"esc_device.cuh\"\nnamespace esc {\nstruct JitPred {\n"
+      "  template <int C> static __device__ __forceinline__ uint32_t eval(const KParams& p, const RowRef& rr, "
+      "uint32_t valid) { return eval_program<C, true>(p, rr, valid); }\n"
+      "  template <int C> static __device__ __forceinline__ void capture(const KParams& p, const RowRef& rr, "
+      "uint32_t bits, uint32_t excl, uint32_t wtp, int64_t seg) { capture_generic<C>(p, rr, bits, excl, wtp, seg); }\n"
+      "};\n}\n";
+  nvrtcProgram prog;
+  const char* headers[] = {kEscHeaderSrc, kEscDeviceSrc};
+  const char* names[] = {"esc.h", "esc_device.cuh"};
+  if (nv.create(&prog, src, "esc_jit_selftest.cu", 2, headers, names) != NVRTC_SUCCESS) return "nvrtcCreateProgram failed";
+  const char* insts[] = {"esc::esc_scan_kernel<1, false, esc::JitPred>", "esc::esc_scan_kernel<4, false, esc::JitPred>",
+                         "esc::esc_scan_kernel<8, false, esc::JitPred>", "esc::esc_scan_kernel<4, true, esc::JitPred>"};
+  for (const char* i : insts) nv.add_name(prog, i);
+  const std::string warps = "-DESC_CONSUMER_WARPS=" + std::to_string(kConsumerWarps);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-fmad=false", "-lineinfo",
+                        "--device-as-default-execution-space", "-DESC_JIT=1", warps.c_str()};
+  const nvrtcResult rc = nv.compile(prog, 7, opts);
+  std::string out;
+  if (rc != NVRTC_SUCCESS) {
+    size_t ls = 0;
+    nv.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    if (ls) nv.log(prog, &log[0]);
+    out = "NVRTC: " + log;
+  }
+  nv.destroy(&prog);
+  return out;
+}
+
 }  // namespace jit

@@ -914,6 +914,34 @@ int esc_gather(const esc_column_t* col, const int64_t* d_idx, int64_t n, void* o
   return ESC_OK;
 }
 
+int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const int64_t* bytes, void* stream) {
+  if (n < 0 || n > ESC_MAX_REGIONS) return fail(ESC_ERR_INVALID, "region count out of range");
+  if (n == 0) return ESC_OK;
+  if (dst == nullptr || src == nullptr || bytes == nullptr) return fail(ESC_ERR_INVALID, "null region arrays");
+  static thread_local CopyRegions cr;
+  cr.n = n;
+  long long most = 0;
+  for (int i = 0; i < n; ++i) {
+    if (bytes[i] < 0) return fail(ESC_ERR_INVALID, "negative region size");
+    if (bytes[i] > 0 && (dst[i] == nullptr || src[i] == nullptr)) return fail(ESC_ERR_INVALID, "null region");
+    cr.dst[i] = static_cast<uint8_t*>(dst[i]);
+    cr.src[i] = static_cast<const uint8_t*>(src[i]);
+    cr.bytes[i] = bytes[i];
+    most = std::max(most, (long long)bytes[i]);
+  }
+  if (most == 0) return ESC_OK;
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  long long bx = (most / 16 + 255) / 256;
+  const long long cap = std::max(1ll, (long long)sms * 8 / n);
+  if (bx > cap) bx = cap;
+  if (bx < 1) bx = 1;
+  copy_regions_kernel<<<dim3((unsigned)bx, (unsigned)n), 256, 0, static_cast<cudaStream_t>(stream)>>>(cr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("copy launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
 const char* esc_last_error(void) { return g_last_error.c_str(); }
 
 int esc_abi_version(void) { return ESC_ABI_VERSION; }
@@ -924,6 +952,12 @@ int esc_set_jit(int mode, int64_t min_rows) {
   if (mode < 0 || mode > 2) return fail(ESC_ERR_INVALID, "JIT mode must be 0, 1 or 2");
   jit::g_mode = mode;
   if (min_rows >= 0) jit::g_min_rows = min_rows;
+  return ESC_OK;
+}
+
+int esc_jit_selftest(void) {
+  const std::string log = jit::selftest();
+  if (!log.empty()) return fail(ESC_ERR_UNSUPPORTED, log);
   return ESC_OK;
 }
 

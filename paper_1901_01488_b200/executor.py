@@ -148,12 +148,11 @@ def set_capture(on: bool) -> bool:
 
 
 def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor | None, n: int, capture=(),
-                  sync: bool = True, d_count: torch.Tensor | None = None, scratch: bool = False):
+                  sync: bool = True, d_count: torch.Tensor | None = None):
     """K1 + selection outputs (and capture of ``capture`` columns' sparse hits); returns
     (count, [udf fail words], Selection).  ``sync=False`` returns right after the launch with
     count/fails None (read them with :func:`finish_select`); ``d_count`` (device int64[1])
-    receives the exact count on the device.  ``scratch``: the selection buffers are the
-    workspace's (reused by the next scratch selection on this stream: consume it first)."""
+    receives the exact count on the device."""
     lib = N.load_library()
     stream = _stream(table.device)
     ws = N.workspace(table.device, stream)
@@ -163,24 +162,17 @@ def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor |
     if capture and (ids is not None or cp.tile_rows() > 4096):
         capture = []  # no capture through row-id chains or with 32-row-per-lane (narrow) tiles
     capture = capture[: N.MAX_PROJ]
-    key = (n, tuple((c.values.dtype, c.nulls is not None) for c in capture))
-    hit = ws.scratch.get(key) if scratch else None
-    if hit is None:
-        words, segs, cap_entries = C.c_int64(), C.c_int64(), C.c_int64()
-        lib.esc_selection_sizes(n, C.byref(words), C.byref(segs), C.byref(cap_entries))
-        if sum(c.values.element_size() for c in capture) * cap_entries.value > _CAPTURE_BYTES_LIMIT:
-            capture, key = [], (n, ())
-        dev = table.device
-        buffers = [torch.empty(max(words.value, 1), dtype=torch.int32, device=dev),
-                   torch.empty(max(segs.value, 1), dtype=torch.int32, device=dev)]
-        for col in capture:
-            buffers.append(torch.empty(max(cap_entries.value, 1), dtype=col.values.dtype, device=dev))
-            buffers.append(torch.empty(max(cap_entries.value, 1), dtype=torch.uint8, device=dev)
-                           if col.nulls is not None else None)
-        if scratch:
-            ws.scratch = {key: buffers}  # one live scratch selection per stream
-    else:
-        buffers = hit
+    words, segs, cap_entries = C.c_int64(), C.c_int64(), C.c_int64()
+    lib.esc_selection_sizes(n, C.byref(words), C.byref(segs), C.byref(cap_entries))
+    if sum(c.values.element_size() for c in capture) * cap_entries.value > _CAPTURE_BYTES_LIMIT:
+        capture = []
+    dev = table.device
+    buffers = [torch.empty(max(words.value, 1), dtype=torch.int32, device=dev),
+               torch.empty(max(segs.value, 1), dtype=torch.int32, device=dev)]
+    for col in capture:
+        buffers.append(torch.empty(max(cap_entries.value, 1), dtype=col.values.dtype, device=dev))
+        buffers.append(torch.empty(max(cap_entries.value, 1), dtype=torch.uint8, device=dev)
+                       if col.nulls is not None else None)
     desc = N.EscSelection()
     desc.bitmap = buffers[0].data_ptr()
     desc.seg_counts = buffers[1].data_ptr()
@@ -205,6 +197,41 @@ def launch_select(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor |
         return None, None, sel
     count, fails = finish_select(sel, cp)
     return count, fails, sel
+
+
+def _plan_selection(cp: CompiledPredicate, table: ColumnTable, n: int, capture, ws):
+    """Selection buffers + descriptor for a step plan (allocated, not launched)."""
+    lib = N.load_library()
+    slot_of = cp.slot_of
+    cap_cols = [table.column(c) for c in dict.fromkeys(capture) if c in slot_of] if _CAPTURE else []
+    if cp.tile_rows() > 4096:
+        cap_cols = []
+    cap_cols = cap_cols[: N.MAX_PROJ]
+    words, segs, cap_entries = C.c_int64(), C.c_int64(), C.c_int64()
+    lib.esc_selection_sizes(n, C.byref(words), C.byref(segs), C.byref(cap_entries))
+    if sum(c.values.element_size() for c in cap_cols) * cap_entries.value > _CAPTURE_BYTES_LIMIT:
+        cap_cols = []
+    dev = table.device
+    buffers = [torch.empty(max(words.value, 1), dtype=torch.int32, device=dev),
+               torch.empty(max(segs.value, 1), dtype=torch.int32, device=dev)]
+    desc = N.EscSelection()
+    desc.bitmap = buffers[0].data_ptr()
+    desc.seg_counts = buffers[1].data_ptr()
+    captured = {}
+    for k, col in enumerate(cap_cols):
+        vals = torch.empty(max(cap_entries.value, 1), dtype=col.values.dtype, device=dev)
+        buffers.append(vals)
+        desc.cap_slot[k] = slot_of[col.name]
+        desc.cap_values[k] = vals.data_ptr()
+        if col.nulls is not None:
+            nb = torch.empty(max(cap_entries.value, 1), dtype=torch.uint8, device=dev)
+            buffers.append(nb)
+            desc.cap_nulls[k] = nb.data_ptr()
+        captured[col.name] = k
+    desc.n_cap = len(captured)
+    desc.d_count = ws.dcount.data_ptr()
+    return None, None, Selection(table, None, desc, buffers, captured, cp.column_array(), dict(slot_of), n, None)
+
 
 
 def finish_select(sel: Selection, cp: CompiledPredicate):
@@ -446,6 +473,8 @@ ONEPASS_MAX_ROWS = int(os.environ.get("ESC_ONEPASS_MAX_ROWS", str(1 << 21)))
 # the compaction is queued behind the scan (one host round trip per table) when its
 # capacity-sized output buffers stay below this many bytes
 SPECULATE_BYTES = int(os.environ.get("ESC_SPECULATE_BYTES", str(4 << 30)))
+# device bytes the cached step plans (selection + capacity-sized output buffers) may hold per stream
+STEP_PLAN_BYTES = int(os.environ.get("ESC_STEP_PLAN_BYTES", str(8 << 30)))
 
 
 def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: int):
@@ -466,21 +495,126 @@ def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: i
         if sel.count > capacity:
             return sel.count, None
         return sel.count, materialize_selection(sel, needed)
+    return _queued_step(table, pred, proj, capacity)
+
+
+@dataclass
+class _StepPlan:
+    """Everything one queued ESC step launches with, built once per (predicate, table, columns,
+    capacity) and kept in the stream's workspace: the selection and its buffers, the
+    capacity-sized compaction outputs and the argument structs (the host only re-issues)."""
+
+    key: tuple
+    cp: CompiledPredicate         # held: keeps id(cp) in ``key`` unique
+    sel: Selection
+    outs: object
+    out_values: list
+    out_nulls: list
+    mat_cols: object
+    mat_ncols: int
+    nbytes: int = 0
+
+
+def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: int, ws) -> _StepPlan:
+    key = (id(cp), id(table), tuple(c.name for c in proj), capacity)
+    plans = ws.scratch.setdefault("plans", {})
+    plan = plans.pop(key, None)
+    if plan is not None:
+        plans[key] = plan  # most recently used last
+        return plan
+    n = table.row_count
+    _, _, sel = _plan_selection(cp, table, n, [c.name for c in proj], ws)
+    slot_of = dict(sel.slot_of)
+    nscan = len(sel.cols)
+    extra = [c for c in proj if c.name not in slot_of]
+    for j, c in enumerate(extra):
+        slot_of[c.name] = nscan + j
+    cols = (N.EscColumn * max(nscan + len(extra), 1))()
+    for i in range(nscan):
+        cols[i] = sel.cols[i]
+    for j, col in enumerate(extra):
+        cols[nscan + j].data = col.values.data_ptr() if len(col) else None
+        cols[nscan + j].nulls = col.nulls.data_ptr() if col.nulls is not None and len(col) else None
+        cols[nscan + j].dtype = N.dtype_code(col.values)
+    outs = N.EscOutputs()
+    outs.n_proj = len(proj)
+    outs.capacity = capacity
+    outs.flags = N.OUT_SKIP_OVER_CAPACITY
+    values, nulls = [], []
+    for k, col in enumerate(proj):
+        v = torch.empty(capacity, dtype=col.values.dtype, device=table.device)
+        m = torch.empty(capacity, dtype=torch.bool, device=table.device) if col.nulls is not None else None
+        values.append(v)
+        nulls.append(m)
+        outs.slot[k] = slot_of[col.name]
+        outs.out_values[k] = v.data_ptr()
+        outs.out_nulls[k] = m.data_ptr() if m is not None else None
+    plan = _StepPlan(key, cp, sel, outs, values, nulls, cols, nscan + len(extra))
+    plan.nbytes = sum(b.numel() * b.element_size() for b in [*sel.buffers, *values, *[m for m in nulls if m is not None]])
+    plans[key] = plan
+    while len(plans) > 1 and sum(p.nbytes for p in plans.values()) > STEP_PLAN_BYTES:
+        plans.pop(next(iter(plans)))  # evict least recently used
+    return plan
+
+
+def release_step_plans(device: torch.device | None = None):
+    """Drop the cached step plans (and their device buffers) of the current stream."""
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    N.workspace(dev, torch.cuda.current_stream(dev)).scratch.pop("plans", None)
+
+
+def _queued_step(table: ColumnTable, pred: ex.Expr, proj: list, capacity: int):
+    """Scan + compaction queued back to back (the compaction checks the count on the device),
+    one host wait, then ONE batched copy trims the qualifying rows out of the plan's buffers."""
     cp = compile_predicate(table, pred)
     n = table.row_count
-    ws = N.workspace(table.device, _stream(table.device))
-    _, _, sel = launch_select(cp, table, None, n, capture=needed, sync=False, d_count=ws.dcount, scratch=True)
-    values, nulls, _ = launch_materialize_selection(sel, proj, capacity, want_row_ids=False,
-                                                    skip_over_capacity=True)
-    count, fails = finish_select(sel, cp)
+    lib = N.load_library()
+    stream = _stream(table.device)
+    ws = N.workspace(table.device, stream)
+    ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
+    plan = _step_plan(cp, table, proj, capacity, ws)
+    sp = C.c_void_p(stream.cuda_stream)
+    ev0 = _ev_start(stream)
+    N.check(lib.esc_scan_select(C.byref(cp.program), cp.column_array(), cp.ncols, n, None, C.byref(plan.sel.desc),
+                                C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
+            "esc_scan_select")
+    _ev_end(stream, ev0, "select")
+    ev0 = _ev_start(stream)
+    N.check(lib.esc_materialize_selection(C.byref(plan.sel.desc), n, plan.mat_cols, plan.mat_ncols, None,
+                                          C.byref(plan.outs), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
+            "esc_materialize_selection")
+    _ev_end(stream, ev0, "materialize")
+    stream.synchronize()
+    count, fails = ws.read_result(cp.n_udfs)
     if cp.unbound or cp.may_fail:
         raise_udf_errors(table, cp, fails, None, n)
     if count > capacity:
         return count, None
-    out = []
-    for c, v, m in zip(proj, values, nulls):  # trim (stream-ordered copies; the big buffers recycle)
-        out.append(Column(c.name, c.kind, v[:count].clone(), m[:count].clone() if m is not None else None,
-                          c.dictionary))
+    # exact-size temp columns: one allocation, one batched copy launch
+    regions = []
+    for v, m in zip(plan.out_values, plan.out_nulls):
+        regions.append((v, count * v.element_size()))
+        if m is not None:
+            regions.append((m, count))
+    offs, total = [], 0
+    for _, nb in regions:
+        offs.append(total)
+        total += (nb + 255) & ~255
+    buf = torch.empty(max(total, 1), dtype=torch.uint8, device=table.device)
+    k = len(regions)
+    dst = (C.c_void_p * k)(*[buf.data_ptr() + o for o in offs])
+    src = (C.c_void_p * k)(*[t.data_ptr() for t, _ in regions])
+    nbytes = (C.c_int64 * k)(*[nb for _, nb in regions])
+    N.check(lib.esc_copy_regions(k, dst, src, nbytes, sp), "esc_copy_regions")
+    out, r = [], 0
+    for c, v, m in zip(proj, plan.out_values, plan.out_nulls):
+        vv = buf[offs[r]: offs[r] + count * v.element_size()].view(v.dtype)
+        r += 1
+        mm = None
+        if m is not None:
+            mm = buf[offs[r]: offs[r] + count].view(torch.bool)
+            r += 1
+        out.append(Column(c.name, c.kind, vv, mm, c.dictionary))
     return count, out
 
 

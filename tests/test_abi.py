@@ -81,3 +81,13 @@ def test_kernels_refuse_cpu_tensors():
     t = ColumnTable("t", [Column("a", KIND_INT32, np.arange(10, dtype=np.int32), device="cpu")])
     with pytest.raises(NativeUnavailable):
         count_star(t, ex.Comparison(ex.ColumnRef("t", "a"), "<", 5))
+
+
+def test_jit_sources_compile_with_nvrtc(native_lib):
+    """The JIT tier hands the embedded esc.h + esc_device.cuh to NVRTC at run time; compile every
+    kernel instantiation it emits here (NVRTC needs no device) so a source NVRTC rejects never
+    reaches a GPU box as a silent fall-back to the interpreter."""
+    rc = native_lib.esc_jit_selftest()
+    if rc == 4 and b"unavailable" in native_lib.esc_last_error().lower():
+        pytest.skip("NVRTC not installed")
+    assert rc == 0, native_lib.esc_last_error().decode(errors="replace")[:4000]
