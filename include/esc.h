@@ -286,6 +286,69 @@ int esc_gather(const esc_column_t* col, const int64_t* d_idx, int64_t n, void* o
 #define ESC_MAX_REGIONS 72
 int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const int64_t* bytes, void* stream);
 
+/* ---- hash joins over the device-resident temps ------------------------ */
+#define ESC_MAX_STEPS 8  /* build steps of one probe pipeline */
+
+/* slots[0..capacity) <- -1, then slot of unique key i <- i: first free slot of the linear probe
+ * sequence from splitmix64(bits(key)) & (capacity - 1).  capacity: a power of two > n_unique
+ * (the reference sizes it for load <= 0.7).  replaces HashTableIndex._insert_all
+ * (executor.py:304-325). */
+int esc_hash_insert(const int64_t* unique_keys, int64_t n_unique, int64_t* slots, int64_t capacity, void* stream);
+
+/* out_groups[i] = g with unique_keys[g] == key(i), else -1 (absent, NULL key or !valid[i]).
+ * key(i) = keys[rows ? rows[i] : i] at native integer width key_dtype; key_nulls (bool mask
+ * indexed like keys), rows and valid (bool per i) are optional.  replaces
+ * HashTableIndex.probe_groups (executor.py:327-346). */
+int esc_hash_probe(const int64_t* slots, int64_t capacity, const int64_t* unique_keys, const void* keys,
+                   int32_t key_dtype, const uint8_t* key_nulls, const int64_t* rows, const uint8_t* valid,
+                   int64_t n, int64_t* out_groups, void* stream);
+
+/* One probe stage's expansion: tuple i with groups[i] = g >= 0 owns outputs offsets[i] ..
+ * offsets[i] + (group_start[g+1] - group_start[g]) - 1, which receive out_tuple = i (optional)
+ * and out_row = group_rows[group_start[g] + j] in group order.  replaces _expand_matches and the
+ * np.repeat of _probe_chunk (executor.py:373-386, :436-447). */
+int esc_expand(const int64_t* groups, const int64_t* offsets, int64_t n, const int64_t* group_start,
+               const int64_t* group_rows, int64_t* out_tuple, int64_t* out_row, void* stream);
+
+enum { ESC_JOIN_DENSE = 0, ESC_JOIN_HASH = 1 };
+
+/* One probe-keyed build step of a COUNT pipeline. */
+typedef struct {
+  const void* key_data;     /* the probe table's key column (device, native integer width)   */
+  const uint8_t* key_nulls; /* its bool NULL mask or NULL                                     */
+  int32_t key_dtype;
+  int32_t mode;             /* ESC_JOIN_DENSE or ESC_JOIN_HASH                                */
+  /* DENSE (star joins): factor(k) = factor[k - dense_min] for 0 <= k - dense_min < dense_len,
+   * else 0; factor_bits = 1 (bitmap of 32-bit words), 8, 16, 32 or 64; 16-byte aligned       */
+  int64_t dense_min;
+  int64_t dense_len;
+  const void* factor;
+  int32_t factor_bits;
+  int32_t pad;
+  /* HASH: g = the key's group (esc_hash_probe's table); weight[s][g] = its factor at stage s  */
+  const int64_t* slots;
+  int64_t capacity;
+  const int64_t* unique_keys;
+  const uint64_t* weight[ESC_MAX_STEPS + 1];
+} esc_join_step_t;
+
+typedef struct {
+  int32_t n_steps;   /* probe-keyed steps below (the others are folded into their weights)   */
+  int32_t n_stages;  /* build steps of the pipeline: stages 1..n_stages are counted           */
+  int32_t star;      /* 1: every step is probe-keyed and stage-invariant (DENSE allowed)      */
+  int32_t pad;
+  int64_t nrows;     /* probe table rows                                                      */
+  const uint32_t* bitmap;          /* rows passing the probe predicate (esc_scan_select), or NULL */
+  int32_t stage_of[ESC_MAX_STEPS]; /* stage (1..n_stages) of each probe-keyed step, increasing  */
+  esc_join_step_t steps[ESC_MAX_STEPS];
+} esc_join_t;
+
+/* The fused probe pipeline of a COUNT(*) plan: d_stage_counts[s] (device u64[n_stages + 1]) =
+ * tuples after stage s (s = 0: probe rows passing the predicate) = sum over those rows of the
+ * product of their steps' factors — probe_joins' stats.probe_out and result_rows
+ * (executor.py:403-474) without expanding a tuple. */
+int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream);
+
 /* ---- misc ------------------------------------------------------------------------------- */
 
 const char* esc_last_error(void);
@@ -308,7 +371,7 @@ int esc_jit_stats(int64_t* out);
  * Returns the previous setting. */
 int esc_set_stream_div(int div);
 /* sizeof() of the ABI structs, for binding checks: 0 program, 1 instr, 2 udf, 3 udf_op,
- * 4 column, 5 result, 6 outputs, 7 selection; -1 for an unknown id. */
+ * 4 column, 5 result, 6 outputs, 7 selection, 8 join step, 9 join; -1 for an unknown id. */
 int esc_struct_size(int which);
 /* Tile geometry the kernels use for a program over these columns (for roofline accounting). */
 int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols);

@@ -255,3 +255,115 @@ def py_mod(x: float, y: float) -> float:
 
 def is_finite(x) -> bool:
     return isinstance(x, (int, float)) and math.isfinite(x)
+
+
+# ---------------------------------------------------------------------------------------------
+# hash joins: reference executor.py:253-531, numpy restatement
+# ---------------------------------------------------------------------------------------------
+@dataclass
+class OIndex:
+    """HashTableIndex (executor.py:275-303): groups of equal keys over the non-NULL rows.  The
+    group id of a key is its index among the ascending unique keys (np.unique); a group's rows
+    are ascending (stable argsort of the inverse)."""
+
+    table: OTable
+    key: str
+    n_entries: int
+    unique_keys: np.ndarray
+    group_rows: np.ndarray
+    group_start: np.ndarray
+    group_counts: np.ndarray
+
+    @property
+    def distinct_keys(self) -> int:
+        return int(self.unique_keys.size)
+
+    def probe_groups(self, keys: np.ndarray, valid: np.ndarray) -> np.ndarray:
+        """executor.py:327-346: group id per key, -1 when absent or invalid (the open-addressed
+        probe returns exactly the np.unique index of the key, restated by a sorted search)."""
+        out = np.full(keys.shape, -1, dtype=np.int64)
+        if self.unique_keys.size == 0:
+            return out
+        k = keys.astype(np.int64)
+        pos = np.searchsorted(self.unique_keys, k)
+        ok = valid & (pos < self.unique_keys.size)
+        ok[ok] = self.unique_keys[pos[ok]] == k[ok]
+        out[ok] = pos[ok]
+        return out
+
+    def lookup(self, key: int) -> np.ndarray:
+        g = self.probe_groups(np.asarray([key], dtype=np.int64), np.ones(1, dtype=bool))[0]
+        if g < 0:
+            return np.empty(0, dtype=np.int64)
+        return self.group_rows[self.group_start[g]: self.group_start[g + 1]]
+
+
+def build_index(table: OTable, key: str, rows: np.ndarray) -> OIndex:
+    """HashTableIndex.__init__ (executor.py:281-298)."""
+    col = table.columns[key]
+    key_vals = col.values[rows]
+    non_null = ~col.nulls[rows]
+    rows = rows[non_null]
+    key_vals = key_vals[non_null].astype(np.int64)
+    uk, inverse = np.unique(key_vals, return_inverse=True)
+    order = np.argsort(inverse, kind="stable")
+    counts = np.bincount(inverse, minlength=uk.size).astype(np.int64)
+    start = np.concatenate((np.zeros(1, dtype=np.int64), np.cumsum(counts)))
+    return OIndex(table, key, int(rows.size), uk, rows[order].astype(np.int64), start, counts)
+
+
+def build_hash(table: OTable, key: str, residual=None, udfs=None) -> OIndex:
+    """executor.py:353-358."""
+    return build_index(table, key, eval_predicate(table, residual, None, udfs))
+
+
+def expand_matches(index: OIndex, groups: np.ndarray):
+    """_expand_matches (executor.py:373-386)."""
+    counts = index.group_counts[groups]
+    starts = index.group_start[groups]
+    total = int(counts.sum())
+    if total == 0:
+        return counts, np.empty(0, dtype=np.int64)
+    offsets = np.zeros(groups.size, dtype=np.int64)
+    np.cumsum(counts[:-1], out=offsets[1:])
+    flat = np.arange(total, dtype=np.int64)
+    flat -= np.repeat(offsets, counts)
+    flat += np.repeat(starts, counts)
+    return counts, index.group_rows[flat]
+
+
+def probe_joins(probe: OTable, probe_alias: str, probe_pred, steps, projection=None, udfs=None):
+    """_probe_chunk + probe_joins (executor.py:403-531) with one chunk.  ``steps`` is a list of
+    (alias, OIndex, (probe_table_alias, probe_column)); ``projection`` a list of (alias, column)
+    or None.  Returns (stage counts, result columns as {name: OColumn} or None)."""
+    prow = eval_predicate(probe, probe_pred, None, udfs)
+    stage_out = [int(prow.size)]
+    brows: dict = {}
+    tables = {probe_alias: probe}
+    for alias, index, (src, cname) in steps:
+        rows_src = prow if src == probe_alias else brows[src]
+        col = tables[src].columns[cname]
+        keys = col.values[rows_src]
+        valid = ~col.nulls[rows_src]
+        groups = index.probe_groups(keys, valid)
+        hit = groups >= 0
+        prow = prow[hit]
+        for a in brows:
+            brows[a] = brows[a][hit]
+        counts, matched = expand_matches(index, groups[hit])
+        prow = np.repeat(prow, counts)
+        for a in brows:
+            brows[a] = np.repeat(brows[a], counts)
+        brows[alias] = matched
+        tables[alias] = index.table
+        stage_out.append(int(prow.size))
+    if projection is None:
+        return stage_out, None
+    rows_of = {probe_alias: prow, **brows}
+    out, used = {}, set()
+    for alias, cname in projection:
+        c = take(tables[alias].columns[cname], rows_of[alias])
+        name = cname if cname not in used else f"{alias}.{cname}"
+        used.add(name)
+        out[name] = c
+    return stage_out, out

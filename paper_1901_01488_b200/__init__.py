@@ -2,15 +2,17 @@
 
 Drop-in for the hot path of the reference ``escdb`` package: the planning-time COUNT sub-query,
 its push-down policy, the order-preserving materialization of qualifying rows into temp tables,
-and join ordering from the exact counts — with every scan, count and compaction running in
-hand-written sm_100a kernels behind the C ABI in ``include/esc.h``.
+join ordering from the exact counts, and the hash-join pipeline that reuses those temps in place
+— with every scan, count, compaction, hash build and probe running in hand-written sm_100a
+kernels behind the C ABI in ``include/esc.h``.
 """
 
 from . import expr
 from .catalog import Catalog
-from .engine import Engine, OptimizeResult
+from .engine import Engine, OptimizeResult, QueryResult
 from .errors import EscdbError
 from .executor import RowSelection, count_star, eval_predicate, execute_count, materialize
+from .join import BuildStep, ExecStats, HashTableIndex, build_hash, execute_plan, probe_joins
 from .optimizer import (
     EscConfig,
     compute_exact_selectivity,
@@ -27,8 +29,9 @@ from .storage import Column, ColumnKind, ColumnTable, Dictionary
 __version__ = "0.1.0"
 
 __all__ = [
-    "Catalog", "Column", "ColumnKind", "ColumnTable", "Dictionary", "Engine", "EscConfig",
-    "EscdbError", "OptimizeResult", "RowSelection", "__version__", "build_join_graph",
+    "BuildStep", "Catalog", "Column", "ColumnKind", "ColumnTable", "Dictionary", "Engine", "EscConfig",
+    "EscdbError", "ExecStats", "HashTableIndex", "OptimizeResult", "QueryResult", "RowSelection",
+    "__version__", "build_hash", "build_join_graph", "execute_plan", "probe_joins",
     "compute_exact_selectivity", "count_star", "decide_pushdown", "eval_predicate",
     "execute_count", "explain_json", "explain_text", "expr", "materialize",
     "materialize_pushdown", "order_builds", "plan", "query",

@@ -89,9 +89,27 @@ class EscSelection(C.Structure):
                 ("cap_nulls", C.c_void_p * MAX_PROJ), ("d_count", C.c_void_p)]
 
 
+MAX_STEPS = 8
+JOIN_DENSE, JOIN_HASH = 0, 1
+
+
+class EscJoinStep(C.Structure):
+    _fields_ = [("key_data", C.c_void_p), ("key_nulls", C.c_void_p), ("key_dtype", C.c_int32), ("mode", C.c_int32),
+                ("dense_min", C.c_int64), ("dense_len", C.c_int64), ("factor", C.c_void_p),
+                ("factor_bits", C.c_int32), ("pad", C.c_int32), ("slots", C.c_void_p), ("capacity", C.c_int64),
+                ("unique_keys", C.c_void_p), ("weight", C.c_void_p * (MAX_STEPS + 1))]
+
+
+class EscJoin(C.Structure):
+    _fields_ = [("n_steps", C.c_int32), ("n_stages", C.c_int32), ("star", C.c_int32), ("pad", C.c_int32),
+                ("nrows", C.c_int64), ("bitmap", C.c_void_p), ("stage_of", C.c_int32 * MAX_STEPS),
+                ("steps", EscJoinStep * MAX_STEPS)]
+
+
 SEG_CAPTURED = 0x80000000
 OUT_SKIP_OVER_CAPACITY = 1
-STRUCTS = [EscProgram, EscInstr, EscUdf, EscUdfOp, EscColumn, EscResult, EscOutputs, EscSelection]
+STRUCTS = [EscProgram, EscInstr, EscUdf, EscUdfOp, EscColumn, EscResult, EscOutputs, EscSelection, EscJoinStep,
+           EscJoin]
 
 # every symbol include/esc.h declares, with its ctypes signature
 _SIGNATURES = {
@@ -124,6 +142,12 @@ _SIGNATURES = {
     "esc_jit_selftest": (C.c_int, []),
     "esc_set_stream_div": (C.c_int, [C.c_int]),
     "esc_copy_regions": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "esc_hash_insert": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
+    "esc_hash_probe": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "esc_expand": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.c_void_p]),
+    "esc_join_count": (C.c_int, [C.POINTER(EscJoin), C.c_void_p, C.c_void_p]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

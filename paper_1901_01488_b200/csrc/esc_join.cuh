@@ -1,0 +1,402 @@
+// esc_join.cuh — hash joins over the device-resident ESC temps, included
+// by esc_kernels.cu.
+//
+//   esc_hash_insert   HashTableIndex._insert_all   (executor.py:304-325)
+//   esc_hash_probe    HashTableIndex.probe_groups  (executor.py:327-346)
+//   esc_expand        _expand_matches + np.repeat  (executor.py:373-386, :436-447)
+//   esc_join_count    the fused probe pipeline of a COUNT(*) plan (executor.py:403-474): one
+//                     pass over the probe table's key columns, every hash lookup and the
+//                     per-stage tuple counts fused, nothing expanded.
+//
+// The table is the reference's: open addressing, splitmix64 of the key's 64-bit pattern, linear
+// probing, capacity a power of two at load <= 0.7, slots hold dense group ids (= index into the
+// ascending unique keys).  Inserting with atomicCAS instead of the reference's sorted rounds puts
+// keys in different slots of a probe run, but every lookup returns the same group id, so groups,
+// counts, row sets and row order are identical.
+//
+// esc_join_count: a COUNT over a join tree never needs the expanded tuples.  The host folds every
+// step into a per-group weight (group size x the weights of the steps probed from its rows,
+// computed bottom-up per stage prefix), so a probe row contributes prod_t weight_t[group_t(row)]
+// to each stage.  For a star (every probe key on the probe table) the weights are stage-invariant
+// and are handed over as dense "factor" arrays indexed by key - min: 1-bit for primary-key
+// dimensions.  Small factor arrays are staged in shared memory, so the pass streams the probe
+// table's key columns at HBM speed with all lookups on-chip.
+#pragma once
+
+namespace esc {
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void hash_insert_kernel(const long long* __restrict__ uk, int64_t n, unsigned long long* slots,
+                                   unsigned long long mask) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long pos = splitmix64((unsigned long long)uk[i]) & mask;
+    while (atomicCAS(&slots[pos], ~0ull, (unsigned long long)i) != ~0ull) pos = (pos + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ long long hash_find(const long long* __restrict__ slots, unsigned long long mask,
+                                               const long long* __restrict__ uk, long long key) {
+  unsigned long long pos = splitmix64((unsigned long long)key) & mask;
+  while (true) {
+    const long long s = __ldg(slots + pos);
+    if (s < 0) return -1;
+    if (__ldg(uk + s) == key) return s;
+    pos = (pos + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ long long ld_key(const uint8_t* base, int dtype, int64_t row) {
+  switch (dtype) {
+    case ESC_I8: return reinterpret_cast<const int8_t*>(base)[row];
+    case ESC_I16: return reinterpret_cast<const int16_t*>(base)[row];
+    case ESC_I32: return reinterpret_cast<const int32_t*>(base)[row];
+    case ESC_U8: return reinterpret_cast<const uint8_t*>(base)[row];
+    case ESC_U16: return reinterpret_cast<const uint16_t*>(base)[row];
+    case ESC_U32: return reinterpret_cast<const uint32_t*>(base)[row];
+    default: return reinterpret_cast<const long long*>(base)[row];
+  }
+}
+
+struct ProbeParams {
+  const long long* slots;
+  unsigned long long mask;
+  const long long* uk;
+  const uint8_t* keys;
+  int32_t dtype;
+  const uint8_t* nulls;
+  const int64_t* rows;
+  const uint8_t* valid;
+  int64_t n;
+  long long* out;
+};
+
+__global__ void hash_probe_kernel(const ProbeParams p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+    long long g = -1;
+    const int64_t r = p.rows ? p.rows[i] : i;
+    if ((p.valid == nullptr || p.valid[i]) && (p.nulls == nullptr || p.nulls[r] == 0))
+      g = hash_find(p.slots, p.mask, p.uk, ld_key(p.keys, p.dtype, r));
+    p.out[i] = g;
+  }
+}
+
+// one thread per tuple: its matches, in group order, at its exclusive offset
+__global__ void expand_kernel(const long long* __restrict__ groups, const long long* __restrict__ offsets, int64_t n,
+                              const long long* __restrict__ gstart, const long long* __restrict__ grows,
+                              long long* __restrict__ out_tuple, long long* __restrict__ out_row) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long g = groups[i];
+    if (g < 0) continue;
+    const long long s = gstart[g], e = gstart[g + 1];
+    long long o = offsets[i];
+    for (long long j = s; j < e; ++j, ++o) {
+      if (out_tuple) out_tuple[o] = i;
+      out_row[o] = grows[j];
+    }
+  }
+}
+
+// ---- fused COUNT probe ------------------------------------------------------------------------
+struct JoinStepK {
+  const uint8_t* keys;
+  const uint8_t* nulls;
+  int32_t dtype;
+  int32_t mode;         // ESC_JOIN_DENSE / ESC_JOIN_HASH
+  long long dmin;
+  long long dlen;
+  const uint8_t* factor;  // global factor array (dense)
+  int32_t fbits;          // 1, 8, 16, 32, 64
+  uint32_t smem_off;      // byte offset of the staged factor array, or kNoSmem
+  const long long* slots;
+  unsigned long long mask;
+  const long long* uk;
+  const unsigned long long* weight[ESC_MAX_STEPS + 1];
+};
+
+constexpr uint32_t kNoSmem = 0xFFFFFFFFu;
+
+struct JoinParams {
+  int32_t n_steps;
+  int32_t n_stages;
+  int32_t star;
+  int32_t pad;
+  int64_t nrows;
+  const uint32_t* bitmap;
+  int32_t stage_of[ESC_MAX_STEPS];
+  JoinStepK steps[ESC_MAX_STEPS];
+  uint32_t smem_bytes;
+  unsigned long long* out;  // [n_stages + 1]
+};
+
+__device__ __forceinline__ unsigned long long factor_at(const uint8_t* f, int bits, long long i) {
+  switch (bits) {
+    case 1: return (reinterpret_cast<const uint32_t*>(f)[i >> 5] >> (i & 31)) & 1u;
+    case 8: return f[i];
+    case 16: return reinterpret_cast<const uint16_t*>(f)[i];
+    case 32: return reinterpret_cast<const uint32_t*>(f)[i];
+    default: return reinterpret_cast<const unsigned long long*>(f)[i];
+  }
+}
+
+constexpr int kJoinThreads = 512;
+
+__global__ void __launch_bounds__(kJoinThreads) join_count_kernel(const __grid_constant__ JoinParams p) {
+  extern __shared__ __align__(16) uint8_t jsm[];
+  // stage the small dense factor arrays (all lookups of the pass then stay on chip)
+  for (int t = 0; t < p.n_steps; ++t) {
+    const JoinStepK& s = p.steps[t];
+    if (s.mode != ESC_JOIN_DENSE || s.smem_off == kNoSmem) continue;
+    const long long bytes = s.fbits == 1 ? ((s.dlen + 31) / 32) * 4 : s.dlen * (s.fbits / 8);
+    const long long words = (bytes + 15) / 16;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x)
+      reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(reinterpret_cast<const uint4*>(s.factor) + i);
+  }
+  __syncthreads();
+  // every loop over steps / stages is fully unrolled with compile-time indices, so the per-stage
+  // accumulators and group ids live in registers
+  unsigned long long acc[ESC_MAX_STEPS + 1];
+#pragma unroll
+  for (int i = 0; i <= ESC_MAX_STEPS; ++i) acc[i] = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwords = (p.nrows + 31) / 32;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = gw; w < nwords; w += nw) {
+    const int64_t row = w * 32 + lane;
+    bool sel = row < p.nrows;
+    if (sel && p.bitmap != nullptr) sel = (__ldg(p.bitmap + w) >> lane) & 1u;
+    if (!sel) continue;
+    acc[0] += 1;
+    if (p.star) {
+      // star: step t is stage t + 1 and its factor is stage-invariant
+      unsigned long long run = 1;
+#pragma unroll
+      for (int t = 0; t < ESC_MAX_STEPS; ++t) {
+        if (t >= p.n_steps) break;
+        const JoinStepK& s = p.steps[t];
+        unsigned long long f = 0;
+        if (run != 0 && (s.nulls == nullptr || s.nulls[row] == 0)) {
+          const long long k = ld_key(s.keys, s.dtype, row);
+          if (s.mode == ESC_JOIN_DENSE) {
+            const long long i = k - s.dmin;
+            if (i >= 0 && i < s.dlen) f = factor_at(s.smem_off != kNoSmem ? jsm + s.smem_off : s.factor, s.fbits, i);
+          } else {
+            const long long g = hash_find(s.slots, s.mask, s.uk, k);
+            if (g >= 0) f = __ldg(s.weight[t + 1] + g);
+          }
+        }
+        run *= f;
+        acc[t + 1] += run;
+      }
+    } else {
+      long long g[ESC_MAX_STEPS];
+#pragma unroll
+      for (int t = 0; t < ESC_MAX_STEPS; ++t) {
+        g[t] = -1;
+        if (t < p.n_steps) {
+          const JoinStepK& s = p.steps[t];
+          if (s.nulls == nullptr || s.nulls[row] == 0) g[t] = hash_find(s.slots, s.mask, s.uk, ld_key(s.keys, s.dtype, row));
+        }
+      }
+#pragma unroll
+      for (int st = 1; st <= ESC_MAX_STEPS; ++st) {
+        if (st > p.n_stages) break;
+        unsigned long long prod = 1;
+#pragma unroll
+        for (int t = 0; t < ESC_MAX_STEPS; ++t) {
+          if (t < p.n_steps && p.stage_of[t] <= st)
+            prod = g[t] < 0 ? 0ull : prod * (prod ? __ldg(p.steps[t].weight[st] + g[t]) : 0ull);
+        }
+        acc[st] += prod;
+      }
+    }
+  }
+  // block reduction -> one atomicAdd per stage per block
+  __shared__ unsigned long long red[kJoinThreads / 32][ESC_MAX_STEPS + 1];
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int st = 0; st <= ESC_MAX_STEPS; ++st) {
+    unsigned long long v = acc[st];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+    if (lane == 0) red[warp][st] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x <= p.n_stages) {
+    unsigned long long v = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) v += red[w2][threadIdx.x];
+    if (v) atomicAdd(p.out + threadIdx.x, v);
+  }
+}
+
+}  // namespace esc
+
+// ==========================================================================================
+// C ABI (joins)
+// ==========================================================================================
+extern "C" {
+
+int esc_hash_insert(const int64_t* unique_keys, int64_t n_unique, int64_t* slots, int64_t capacity, void* stream) {
+  if (capacity <= 0 || (capacity & (capacity - 1)) != 0) return fail(ESC_ERR_INVALID, "capacity must be a power of two");
+  if (n_unique < 0 || n_unique >= capacity) return fail(ESC_ERR_INVALID, "capacity must exceed the unique keys");
+  if (slots == nullptr || (n_unique > 0 && unique_keys == nullptr)) return fail(ESC_ERR_INVALID, "null hash buffers");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(slots, 0xFF, (size_t)capacity * sizeof(int64_t), st);
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("slot init: ") + cudaGetErrorString(e));
+  if (n_unique == 0) return ESC_OK;
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  int64_t blocks = (n_unique + 255) / 256;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  esc::hash_insert_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const long long*>(unique_keys), n_unique,
+                                                            reinterpret_cast<unsigned long long*>(slots),
+                                                            (unsigned long long)capacity - 1);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash insert launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
+int esc_hash_probe(const int64_t* slots, int64_t capacity, const int64_t* unique_keys, const void* keys,
+                   int32_t key_dtype, const uint8_t* key_nulls, const int64_t* rows, const uint8_t* valid, int64_t n,
+                   int64_t* out_groups, void* stream) {
+  if (capacity <= 0 || (capacity & (capacity - 1)) != 0) return fail(ESC_ERR_INVALID, "capacity must be a power of two");
+  if (n < 0) return fail(ESC_ERR_INVALID, "negative probe count");
+  if (n == 0) return ESC_OK;
+  if (slots == nullptr || unique_keys == nullptr || keys == nullptr || out_groups == nullptr)
+    return fail(ESC_ERR_INVALID, "null probe buffers");
+  if (key_dtype == ESC_F32 || key_dtype == ESC_F64 || dtype_width(key_dtype) == 0)
+    return fail(ESC_ERR_UNSUPPORTED, "hash keys must be integer columns");
+  esc::ProbeParams p;
+  p.slots = reinterpret_cast<const long long*>(slots);
+  p.mask = (unsigned long long)capacity - 1;
+  p.uk = reinterpret_cast<const long long*>(unique_keys);
+  p.keys = static_cast<const uint8_t*>(keys);
+  p.dtype = key_dtype;
+  p.nulls = key_nulls;
+  p.rows = rows;
+  p.valid = valid;
+  p.n = n;
+  p.out = reinterpret_cast<long long*>(out_groups);
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+  esc::hash_probe_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash probe launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
+int esc_expand(const int64_t* groups, const int64_t* offsets, int64_t n, const int64_t* group_start,
+               const int64_t* group_rows, int64_t* out_tuple, int64_t* out_row, void* stream) {
+  if (n < 0) return fail(ESC_ERR_INVALID, "negative tuple count");
+  if (n == 0) return ESC_OK;
+  if (groups == nullptr || offsets == nullptr || group_start == nullptr || out_row == nullptr)
+    return fail(ESC_ERR_INVALID, "null expansion buffers");
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+  esc::expand_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const long long*>(groups), reinterpret_cast<const long long*>(offsets), n,
+      reinterpret_cast<const long long*>(group_start), reinterpret_cast<const long long*>(group_rows),
+      reinterpret_cast<long long*>(out_tuple), reinterpret_cast<long long*>(out_row));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("expand launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
+int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) {
+  if (j == nullptr || d_stage_counts == nullptr) return fail(ESC_ERR_INVALID, "null join arguments");
+  if (j->n_steps < 0 || j->n_steps > ESC_MAX_STEPS || j->n_stages < 0 || j->n_stages > ESC_MAX_STEPS)
+    return fail(ESC_ERR_INVALID, "join step count out of range");
+  if (j->nrows < 0) return fail(ESC_ERR_INVALID, "negative probe rows");
+  static thread_local esc::JoinParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.n_steps = j->n_steps;
+  p.n_stages = j->n_stages;
+  p.star = j->star ? 1 : 0;
+  p.nrows = j->nrows;
+  p.bitmap = j->bitmap;
+  p.out = reinterpret_cast<unsigned long long*>(d_stage_counts);
+  int prev_stage = 0;
+  uint32_t smem = 0;
+  const uint32_t smem_cap = 160 * 1024;
+  for (int t = 0; t < j->n_steps; ++t) {
+    const esc_join_step_t& s = j->steps[t];
+    esc::JoinStepK& k = p.steps[t];
+    if (j->stage_of[t] <= prev_stage || j->stage_of[t] > j->n_stages)
+      return fail(ESC_ERR_INVALID, "stage_of must increase within 1..n_stages");
+    prev_stage = p.stage_of[t] = j->stage_of[t];
+    if (s.key_data == nullptr && j->nrows > 0) return fail(ESC_ERR_INVALID, "null join key column");
+    if (s.key_dtype == ESC_F32 || s.key_dtype == ESC_F64 || dtype_width(s.key_dtype) == 0)
+      return fail(ESC_ERR_UNSUPPORTED, "join keys must be integer columns");
+    k.keys = static_cast<const uint8_t*>(s.key_data);
+    k.nulls = s.key_nulls;
+    k.dtype = s.key_dtype;
+    k.mode = s.mode;
+    k.smem_off = esc::kNoSmem;
+    if (s.mode == ESC_JOIN_DENSE) {
+      if (!j->star) return fail(ESC_ERR_INVALID, "dense factor arrays need a star (stage-invariant) join");
+      if (s.factor_bits != 1 && s.factor_bits != 8 && s.factor_bits != 16 && s.factor_bits != 32 && s.factor_bits != 64)
+        return fail(ESC_ERR_INVALID, "factor_bits must be 1, 8, 16, 32 or 64");
+      if (s.dense_len < 0 || (s.dense_len > 0 && s.factor == nullptr)) return fail(ESC_ERR_INVALID, "bad dense factor");
+      if (reinterpret_cast<uintptr_t>(s.factor) % 16 != 0) return fail(ESC_ERR_INVALID, "factor array must be 16-byte aligned");
+      k.dmin = s.dense_min;
+      k.dlen = s.dense_len;
+      k.factor = static_cast<const uint8_t*>(s.factor);
+      k.fbits = s.factor_bits;
+      const long long bytes = s.factor_bits == 1 ? ((s.dense_len + 31) / 32) * 4 : s.dense_len * (s.factor_bits / 8);
+      const uint32_t need = (uint32_t)((bytes + 15) / 16 * 16);
+      if (bytes <= (long long)smem_cap && smem + need <= smem_cap) {
+        k.smem_off = smem;
+        smem += need;
+      }
+    } else if (s.mode == ESC_JOIN_HASH) {
+      if (s.capacity <= 0 || (s.capacity & (s.capacity - 1)) != 0 || s.slots == nullptr || s.unique_keys == nullptr)
+        return fail(ESC_ERR_INVALID, "bad hash table");
+      k.slots = reinterpret_cast<const long long*>(s.slots);
+      k.mask = (unsigned long long)s.capacity - 1;
+      k.uk = reinterpret_cast<const long long*>(s.unique_keys);
+      for (int st = p.stage_of[t]; st <= j->n_stages; ++st) {
+        if (s.weight[st] == nullptr) return fail(ESC_ERR_INVALID, "missing stage weight array");
+        k.weight[st] = reinterpret_cast<const unsigned long long*>(s.weight[st]);
+      }
+    } else {
+      return fail(ESC_ERR_INVALID, "bad join step mode");
+    }
+  }
+  if (j->star && j->n_steps != j->n_stages) return fail(ESC_ERR_INVALID, "a star join probes every stage");
+  p.smem_bytes = smem;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_stage_counts, 0, (size_t)(j->n_stages + 1) * sizeof(uint64_t), st);
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("stage count init: ") + cudaGetErrorString(e));
+  if (j->nrows == 0) return ESC_OK;
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  static thread_local uint32_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    e = cudaFuncSetAttribute(esc::join_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    configured = smem;
+  }
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, esc::join_count_kernel, esc::kJoinThreads, smem) !=
+          cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int64_t words = (j->nrows + 31) / 32;
+  int64_t blocks = (words + esc::kJoinThreads / 32 - 1) / (esc::kJoinThreads / 32);
+  if (blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;
+  esc::join_count_kernel<<<(unsigned)blocks, esc::kJoinThreads, smem, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("join count launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
+}  // extern "C"

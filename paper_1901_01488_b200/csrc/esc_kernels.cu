@@ -987,6 +987,8 @@ int esc_struct_size(int which) {
     case 5: return (int)sizeof(esc_result_t);
     case 6: return (int)sizeof(esc_outputs_t);
     case 7: return (int)sizeof(esc_selection_t);
+    case 8: return (int)sizeof(esc_join_step_t);
+    case 9: return (int)sizeof(esc_join_t);
     default: return -1;
   }
 }
@@ -1005,3 +1007,5 @@ int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t n
 }
 
 }  // extern "C"
+
+#include "esc_join.cuh"

@@ -302,7 +302,86 @@ def star_known():
     return res
 
 
+def join_known():
+    """Reference build_hash / probe_joins on tests/golden/join_cases.py: stage counts, result rows,
+    projected columns in order (full lists: the cases are small)."""
+    sys.path.insert(0, HERE)
+    import join_cases
+    from escdb.executor import BuildStep as RBuildStep, build_hash as rbuild, probe_joins as rprobe
+
+    out = {}
+    for case in join_cases.cases():
+        tabs = {}
+        for alias, cols in case["tables"].items():
+            tabs[alias] = RTable(alias, [RColumn(c, KIND_INT64, v, n) for c, (v, n) in cols.items()])
+        steps = []
+        for st in case["steps"]:
+            t = tabs[st["alias"]]
+            res = json_to_ref(st["residual"], t) if st["residual"] is not None else None
+            idx = rbuild(t, st["key"], res)
+            src, cname = st["probe_key"]
+            steps.append(RBuildStep(st["alias"], idx, rex.ColumnRef(src, cname, KIND_INT64)))
+        probe = tabs[case["probe"]]
+        pp = json_to_ref(case["probe_pred"], probe) if case["probe_pred"] is not None else None
+        proj = None
+        if case["projection"] is not None:
+            proj = tuple(rex.ColumnRef(a, c, KIND_INT64) for a, c in case["projection"])
+        result, stats = rprobe(probe, case["probe"], pp, steps, proj)
+        rec = {"probe_out": [int(x) for x in stats.probe_out], "result_rows": int(stats.result_rows),
+               "build_cards": [int(x) for x in stats.build_cards],
+               "build_distinct": [int(x) for x in stats.build_distinct]}
+        if result is not None:
+            rec["columns"] = [[c.name, np.asarray(c.values).tolist(), np.asarray(c.null_mask).tolist()]
+                              for c in result.columns]
+        out[case["name"]] = rec
+    return out
+
+
+def star_execute_known():
+    """The config-3 star query executed by the reference: plan with ESC, execute_plan COUNT."""
+    from escdb.optimizer import execute_plan as rexec
+
+    g = datagen.config3(fact_rows=60_000_000)
+    cat = RCatalog()
+    names = {"date": "dates"}
+    for tname, cols in g.items():
+        rc = []
+        for cname, spec in cols.items():
+            if spec[0] == "TEXT":
+                d = RDict()
+                for w in spec[2]:
+                    d.encode(w)
+                rc.append(RColumn(cname, KIND_TEXT, spec[1], np.zeros(len(spec[1]), bool), d))
+            else:
+                rc.append(RColumn(cname, KIND_INT64, spec[1], np.zeros(len(spec[1]), bool)))
+        cat.register(RTable(names.get(tname, tname), rc))
+    sql = ("SELECT COUNT(*) FROM fact, dates, customer, supplier, part WHERE f_datekey = d_datekey "
+           "AND f_custkey = c_custkey AND f_suppkey = s_suppkey AND f_partkey = p_partkey "
+           "AND c_region = 'R1' AND (p_category = 'C03' OR p_category = 'C07') "
+           "AND d_year BETWEEN 1993 AND 1994 AND (s_nation = 'N02' OR s_nation = 'N05')")
+    import time as _t
+
+    p = rplan(rfe.analyze(rfe.parse(sql), cat), cat, REscConfig())
+    t0 = _t.perf_counter()
+    _, count, stats = rexec(p, cat)
+    ms = (_t.perf_counter() - t0) * 1e3
+    cat.temps.sweep()
+    return {"count": int(count), "probe_out": [int(x) for x in stats.probe_out], "execute_ms_reference": ms,
+            "order": p.build_order}
+
+
 def main():
+    if "--only-joins" in sys.argv:  # refresh just the join sections of known.json
+        path = os.path.join(HERE, "known.json")
+        with open(path) as fh:
+            known = json.load(fh)
+        known["joins"] = join_known()
+        if "--skip-star" not in sys.argv:
+            known["star_execute"] = star_execute_known()
+        with open(path, "w") as fh:
+            json.dump(known, fh, indent=1)
+        print("join fixtures written")
+        return
     custom = generate(GenSpec("custom", 0.02, 3, null_fraction=0.08))["data"]
     orders = generate(GenSpec("tpch_subset", 0.001, 7))["orders"]
     arrays = {}
@@ -320,7 +399,8 @@ def main():
     }
     with open(os.path.join(HERE, "corpus.json"), "w") as fh:
         json.dump(corpus, fh, separators=(",", ":"))
-    known = {"configs": config_known(), "shop": shop_known(), "star": star_known(),
+    known = {"configs": config_known(), "shop": shop_known(), "star": star_known(), "joins": join_known(),
+             "star_execute": star_execute_known(),
              "generator": "reference escdb 0.1.0 (pkg/src/escdb), numpy " + np.__version__}
     with open(os.path.join(HERE, "known.json"), "w") as fh:
         json.dump(known, fh, indent=1)
