@@ -125,7 +125,7 @@ struct JoinParams {
   int32_t n_steps;
   int32_t n_stages;
   int32_t star;
-  int32_t pad;
+  int32_t bits;  // semi-join star: 1-bit dense factors, int32 keys without NULLs -> join_bits_kernel
   int64_t nrows;
   const uint32_t* bitmap;
   int32_t stage_of[ESC_MAX_STEPS];
@@ -146,7 +146,7 @@ __device__ __forceinline__ unsigned long long factor_at(const uint8_t* f, int bi
 
 constexpr int kJoinThreads = 512;
 
-__global__ void __launch_bounds__(kJoinThreads) join_count_kernel(const __grid_constant__ JoinParams p) {
+__global__ void __launch_bounds__(kJoinThreads, 2) join_count_kernel(const __grid_constant__ JoinParams p) {
   extern __shared__ __align__(16) uint8_t jsm[];
   // stage the small dense factor arrays (all lookups of the pass then stay on chip)
   for (int t = 0; t < p.n_steps; ++t) {
@@ -220,6 +220,110 @@ __global__ void __launch_bounds__(kJoinThreads) join_count_kernel(const __grid_c
   // block reduction -> one atomicAdd per stage per block
   __shared__ unsigned long long red[kJoinThreads / 32][ESC_MAX_STEPS + 1];
   const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int st = 0; st <= ESC_MAX_STEPS; ++st) {
+    unsigned long long v = acc[st];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+    if (lane == 0) red[warp][st] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x <= p.n_stages) {
+    unsigned long long v = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) v += red[w2][threadIdx.x];
+    if (v) atomicAdd(p.out + threadIdx.x, v);
+  }
+}
+
+// Semi-join star (every step a 1-bit dense factor over int32 keys without NULLs — the primary-key
+// dimensions of a star schema): a thread owns 4 consecutive rows, issues every step's 16-byte key
+// load at once, and walks a 4-bit survivor mask through the on-chip bitmaps; stage s adds
+// popc(mask).  No multiplies, 32-bit counters, no dependent global loads.
+template <int NS>
+__device__ __forceinline__ void bits_load(const JoinParams& p, int64_t q, int64_t full, uint32_t m, int4 (&k)[NS]) {
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    const int* kp = reinterpret_cast<const int*>(p.steps[t].keys);
+    if (q < full) {
+      k[t] = __ldg(reinterpret_cast<const int4*>(kp) + q);
+    } else {  // ragged tail: only the rows that exist
+      const int64_t row0 = q * 4;
+      k[t].x = (m & 1u) ? __ldg(kp + row0) : 0;
+      k[t].y = (m >> 1) & 1u ? __ldg(kp + row0 + 1) : 0;
+      k[t].z = (m >> 2) & 1u ? __ldg(kp + row0 + 2) : 0;
+      k[t].w = (m >> 3) & 1u ? __ldg(kp + row0 + 3) : 0;
+    }
+  }
+}
+
+template <int NS>
+__device__ __forceinline__ uint32_t bits_rows_mask(const JoinParams& p, int64_t q, int64_t full) {
+  if (q * 4 >= p.nrows) return 0;
+  const int64_t row0 = q * 4;
+  uint32_t m = q < full ? 0xFu : (0xFu >> (4 - (p.nrows - row0)));
+  if (p.bitmap != nullptr) m &= (__ldg(p.bitmap + (row0 >> 5)) >> (row0 & 31)) & 0xFu;
+  return m;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_bits_kernel(const __grid_constant__ JoinParams p) {
+  extern __shared__ __align__(16) uint8_t jsm[];
+  for (int t = 0; t < NS; ++t) {
+    const JoinStepK& s = p.steps[t];
+    if (s.smem_off == kNoSmem) continue;
+    const long long words = (((s.dlen + 31) / 32) * 4 + 15) / 16;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x)
+      reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(reinterpret_cast<const uint4*>(s.factor) + i);
+  }
+  __syncthreads();
+  uint32_t acc[ESC_MAX_STEPS + 1];
+#pragma unroll
+  for (int i = 0; i <= ESC_MAX_STEPS; ++i) acc[i] = 0;
+  // per-step lookup state in registers: shared-memory bitmap, 32-bit key offset and span
+  const uint32_t* bmap[NS];
+  int kmin[NS];
+  uint32_t klen[NS];
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    bmap[t] = reinterpret_cast<const uint32_t*>(jsm + p.steps[t].smem_off);
+    kmin[t] = (int)p.steps[t].dmin;
+    klen[t] = (uint32_t)p.steps[t].dlen;
+  }
+  const int64_t nquads = (p.nrows + 3) / 4;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t full = p.nrows / 4;
+  // software pipeline: the next quad's keys are in flight while this quad's masks are computed
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t m = bits_rows_mask<NS>(p, q, full);
+  int4 k[NS];
+  if (m) bits_load<NS>(p, q, full, m, k);
+  while (q < nquads) {
+    const int64_t qn = q + nth;
+    const uint32_t mn = bits_rows_mask<NS>(p, qn, full);
+    int4 kn[NS];
+    if (mn) bits_load<NS>(p, qn, full, mn, kn);
+    if (m) {
+      acc[0] += __popc(m);
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        const int kv[4] = {k[t].x, k[t].y, k[t].z, k[t].w};
+        uint32_t hit = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t i = (uint32_t)kv[j] - (uint32_t)kmin[t];  // wraps below min: out of span
+          if (((m >> j) & 1u) && i < klen[t]) hit |= ((bmap[t][i >> 5] >> (i & 31)) & 1u) << j;
+        }
+        m &= hit;
+        acc[t + 1] += __popc(m);
+      }
+    }
+    q = qn;
+    m = mn;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) k[t] = kn[t];
+  }
+  __shared__ unsigned long long red[kJoinThreads / 32][ESC_MAX_STEPS + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int st = 0; st <= ESC_MAX_STEPS; ++st) {
     unsigned long long v = acc[st];
@@ -373,6 +477,14 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
     }
   }
   if (j->star && j->n_steps != j->n_stages) return fail(ESC_ERR_INVALID, "a star join probes every stage");
+  p.bits = p.star;
+  for (int t = 0; t < j->n_steps; ++t) {
+    const esc::JoinStepK& k = p.steps[t];
+    if (k.mode != ESC_JOIN_DENSE || k.fbits != 1 || k.dtype != ESC_I32 || k.nulls != nullptr ||
+        reinterpret_cast<uintptr_t>(k.keys) % 16 != 0 || k.smem_off == esc::kNoSmem || k.dmin < INT32_MIN ||
+        k.dmin > INT32_MAX || k.dlen > INT32_MAX)
+      p.bits = 0;
+  }
   p.smem_bytes = smem;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(d_stage_counts, 0, (size_t)(j->n_stages + 1) * sizeof(uint64_t), st);
@@ -380,20 +492,28 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
   if (j->nrows == 0) return ESC_OK;
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
-  static thread_local uint32_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    e = cudaFuncSetAttribute(esc::join_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static void (*const bits_kernels[ESC_MAX_STEPS + 1])(const esc::JoinParams) = {
+      nullptr, esc::join_bits_kernel<1>, esc::join_bits_kernel<2>, esc::join_bits_kernel<3>,
+      esc::join_bits_kernel<4>, esc::join_bits_kernel<5>, esc::join_bits_kernel<6>, esc::join_bits_kernel<7>,
+      esc::join_bits_kernel<8>};
+  if (p.n_steps == 0) p.bits = 0;
+  auto kern = p.bits ? bits_kernels[p.n_steps] : esc::join_count_kernel;
+  static thread_local uint32_t configured[ESC_MAX_STEPS + 1] = {};
+  const int ci = p.bits ? p.n_steps : 0;
+  if (smem > 48 * 1024 && smem > configured[ci]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    configured = smem;
+    configured[ci] = smem;
   }
   int per_sm = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, esc::join_count_kernel, esc::kJoinThreads, smem) !=
-          cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, esc::kJoinThreads, smem) != cudaSuccess ||
+      per_sm < 1)
     per_sm = 1;
-  const int64_t words = (j->nrows + 31) / 32;
-  int64_t blocks = (words + esc::kJoinThreads / 32 - 1) / (esc::kJoinThreads / 32);
+  const int64_t units = p.bits ? (j->nrows + 3) / 4 / 32 + 1 : (j->nrows + 31) / 32;  // warps of work
+  int64_t blocks = (units + esc::kJoinThreads / 32 - 1) / (esc::kJoinThreads / 32);
   if (blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;
-  esc::join_count_kernel<<<(unsigned)blocks, esc::kJoinThreads, smem, st>>>(p);
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, esc::kJoinThreads, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("join count launch: ") + cudaGetErrorString(e));
   return ESC_OK;

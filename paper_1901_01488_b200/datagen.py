@@ -212,6 +212,11 @@ CONFIG3_WHERE = {
 CONFIG3_EDGES = [("fact", "f_datekey", "date", "d_datekey"), ("fact", "f_custkey", "customer", "c_custkey"),
                  ("fact", "f_suppkey", "supplier", "s_suppkey"), ("fact", "f_partkey", "part", "p_partkey")]
 
+# the reference's answer for the config-3 star query over the 60M-row fact (COUNT and stage
+# counts of execute_plan), pinned in tests/golden/known.json["star_execute"]
+CONFIG3_STAR_COUNT = 21105
+CONFIG3_STAR_PROBE_OUT = [60_000_000, 4_559_813, 1_303_361, 260_088, 21_105]
+
 
 # ---- block-seeded variants for the 600M-row benchmarks ----------------------------------------
 # The exact Appendix B recipes above draw each column from one sequential stream, which takes

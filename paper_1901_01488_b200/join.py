@@ -183,9 +183,11 @@ class ExecStats:
 # ------------------------------------------------------------------------------------------------
 # COUNT pipeline: one fused pass
 # ------------------------------------------------------------------------------------------------
-DENSE_SPAN_FACTOR = 4        # a key range up to 4x the distinct keys is indexed directly
-DENSE_SPAN_MIN = 1 << 16
-DENSE_SPAN_MAX = 1 << 27
+# a key range is indexed directly (factor[key - min]) when that array is small: at most
+# DENSE_MAX_BYTES, or no bigger than DENSE_VS_HASH x the hash table it replaces
+DENSE_MAX_BYTES = 8 << 20
+DENSE_VS_HASH = 4
+DENSE_SPAN_MAX = 1 << 28
 
 
 def _factor_array(index: HashTableIndex):
@@ -196,11 +198,14 @@ def _factor_array(index: HashTableIndex):
         return None
     lo, hi = int(index.unique_keys[0]), int(index.unique_keys[-1])
     span = hi - lo + 1
-    if span > max(DENSE_SPAN_FACTOR * u, DENSE_SPAN_MIN) or span > DENSE_SPAN_MAX:
+    most = int(index.group_counts.max())
+    bits = 1 if most <= 1 else 8 if most < 256 else 16 if most < 65536 else 32 if most < (1 << 32) else 64
+    nbytes = span * bits // 8
+    hash_bytes = index.capacity * 8 + u * 16
+    if span > DENSE_SPAN_MAX or nbytes > max(DENSE_MAX_BYTES, DENSE_VS_HASH * hash_bytes):
         return None
     dev = index.table.device
     idx = index.unique_keys - lo
-    most = int(index.group_counts.max())
     if most <= 1:
         words = torch.zeros(((span + 31) // 32 + 3) // 4 * 4, dtype=torch.int64, device=dev)
         words.scatter_add_(0, idx >> 5, torch.ones_like(idx) << (idx & 31))
@@ -287,8 +292,11 @@ def _count_pipeline(probe: ColumnTable, probe_alias: str, probe_pred, steps: lis
     j.n_steps = len(probe_keyed)
     out = torch.empty(S + 1, dtype=torch.int64, device=probe.device)
     lib = N.load_library()
-    N.check(lib.esc_join_count(C.byref(j), C.c_void_p(out.data_ptr()),
-                               C.c_void_p(_stream(probe.device).cuda_stream)), "esc_join_count")
+    stream = _stream(probe.device)
+    ev0 = executor._ev_start(stream)
+    N.check(lib.esc_join_count(C.byref(j), C.c_void_p(out.data_ptr()), C.c_void_p(stream.cuda_stream)),
+            "esc_join_count")
+    executor._ev_end(stream, ev0, "join")
     counts = [int(x) for x in out.cpu().tolist()]
     del keep
     return counts
