@@ -352,6 +352,8 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream);
 /* ---- misc ------------------------------------------------------------------------------- */
 
 const char* esc_last_error(void);
+/* Kernels this library has launched since it was loaded (all entry points, all threads). */
+int64_t esc_launch_count(void);
 int esc_abi_version(void);
 /* Number of SMs of the current device (0 when no device). */
 int esc_device_sm_count(void);

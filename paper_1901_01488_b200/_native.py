@@ -133,6 +133,7 @@ _SIGNATURES = {
     "esc_gather": (C.c_int, [C.POINTER(EscColumn), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                              C.c_void_p]),
     "esc_last_error": (C.c_char_p, []),
+    "esc_launch_count": (C.c_int64, []),
     "esc_abi_version": (C.c_int, []),
     "esc_device_sm_count": (C.c_int, []),
     "esc_struct_size": (C.c_int, [C.c_int]),

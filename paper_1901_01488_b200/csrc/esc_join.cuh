@@ -358,6 +358,7 @@ int esc_hash_insert(const int64_t* unique_keys, int64_t n_unique, int64_t* slots
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   int64_t blocks = (n_unique + 255) / 256;
   if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  ++g_launches;
   esc::hash_insert_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const long long*>(unique_keys), n_unique,
                                                             reinterpret_cast<unsigned long long*>(slots),
                                                             (unsigned long long)capacity - 1);
@@ -391,6 +392,7 @@ int esc_hash_probe(const int64_t* slots, int64_t capacity, const int64_t* unique
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+  ++g_launches;
   esc::hash_probe_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash probe launch: ") + cudaGetErrorString(e));
@@ -407,6 +409,7 @@ int esc_expand(const int64_t* groups, const int64_t* offsets, int64_t n, const i
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+  ++g_launches;
   esc::expand_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const long long*>(groups), reinterpret_cast<const long long*>(offsets), n,
       reinterpret_cast<const long long*>(group_start), reinterpret_cast<const long long*>(group_rows),
@@ -513,6 +516,7 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
   int64_t blocks = (units + esc::kJoinThreads / 32 - 1) / (esc::kJoinThreads / 32);
   if (blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;
   if (blocks < 1) blocks = 1;
+  ++g_launches;
   kern<<<(unsigned)blocks, esc::kJoinThreads, smem, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("join count launch: ") + cudaGetErrorString(e));

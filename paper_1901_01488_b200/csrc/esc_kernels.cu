@@ -55,6 +55,7 @@ namespace {
 using namespace esc;
 
 thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};  // kernels this library has launched (esc_launch_count)
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -548,6 +549,7 @@ int launch_c(const KParams& kp, cudaStream_t stream) {
         attr[0].val.cooperative = COMPACT ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        ++g_launches;
         cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), args);
         if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("JIT kernel launch: ") + cudaGetErrorString(e));
         return ESC_OK;
@@ -559,9 +561,11 @@ int launch_c(const KParams& kp, cudaStream_t stream) {
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
   if (COMPACT) {  // cooperative: all CTAs co-resident (the static-schedule look-back relies on it)
     void* args[] = {const_cast<KParams*>(&kp)};
+    ++g_launches;
     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid),
                                     dim3(Layout<COMPACT>::kThreads), args, smem, stream);
   } else {
+    ++g_launches;
     kern<<<(unsigned)grid, Layout<COMPACT>::kThreads, smem, stream>>>(kp);
     e = cudaGetLastError();
   }
@@ -807,8 +811,10 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const unsigned segs = (unsigned)((sp.n_segs + kScanSeg - 1) / kScanSeg);
+  ++g_launches;
   tile_scan_partials<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, sp.rule.n_dense,
                                                      sp.rule.skip_count, sp.rule.skip_capacity);
+  ++g_launches;
   tile_scan_apply<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, offsets, sp.rule);
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
@@ -823,10 +829,12 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
     }
     int64_t tiles = sp.rule.n_tiles;
     const unsigned grid = (unsigned)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
+    ++g_launches;
     sel_stream_kernel<<<grid, (1 + kStreamConsumers) * 32, smem, st>>>(tp);
   }
   const int64_t want = (sp.n_segs + 32 * kSelWarps - 1) / (32 * kSelWarps);  // 32 segments per warp
   const int64_t grid = want < (int64_t)sms * 16 ? want : (int64_t)sms * 16;
+  ++g_launches;
   sel_compact_kernel<<<(unsigned)grid, kSelWarps * 32, 0, st>>>(sp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("selection compaction launch: ") + cudaGetErrorString(e));
@@ -889,21 +897,25 @@ int esc_gather(const esc_column_t* col, const int64_t* d_idx, int64_t n, void* o
   if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
   switch (w) {
     case 1:
+      ++g_launches;
       gather_kernel<uint8_t><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const uint8_t*>(col->data), col->nulls,
                                                                    d_idx, n, static_cast<uint8_t*>(out_values),
                                                                    out_nulls);
       break;
     case 2:
+      ++g_launches;
       gather_kernel<uint16_t><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const uint16_t*>(col->data),
                                                                     col->nulls, d_idx, n,
                                                                     static_cast<uint16_t*>(out_values), out_nulls);
       break;
     case 4:
+      ++g_launches;
       gather_kernel<uint32_t><<<(unsigned)blocks, threads, 0, st>>>(static_cast<const uint32_t*>(col->data),
                                                                     col->nulls, d_idx, n,
                                                                     static_cast<uint32_t*>(out_values), out_nulls);
       break;
     default:
+      ++g_launches;
       gather_kernel<unsigned long long><<<(unsigned)blocks, threads, 0, st>>>(
           static_cast<const unsigned long long*>(col->data), col->nulls, d_idx, n,
           static_cast<unsigned long long*>(out_values), out_nulls);
@@ -936,6 +948,7 @@ int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const 
   const long long cap = std::max(1ll, (long long)sms * 8 / n);
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
+  ++g_launches;
   copy_regions_kernel<<<dim3((unsigned)bx, (unsigned)n), 256, 0, static_cast<cudaStream_t>(stream)>>>(cr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("copy launch: ") + cudaGetErrorString(e));
@@ -943,6 +956,8 @@ int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const 
 }
 
 const char* esc_last_error(void) { return g_last_error.c_str(); }
+
+int64_t esc_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int esc_abi_version(void) { return ESC_ABI_VERSION; }
 

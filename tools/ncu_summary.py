@@ -1,7 +1,7 @@
 """Summarise ncu captures for profiles/ (not part of the product).
 
-python tools/ncu_summary.py <report.ncu-rep> <label> [--traffic-key KEY]
-  -> appends a markdown section to profiles/ncu_r01.md and (with --traffic-key) records the
+python tools/ncu_summary.py <report.ncu-rep> <label> [--traffic-key KEY] [--out FILE]
+  -> appends a markdown section to profiles/ncu_r01.md (or FILE) and (with --traffic-key) records the
      launch's DRAM bytes in profiles/traffic.json (read by bench.py for roofline.traffic).
 """
 
@@ -26,6 +26,8 @@ METRICS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
     ("smsp__sass_inst_executed_op_local_ld.sum", "local loads"),
+    ("launch__shared_mem_per_block_dynamic", "dynamic smem/block"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
 ]
 
 
@@ -60,7 +62,8 @@ def main():
             data = json.load(open(path)) if os.path.exists(path) else {}
             data[key] = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
             json.dump(data, open(path, "w"), indent=1)
-    with open(os.path.join(ROOT, "profiles", "ncu_r01.md"), "a") as fh:
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join(ROOT, "profiles", "ncu_r01.md")
+    with open(out, "a") as fh:
         fh.write("\n".join(lines) + "\n")
 
 
