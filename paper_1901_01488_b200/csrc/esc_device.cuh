@@ -1340,8 +1340,8 @@ __device__ __forceinline__ void gather4(const uint8_t* data, void* out, const bo
 
 // One warp per 32 consecutive segments (seg_rows = 128*C rows = 4*C <= 32 bitmap words each):
 //  - captured segments: each LANE copies its own segment's captured hits (<= 4*C per column);
-//  - sparse segments (<= one hit per 32 rows): each lane walks its segment's words, so a warp
-//    keeps 32 independent gathers in flight;
+//  - sparse segments (<= one hit per 32 rows): C lanes per segment, each walking one 128-row
+//    chunk, so a warp keeps 32 independent chunks' gathers in flight;
 //  - dense segments: the whole warp, one row per lane of each word (contiguous reads/writes).
 // Segments of dense stream tiles are skipped (sel_stream_kernel writes them).
 __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
@@ -1382,26 +1382,50 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
       }
     }
     const bool bitmap_work = cnt > 0 && (!captured || p.need_bitmap_captured);
-    // ---- sparse segments: one lane walks its segment's words ----
-    if (bitmap_work && cnt <= sparse_max) {
-      unsigned long long pos = myoff;
-      for (int i = 0; i < W; ++i) {
-        uint32_t word = p.bitmap[myseg * W + i];
-        while (word) {
-          const int b = __ffs(word) - 1;
-          word &= word - 1;
-          if ((long long)pos < cap) {
-            const int64_t row = (myseg * W + i) * 32 + b;
-            const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
-            for (int k = 0; k < p.n_proj; ++k) {
-              if (captured && p.cap_index[k] >= 0) continue;
-              const KCol& col = p.cols[k];
-              st_bits(col.width, p.outs.out_values[k], pos, ld_bits(col, prow));
-              if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
+    // ---- sparse segments: C lanes per segment, one 128-row chunk (4 bitmap words) each: a
+    //      16-byte bitmap load per lane, a width-C segmented scan for the chunk's output base,
+    //      then the chunk's hits (32 * C chunks in flight per warp instead of 32 segments) ----
+    {
+      const bool sparse_work = bitmap_work && cnt <= sparse_max;
+      const int CPS = W / 4;  // chunks per segment (1, 2, 4, 8): a power of two
+      for (int b = 0; b < CPS; ++b) {
+        const int c = b * 32 + lane;
+        const int sl = c / CPS;  // lane owning the chunk's segment
+        const int sub = c % CPS;
+        const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
+        const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, myoff, sl);
+        const bool scap = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, sl) != 0;
+        const int64_t seg = seg0 + sl;
+        uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
+        if (work) w4 = *reinterpret_cast<const uint4*>(p.bitmap + seg * W + sub * 4);
+        const uint32_t pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+        uint32_t incl = pc;
+        for (int d = 1; d < CPS; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d, CPS);
+          if ((lane & (CPS - 1)) >= d) incl += t;
+        }
+        if (!work || pc == 0) continue;
+        unsigned long long pos = soff + incl - pc;
+        const uint32_t words[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+          uint32_t word = words[wi];
+          while (word) {
+            const int bit = __ffs(word) - 1;
+            word &= word - 1;
+            if ((long long)pos < cap) {
+              const int64_t row = (seg * W + sub * 4 + wi) * 32 + bit;
+              const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
+              for (int k = 0; k < p.n_proj; ++k) {
+                if (scap && p.cap_index[k] >= 0) continue;
+                const KCol& col = p.cols[k];
+                st_bits(col.width, p.outs.out_values[k], pos, ld_bits(col, prow));
+                if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
+              }
+              if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
             }
-            if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
+            ++pos;
           }
-          ++pos;
         }
       }
     }
