@@ -222,14 +222,21 @@ def dtype_code(t: torch.Tensor) -> int:
 # --------------------------------------------------------------------------------------------
 # per-(device, stream) workspace and result slot
 # --------------------------------------------------------------------------------------------
+RESULT_SLOTS = 64
+
+
 class _Workspace:
     def __init__(self, device: torch.device):
         self.device = device
         self.buf: torch.Tensor | None = None
         self.nbytes = 0
+        self.ptr = 0
+        self.covers = 0  # largest row count known to fit (workspace size grows with rows)
         # result block written by the last CTA of every launch: pinned host memory is mapped
         # into the device address space under UVA, so no D2H copy is issued
         self.result = torch.zeros(C.sizeof(EscResult), dtype=torch.uint8, pin_memory=True)
+        # more result blocks for steps queued together before one host wait (slots 1..RESULT_SLOTS)
+        self.results = torch.zeros(RESULT_SLOTS * C.sizeof(EscResult), dtype=torch.uint8, pin_memory=True)
         # device-side result block (for NCCL reductions of counts)
         self.dresult = torch.zeros(C.sizeof(EscResult), dtype=torch.uint8, device=device)
         # device copy of the last selection count (queued compactions check it on the device)
@@ -238,6 +245,8 @@ class _Workspace:
         self.scratch: dict = {}
 
     def ensure(self, nrows: int, stream_ptr: int) -> tuple[int, int]:
+        if self.buf is not None and nrows <= self.covers:
+            return self.ptr, self.nbytes
         lib = load_library()
         need = int(lib.esc_workspace_bytes(max(int(nrows), 1)))
         if self.buf is None or self.nbytes < need:
@@ -246,10 +255,19 @@ class _Workspace:
             self.nbytes = size
             check(lib.esc_workspace_init(C.c_void_p(self.buf.data_ptr()), C.c_size_t(size),
                                          C.c_void_p(stream_ptr)), "esc_workspace_init")
-        return self.buf.data_ptr(), self.nbytes
+            self.ptr = self.buf.data_ptr()
+        self.covers = max(self.covers, int(nrows)) if need <= self.nbytes else self.covers
+        return self.ptr, self.nbytes
 
-    def read_result(self, n_udfs: int = 0) -> tuple[int, list[int]]:
-        r = EscResult.from_address(self.result.data_ptr())
+    def result_ptr(self, slot: int = 0) -> int:
+        if slot == 0:
+            return self.result.data_ptr()
+        if not 1 <= slot <= RESULT_SLOTS:
+            raise ValueError(f"result slot {slot} out of range")
+        return self.results.data_ptr() + (slot - 1) * C.sizeof(EscResult)
+
+    def read_result(self, n_udfs: int = 0, slot: int = 0) -> tuple[int, list[int]]:
+        r = EscResult.from_address(self.result_ptr(slot))
         return int(r.count), [int(r.udf_fail[i]) for i in range(n_udfs)]
 
 

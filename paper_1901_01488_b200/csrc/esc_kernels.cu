@@ -373,6 +373,12 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
   while (chunks > 1 &&
          (uint64_t)kConsumerWarps * kChunkRows * chunks * (per_row + scratch_row) * min_stages > kSmemBudget)
     chunks >>= 1;
+  // small tables are latency-bound: smaller tiles spread them over more SMs (a 30K-row one-pass
+  // compaction: 25 us at C = 4 on 8 CTAs, 17 us at C = 1 on 30)
+  {
+    const int sms = sm_count_cached() > 0 ? sm_count_cached() : 148;
+    while (chunks > 1 && nrows < (int64_t)sms * 2 * kConsumerWarps * kChunkRows * chunks) chunks >>= 1;
+  }
   if (const char* e = getenv("ESC_CHUNKS")) {  // tuning override (experiments only)
     const int v = atoi(e);
     if (v == 1 || v == 2 || v == 4 || (v == 8 && outs == nullptr)) chunks = v;

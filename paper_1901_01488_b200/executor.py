@@ -473,6 +473,8 @@ ONEPASS_MAX_ROWS = int(os.environ.get("ESC_ONEPASS_MAX_ROWS", str(1 << 21)))
 # the compaction is queued behind the scan (one host round trip per table) when its
 # capacity-sized output buffers stay below this many bytes
 SPECULATE_BYTES = int(os.environ.get("ESC_SPECULATE_BYTES", str(4 << 30)))
+# capacity-sized outputs up to this size become the temp as views (no trim copy)
+SMALL_OUTPUT_BYTES = int(os.environ.get("ESC_SMALL_OUTPUT_BYTES", str(1 << 20)))
 # device bytes the cached step plans (selection + capacity-sized output buffers) may hold per stream
 STEP_PLAN_BYTES = int(os.environ.get("ESC_STEP_PLAN_BYTES", str(8 << 30)))
 
@@ -485,17 +487,105 @@ def count_and_materialize(table: ColumnTable, pred: ex.Expr, needed, capacity: i
     the qualifying rows are then trimmed out of the ``capacity``-row buffers.  Small tables take
     the single-launch one-pass kernel with the output bounded by ``capacity``.  Returns
     ``(count, columns or None)``."""
-    if table.row_count <= ONEPASS_MAX_ROWS:
-        count, cols = materialize_onepass(table, pred, needed, capacity)
-        return count, (cols if count <= capacity else None)
+    ps = launch_step(table, pred, needed, capacity, slot=1)
+    _stream(table.device).synchronize()
+    return finish_step(ps)
+
+
+@dataclass
+class PendingStep:
+    """An ESC step whose kernels are queued and whose result has not been read back yet
+    (``launch_step`` / ``finish_step``): steps of independent tables share one host wait."""
+
+    table: ColumnTable
+    cp: CompiledPredicate | None
+    proj: list
+    capacity: int
+    kind: str                   # "count" | "onepass" | "queued" | "done"
+    slot: int = 0
+    plan: object = None
+    result: tuple | None = None
+
+
+def launch_step(table: ColumnTable, pred: ex.Expr, needed, capacity: int, materialize: bool = True,
+                slot: int = 1) -> PendingStep:
+    """Queue one table's ESC step on the stream without waiting: K1 count (``materialize``
+    False), the one-pass compaction (small tables) or K1 select + the queued compaction; the
+    kernels' result block is the workspace's pinned ``slot`` (1 .. N.RESULT_SLOTS)."""
+    cp = compile_predicate(table, pred)
+    n = table.row_count
+    lib = N.load_library()
+    stream = _stream(table.device)
+    ws = N.workspace(table.device, stream)
+    ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
+    res = C.c_void_p(ws.result_ptr(slot))
+    sp = C.c_void_p(stream.cuda_stream)
+    if not materialize:
+        ev0 = _ev_start(stream)
+        N.check(lib.esc_scan_count(C.byref(cp.program), cp.column_array(), cp.ncols, n, None, res,
+                                   C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp), "esc_scan_count")
+        _ev_end(stream, ev0, "count")
+        return PendingStep(table, cp, [], capacity, "count", slot)
     proj = [table.column(name) for name in needed]
+    cap = max(0, min(int(capacity), n))
+    if n <= ONEPASS_MAX_ROWS:
+        plan = _onepass_plan(cp, table, proj, cap, ws)
+        ev0 = _ev_start(stream)
+        N.check(lib.esc_compact_onepass(C.byref(cp.program), plan.mat_cols, plan.mat_ncols, n, None,
+                                        C.byref(plan.outs), res, C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
+                "esc_compact_onepass")
+        _ev_end(stream, ev0, "compact")
+        return PendingStep(table, cp, proj, cap, "onepass", slot, plan)
     row_bytes = sum(c.values.element_size() + (1 if c.nulls is not None else 0) for c in proj)
-    if not (0 < capacity and capacity * max(row_bytes, 1) <= SPECULATE_BYTES):
-        sel = select(table, pred, capture=needed)
-        if sel.count > capacity:
-            return sel.count, None
-        return sel.count, materialize_selection(sel, needed)
-    return _queued_step(table, pred, proj, capacity)
+    if not (0 < cap and cap * max(row_bytes, 1) <= SPECULATE_BYTES):
+        sel = select(table, pred, capture=needed)  # waits: the count sizes the output
+        if sel.count > cap:
+            return PendingStep(table, None, proj, cap, "done", result=(sel.count, None))
+        return PendingStep(table, None, proj, cap, "done", result=(sel.count, materialize_selection(sel, needed)))
+    plan = _step_plan(cp, table, proj, cap, ws)
+    ev0 = _ev_start(stream)
+    N.check(lib.esc_scan_select(C.byref(cp.program), cp.column_array(), cp.ncols, n, None, C.byref(plan.sel.desc),
+                                res, C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp), "esc_scan_select")
+    _ev_end(stream, ev0, "select")
+    ev0 = _ev_start(stream)
+    N.check(lib.esc_materialize_selection(C.byref(plan.sel.desc), n, plan.mat_cols, plan.mat_ncols, None,
+                                          C.byref(plan.outs), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
+            "esc_materialize_selection")
+    _ev_end(stream, ev0, "materialize")
+    return PendingStep(table, cp, proj, cap, "queued", slot, plan)
+
+
+def finish_step(ps: PendingStep):
+    """Read back a launched step (after its stream has been synchronised): the reference's UDF
+    errors, then ``(count, columns or None)`` — None when the count exceeds the capacity."""
+    if ps.kind == "done":
+        return ps.result
+    table, cp = ps.table, ps.cp
+    stream = _stream(table.device)
+    ws = N.workspace(table.device, stream)
+    count, fails = ws.read_result(cp.n_udfs, ps.slot)
+    if cp.unbound or cp.may_fail:
+        raise_udf_errors(table, cp, fails, None, table.row_count)
+    if ps.kind == "count":
+        return count, None
+    return count, _take_outputs(ps, ws, count) if count <= ps.capacity else _release(ps, ws)
+
+
+def _release(ps: PendingStep, ws):
+    _plan_checkin(ws, ps.plan)
+    return None
+
+
+def _take_outputs(ps: PendingStep, ws, k: int) -> list[Column]:
+    """The first ``k`` rows of a finished step's outputs as temp columns; small one-pass outputs
+    are handed over as views (their plan is not cached again), others trimmed by one copy."""
+    plan = ps.plan
+    if ps.kind == "onepass" and plan.nbytes <= SMALL_OUTPUT_BYTES:
+        return [Column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
+                for c, v, m in zip(ps.proj, plan.out_values, plan.out_nulls)]
+    cols = _trim(ps.proj, plan.out_values, plan.out_nulls, k, _stream(ps.table.device))
+    _plan_checkin(ws, plan)
+    return cols
 
 
 @dataclass
@@ -517,10 +607,8 @@ class _StepPlan:
 
 def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: int, ws) -> _StepPlan:
     key = (id(cp), id(table), tuple(c.name for c in proj), capacity)
-    plans = ws.scratch.setdefault("plans", {})
-    plan = plans.pop(key, None)
+    plan = ws.scratch.setdefault("plans", {}).pop(key, None)  # checked out until finish_step
     if plan is not None:
-        plans[key] = plan  # most recently used last
         return plan
     n = table.row_count
     _, _, sel = _plan_selection(cp, table, n, [c.name for c in proj], ws)
@@ -551,10 +639,16 @@ def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: 
         outs.out_nulls[k] = m.data_ptr() if m is not None else None
     plan = _StepPlan(key, cp, sel, outs, values, nulls, cols, nscan + len(extra))
     plan.nbytes = sum(b.numel() * b.element_size() for b in [*sel.buffers, *values, *[m for m in nulls if m is not None]])
-    plans[key] = plan
-    while len(plans) > 1 and sum(p.nbytes for p in plans.values()) > STEP_PLAN_BYTES:
-        plans.pop(next(iter(plans)))  # evict least recently used
     return plan
+
+
+def _plan_checkin(ws, plan):
+    """Return a finished step's plan to the stream's cache (most recently used last; least
+    recently used plans are dropped beyond STEP_PLAN_BYTES)."""
+    plans = ws.scratch.setdefault("plans", {})
+    plans[plan.key] = plan
+    while len(plans) > 1 and sum(p.nbytes for p in plans.values()) > STEP_PLAN_BYTES:
+        plans.pop(next(iter(plans)))
 
 
 def release_step_plans(device: torch.device | None = None):
@@ -563,36 +657,64 @@ def release_step_plans(device: torch.device | None = None):
     N.workspace(dev, torch.cuda.current_stream(dev)).scratch.pop("plans", None)
 
 
-def _queued_step(table: ColumnTable, pred: ex.Expr, proj: list, capacity: int):
-    """Scan + compaction queued back to back (the compaction checks the count on the device),
-    one host wait, then ONE batched copy trims the qualifying rows out of the plan's buffers."""
-    cp = compile_predicate(table, pred)
+def materialize_onepass(table: ColumnTable, pred: ex.Expr, needed, capacity: int | None = None):
+    """Single-pass variant (decoupled look-back kernel); same results as :func:`materialize`.
+    Rows beyond ``capacity`` are counted, not written: returns ``(count, columns of the first
+    min(count, capacity) qualifying rows)``."""
     n = table.row_count
-    lib = N.load_library()
-    stream = _stream(table.device)
-    ws = N.workspace(table.device, stream)
-    ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
-    plan = _step_plan(cp, table, proj, capacity, ws)
-    sp = C.c_void_p(stream.cuda_stream)
-    ev0 = _ev_start(stream)
-    N.check(lib.esc_scan_select(C.byref(cp.program), cp.column_array(), cp.ncols, n, None, C.byref(plan.sel.desc),
-                                C.c_void_p(ws.result.data_ptr()), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
-            "esc_scan_select")
-    _ev_end(stream, ev0, "select")
-    ev0 = _ev_start(stream)
-    N.check(lib.esc_materialize_selection(C.byref(plan.sel.desc), n, plan.mat_cols, plan.mat_ncols, None,
-                                          C.byref(plan.outs), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
-            "esc_materialize_selection")
-    _ev_end(stream, ev0, "materialize")
-    stream.synchronize()
-    count, fails = ws.read_result(cp.n_udfs)
-    if cp.unbound or cp.may_fail:
-        raise_udf_errors(table, cp, fails, None, n)
-    if count > capacity:
-        return count, None
-    # exact-size temp columns: one allocation, one batched copy launch
+    cap = n if capacity is None else max(0, min(int(capacity), n))
+    ps = launch_step(table, pred, needed, cap, slot=1) if n <= ONEPASS_MAX_ROWS else None
+    if ps is None:  # large tables: force the one-pass kernel anyway (tests, tuning)
+        cp = compile_predicate(table, pred)
+        proj = [table.column(name) for name in needed]
+        count, fails, values, nulls, _ = launch_compact(cp, table, None, n, proj, cap, want_row_ids=False)
+        if cp.unbound or cp.may_fail:
+            raise_udf_errors(table, cp, fails, None, n)
+        return count, _trim(proj, values, nulls, min(count, cap), _stream(table.device))
+    _stream(table.device).synchronize()
+    ws = N.workspace(table.device, _stream(table.device))
+    count, fails = ws.read_result(ps.cp.n_udfs, ps.slot)
+    if ps.cp.unbound or ps.cp.may_fail:
+        raise_udf_errors(table, ps.cp, fails, None, n)
+    return count, _take_outputs(ps, ws, min(count, cap))
+
+
+def _onepass_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: int, ws) -> _StepPlan:
+    key = ("onepass", id(cp), id(table), tuple(c.name for c in proj), capacity)
+    plan = ws.scratch.setdefault("plans", {}).pop(key, None)  # checked out until finished
+    if plan is not None:
+        return plan
+    extra, slots = [], []
+    for col in proj:
+        if col.name in cp.slot_of:
+            slots.append(cp.slot_of[col.name])
+        else:
+            slots.append(cp.ncols + len(extra))
+            extra.append(col)
+    if cp.ncols + len(extra) > N.MAX_COLS or len(proj) > N.MAX_PROJ:
+        raise ExecutionError("too many columns for one compaction")
+    outs = N.EscOutputs()
+    outs.n_proj = len(proj)
+    outs.capacity = capacity
+    values, nulls = [], []
+    for k, col in enumerate(proj):
+        v = torch.empty(max(capacity, 1), dtype=col.values.dtype, device=table.device)
+        m = torch.empty(max(capacity, 1), dtype=torch.bool, device=table.device) if col.nulls is not None else None
+        values.append(v)
+        nulls.append(m)
+        outs.slot[k] = slots[k]
+        outs.out_values[k] = v.data_ptr() if capacity else None
+        outs.out_nulls[k] = m.data_ptr() if m is not None and capacity else None
+    plan = _StepPlan(key, cp, None, outs, values, nulls, cp.column_array(extra), cp.ncols + len(extra))
+    plan.nbytes = sum(b.numel() * b.element_size() for b in [*values, *[m for m in nulls if m is not None]])
+    return plan
+
+
+def _trim(proj: list, values: list, nulls: list, count: int, stream) -> list[Column]:
+    """Exact-size temp columns: the first ``count`` rows of each capacity-sized output, carved
+    from ONE allocation by ONE batched copy launch (esc_copy_regions)."""
     regions = []
-    for v, m in zip(plan.out_values, plan.out_nulls):
+    for v, m in zip(values, nulls):
         regions.append((v, count * v.element_size()))
         if m is not None:
             regions.append((m, count))
@@ -600,14 +722,20 @@ def _queued_step(table: ColumnTable, pred: ex.Expr, proj: list, capacity: int):
     for _, nb in regions:
         offs.append(total)
         total += (nb + 255) & ~255
-    buf = torch.empty(max(total, 1), dtype=torch.uint8, device=table.device)
+    dev = values[0].device if values else None
+    out = []
+    if not regions:
+        return out
+    buf = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
     k = len(regions)
-    dst = (C.c_void_p * k)(*[buf.data_ptr() + o for o in offs])
-    src = (C.c_void_p * k)(*[t.data_ptr() for t, _ in regions])
-    nbytes = (C.c_int64 * k)(*[nb for _, nb in regions])
-    N.check(lib.esc_copy_regions(k, dst, src, nbytes, sp), "esc_copy_regions")
-    out, r = [], 0
-    for c, v, m in zip(proj, plan.out_values, plan.out_nulls):
+    if count:
+        dst = (C.c_void_p * k)(*[buf.data_ptr() + o for o in offs])
+        src = (C.c_void_p * k)(*[t.data_ptr() for t, _ in regions])
+        nbytes = (C.c_int64 * k)(*[nb for _, nb in regions])
+        N.check(N.load_library().esc_copy_regions(k, dst, src, nbytes, C.c_void_p(stream.cuda_stream)),
+                "esc_copy_regions")
+    r = 0
+    for c, v, m in zip(proj, values, nulls):
         vv = buf[offs[r]: offs[r] + count * v.element_size()].view(v.dtype)
         r += 1
         mm = None
@@ -615,26 +743,7 @@ def _queued_step(table: ColumnTable, pred: ex.Expr, proj: list, capacity: int):
             mm = buf[offs[r]: offs[r] + count].view(torch.bool)
             r += 1
         out.append(Column(c.name, c.kind, vv, mm, c.dictionary))
-    return count, out
-
-
-def materialize_onepass(table: ColumnTable, pred: ex.Expr, needed, capacity: int | None = None):
-    """Single-pass variant (decoupled look-back kernel); same results as :func:`materialize`."""
-    cp = compile_predicate(table, pred)
-    ids, n = _row_ids(RowSelection(table))
-    proj = [table.column(name) for name in needed]
-    cap = n if capacity is None else max(0, min(int(capacity), n))
-    count, fails, values, nulls, _ = launch_compact(cp, table, ids, n, proj, cap, want_row_ids=False)
-    if cp.unbound or cp.may_fail:
-        raise_udf_errors(table, cp, fails, ids, n)
-    k = min(count, cap)
-    out = []
-    for c, v, m in zip(proj, values, nulls):
-        if k < cap:  # keep temps compact: copy the hits out of the capacity-sized buffer
-            v = v[:k].clone()
-            m = m[:k].clone() if m is not None else None
-        out.append(Column(c.name, c.kind, v, m, c.dictionary))
-    return count, out
+    return out
 
 
 def take_column(col: Column, indices) -> Column:

@@ -182,3 +182,37 @@ def test_star_query_executes_like_reference(cuda):
     assert res.stats.probe_out == want["probe_out"]
     assert res.plan.build_order == want["order"]
     assert eng.catalog.temps.live_handles() == []
+
+
+def test_batched_esc_keeps_the_reference_error_sequence(cuda):
+    """plan() queues every table's sub-query before one host wait; results are still read in the
+    reference's order: a UDF failing on the second table raises the reference's message after
+    the first table's temp was registered, and nothing of later tables survives."""
+    from paper_1901_01488_b200 import Catalog, expr as ex, ra
+    from paper_1901_01488_b200.errors import ExecutionError
+    from paper_1901_01488_b200.optimizer import EscConfig, plan
+
+    cat = Catalog()
+    n = 5000
+    fact = _int_table("fact", cuda, fa=list(range(n)), fb=list(range(n)), fc=list(range(n)))
+    cat.register(fact)
+    cat.register(_int_table("a", cuda, ka=list(range(2000)), va=[i % 10 for i in range(2000)]))
+    cat.register(_int_table("b", cuda, kb=list(range(2000)), vb=[i % 7 for i in range(2000)]))
+    cat.register(_int_table("c", cuda, kc=list(range(2000)), vc=[i % 5 for i in range(2000)]))
+    r = ex.ColumnRef
+    inv = ex.FnCall("inv", (r("b", "vb"),), ">", 0.5, lambda x: 1.0 / x)
+    where = ex.And((ex.ColumnCompare(r("fact", "fa"), "=", r("a", "ka")),
+                    ex.ColumnCompare(r("fact", "fb"), "=", r("b", "kb")),
+                    ex.ColumnCompare(r("fact", "fc"), "=", r("c", "kc")),
+                    ex.Equality(r("a", "va"), 3), inv, ex.Equality(r("c", "vc"), 1)))
+    q = ra.query(cat, ["fact", "a", "b", "c"], where)
+    with pytest.raises(ExecutionError) as err:
+        plan(q, cat, EscConfig(min_table_size=1))
+    assert str(err.value) == "count sub-query on 'b' failed: UDF 'inv' failed at row 0: float division by zero"
+    assert len(cat.temps.live_handles()) == 1  # table a's temp, as the reference leaves it
+    cat.temps.sweep()
+    ok = plan(ra.query(cat, ["fact", "a", "c"], ex.And((where.items[0], where.items[2], where.items[3],
+                                                       where.items[5]))), cat, EscConfig(min_table_size=1))
+    assert [(d.table, d.exact_count, d.pushed_down) for d in ok.decisions] == [("a", 200, True), ("c", 400, True)]
+    assert sum(d.subquery_ms for d in ok.decisions) > 0
+    cat.temps.sweep()
