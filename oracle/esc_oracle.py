@@ -367,3 +367,110 @@ def probe_joins(probe: OTable, probe_alias: str, probe_pred, steps, projection=N
         used.add(name)
         out[name] = c
     return stage_out, out
+
+
+# ---------------------------------------------------------------------------------------------
+# equi-depth histograms + estimator: reference catalog.py:178-326
+# ---------------------------------------------------------------------------------------------
+def build_histogram(values: np.ndarray, nulls: np.ndarray, buckets: int) -> dict:
+    """catalog.py:178-223: sort the non-NULL values, edges at ranks (i*n)//k - 1 (duplicates
+    collapse buckets), counts by right-searchsorted, distincts by np.unique per bucket."""
+    valid = np.sort(values[~nulls].astype(np.int64))
+    n = valid.size
+    out = {"null_count": int(values.size - n), "row_count": int(values.size)}
+    if n == 0:
+        out.update(boundaries=[0], counts=[], distincts=[])
+        return out
+    k = min(buckets, n)
+    edges = [int(valid[0])]
+    for i in range(1, k + 1):
+        e = int(valid[min(n - 1, (i * n) // k - 1)])
+        if e > edges[-1]:
+            edges.append(e)
+    if len(edges) == 1:
+        edges.append(edges[0])
+    counts, distincts, lo = [], [], 0
+    for b in range(len(edges) - 1):
+        hi = n if b == len(edges) - 2 else int(np.searchsorted(valid, edges[b + 1], side="right"))
+        counts.append(hi - lo)
+        distincts.append(int(np.unique(valid[lo:hi]).size))
+        lo = hi
+    out.update(boundaries=edges, counts=counts, distincts=distincts)
+    return out
+
+
+def _h_le(h: dict, v: float) -> float:
+    """_estimate_le (catalog.py:226-244)."""
+    if not h["counts"] or h["row_count"] == 0:
+        return 0.0
+    total = 0.0
+    for b in range(len(h["counts"])):
+        lo, hi = h["boundaries"][b], h["boundaries"][b + 1]
+        if v >= hi:
+            total += float(h["counts"][b])
+        elif v < lo:
+            break
+        else:
+            span = hi - lo
+            frac = (v - lo + 1) / (span + 1) if span > 0 else 1.0
+            total += float(h["counts"][b]) * min(1.0, max(0.0, frac))
+            break
+    return total / h["row_count"]
+
+
+def _h_eq(h: dict, v: float) -> float:
+    """_estimate_equality (catalog.py:247-257)."""
+    if not h["counts"] or h["row_count"] == 0:
+        return 0.0
+    if v != int(v):
+        return 0.0
+    for b in range(len(h["counts"])):
+        lo, hi = h["boundaries"][b], h["boundaries"][b + 1]
+        if (lo <= v <= hi) if b == 0 else (lo < v <= hi):
+            return float(h["counts"][b]) / max(1, h["distincts"][b]) / h["row_count"]
+    return 0.0
+
+
+class OracleInestimable(Exception):
+    pass
+
+
+def estimate(h: dict, pred) -> float:
+    """estimate_selectivity + _atom_selectivity (catalog.py:268-326) over one column's histogram;
+    ``pred`` in the JSON form."""
+    def num(x):
+        x = decode_value(x)
+        if isinstance(x, bool) or not isinstance(x, (int, float)):
+            raise OracleInestimable(repr(x))
+        return float(x)
+
+    def clamp(x):
+        return min(1.0, max(0.0, x))
+
+    t = pred[0]
+    if t == "and":
+        s = 1.0
+        for it in pred[1]:
+            s *= estimate(h, it)
+        return clamp(s)
+    if t == "or":
+        miss = 1.0
+        for it in pred[1]:
+            miss *= 1.0 - estimate(h, it)
+        return clamp(1.0 - miss)
+    if t == "not":
+        return clamp(1.0 - estimate(h, pred[1]))
+    if t == "folded":
+        return 1.0 if pred[2] else 0.0
+    if t in ("fn", "colcmp"):
+        raise OracleInestimable(t)
+    present = (h["row_count"] - h["null_count"]) / max(1, h["row_count"])
+    if t == "eq":
+        return clamp(_h_eq(h, num(pred[2])))
+    if t == "range":
+        return clamp(max(0.0, _h_le(h, num(pred[3])) - _h_le(h, num(pred[2]) - 1)))
+    op, v = pred[2], num(pred[3])
+    r = {"<=": lambda: _h_le(h, v), "<": lambda: _h_le(h, v - 1),
+         ">": lambda: max(0.0, present - _h_le(h, v)), ">=": lambda: max(0.0, present - _h_le(h, v - 1)),
+         "<>": lambda: max(0.0, present - _h_eq(h, v))}[op]()
+    return clamp(r)

@@ -2,8 +2,8 @@
 
 Mirrors ``escdb.catalog.Catalog`` (reference ``pkg/src/escdb/catalog.py:63-150``) for everything
 the ESC path touches.  Tables are device-resident :class:`~.storage.ColumnTable` objects; temp
-tables are the compaction kernel's outputs.  The histogram estimator (the reference's contrast
-arm, ``catalog.py:153-326``) is not part of the hot path and is not provided.
+tables are the compaction kernel's outputs.  Histograms of the estimator contrast arm
+(``catalog.py:128-134``, built by :mod:`.histogram`) are cached per (table, column).
 """
 
 from __future__ import annotations
@@ -26,6 +26,7 @@ class Catalog:
     def __init__(self):
         self._tables: dict[str, ColumnTable] = {}
         self._udfs: dict[str, Udf] = {}
+        self._histograms: dict = {}
         self.temps = TempTableStore()
 
     # -- base tables ------------------------------------------------------------------------
@@ -44,7 +45,19 @@ class Catalog:
         self._tables[table.name] = table
 
     def replace(self, table: ColumnTable):
+        """Swap in a rebuilt version of an existing (or new) table (drops its histograms)."""
         self._tables[table.name] = table
+        self._histograms = {k: v for k, v in self._histograms.items() if k[0] != table.name}
+
+    # -- statistics -------------------------------------------------------------------------------
+    def histogram(self, table: str, column: str, buckets: int = 64):
+        """Cached equi-depth histogram (reference ``catalog.py:128-134``), built on the device."""
+        from .histogram import build_histogram
+
+        key = (table, column)
+        if key not in self._histograms:
+            self._histograms[key] = build_histogram(self.table(table), column, buckets)
+        return self._histograms[key]
 
     def table(self, name: str) -> ColumnTable:
         table = self._tables.get(name)

@@ -261,7 +261,8 @@ def shop_known():
     sql = ("SELECT COUNT(*) FROM fact, cust, prod, tiny WHERE f_cid = c_id AND f_pid = p_id AND f_tid = t_id "
            "AND c_band = 3 AND p_cls = 0 AND t_x < 40 AND f_qty < 50")
     out = {}
-    for label, cfg in (("default", REscConfig()), ("min1", REscConfig(min_table_size=1)),
+    for label, cfg in (("histogram", REscConfig(enabled=False, estimator_mode="histogram")),
+                       ("default", REscConfig()), ("min1", REscConfig(min_table_size=1)),
                        ("min5000", REscConfig(min_table_size=5000)), ("nomat", REscConfig(materialize=False)),
                        ("sel0.05", REscConfig(max_selectivity=0.05)), ("off", REscConfig(enabled=False))):
         p = rplan(rfe.analyze(rfe.parse(sql), cat), cat, cfg)
@@ -337,6 +338,34 @@ def join_known():
     return out
 
 
+def histogram_known():
+    """Reference build_histogram + estimate_selectivity on tests/golden/hist_cases.py, and the
+    histogram arm's plans on the shop fixture."""
+    sys.path.insert(0, HERE)
+    import hist_cases
+    from escdb.catalog import build_histogram as rbuild, estimate_selectivity as rest
+    from escdb.errors import Inestimable
+
+    out = {"histograms": {}, "estimates": {}}
+    for name, (vals, nulls) in hist_cases.columns().items():
+        t = RTable("t", [RColumn("v", KIND_INT64, vals, nulls)])
+        for b in hist_cases.BUCKETS:
+            h = rbuild(t, "v", b)
+            out["histograms"][f"{name}/{b}"] = {"boundaries": h.boundaries.tolist(), "counts": h.counts.tolist(),
+                                                "distincts": h.distincts.tolist(), "null_count": int(h.null_count),
+                                                "row_count": int(h.row_count)}
+            if b != 64:
+                continue
+            est = []
+            for j in hist_cases.PREDICATES:
+                try:
+                    est.append(repr(rest(lambda ref: h, json_to_ref(j, t))))
+                except (Inestimable, ValueError, OverflowError) as exc:
+                    est.append(f"error:{type(exc).__name__}")
+            out["estimates"][name] = est
+    return out
+
+
 def star_execute_known():
     """The config-3 star query executed by the reference: plan with ESC, execute_plan COUNT."""
     from escdb.optimizer import execute_plan as rexec
@@ -376,6 +405,8 @@ def main():
         with open(path) as fh:
             known = json.load(fh)
         known["joins"] = join_known()
+        known["histogram"] = histogram_known()
+        known["shop"] = shop_known()
         if "--skip-star" not in sys.argv:
             known["star_execute"] = star_execute_known()
         with open(path, "w") as fh:
@@ -400,6 +431,7 @@ def main():
     with open(os.path.join(HERE, "corpus.json"), "w") as fh:
         json.dump(corpus, fh, separators=(",", ":"))
     known = {"configs": config_known(), "shop": shop_known(), "star": star_known(), "joins": join_known(),
+             "histogram": histogram_known(),
              "star_execute": star_execute_known(),
              "generator": "reference escdb 0.1.0 (pkg/src/escdb), numpy " + np.__version__}
     with open(os.path.join(HERE, "known.json"), "w") as fh:

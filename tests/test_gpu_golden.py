@@ -185,7 +185,8 @@ def test_shop_plans_match_reference(cuda):
     q = _shop_query(cat)
     configs = {"default": EscConfig(), "min1": EscConfig(min_table_size=1),
                "min5000": EscConfig(min_table_size=5000), "nomat": EscConfig(materialize=False),
-               "sel0.05": EscConfig(max_selectivity=0.05), "off": EscConfig(enabled=False)}
+               "sel0.05": EscConfig(max_selectivity=0.05), "off": EscConfig(enabled=False),
+               "histogram": EscConfig(enabled=False, estimator_mode="histogram")}
     for label, want in G.known()["shop"].items():
         p = plan(q, cat, configs[label])
         assert [[d.table, d.exact_count, d.row_count, d.qualified, d.pushed_down] for d in p.decisions] == \

@@ -195,7 +195,10 @@ def test_serde_round_trip():
     assert str(q) == str(p) and serde.to_json(q) == j
 
 
-def test_plan_rejects_histogram_arm():
+def test_histogram_arm_needs_the_device():
+    """The histogram arm builds its synopses on the device: CPU-resident tables fail loudly
+    (no CPU fallback); the baseline arm (no estimates) needs no device."""
+    from paper_1901_01488_b200.errors import NativeUnavailable
     from paper_1901_01488_b200.optimizer import plan
 
     cat = Catalog()
@@ -203,7 +206,7 @@ def test_plan_rejects_histogram_arm():
     cat.register(table("d", k2=range(3), v=range(3)))
     q = ra.query(cat, ["f", "d"], ex.And((ex.ColumnCompare(r("f", "k"), "=", r("d", "k2")),
                                           ex.Comparison(r("d", "v"), "<", 1))))
-    with pytest.raises(PlanError):
+    with pytest.raises(NativeUnavailable):
         plan(q, cat, EscConfig(enabled=False, estimator_mode="histogram"))
     p = plan(q, cat, EscConfig(enabled=False))   # baseline arm: no sub-queries, base cardinalities
     assert p.decisions == [] and p.build_order == ["d"] and p.build_card_sum == 3
