@@ -349,6 +349,31 @@ typedef struct {
  * (executor.py:403-474) without expanding a tuple. */
 int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream);
 
+/* ---- CSV ingestion into device columns --------------------------------- */
+/* replaces storage.load_csv + append_rows' cell conversion (storage.py:245-275, :385-409).
+ * 1. esc_csv_count: totals[0] = field separators, totals[1] = record ends (outside quotes),
+ *    totals[2] = 1 when the text ends inside a quote;
+ * 2. esc_csv_fields: field_end[i] = byte position of separator i, field_kind[i] = 1 ',' / 2 '\n'
+ *    or lone '\r' / 3 "\r\n"; rec_end_field[r] = separator index ending record r;
+ * 3. esc_csv_parse per column: values (INT64 / DECIMAL scaled by 10**scale / DATE epoch days /
+ *    TEXT FNV-1a-64 of the unescaped content + its length), nulls (the \N token), and
+ *    first_error = min over failing cells of ((row * ncols + col) << 4 | code).
+ * The workspace (esc_csv_workspace_bytes) carries the chunk summaries from step 1 to step 2. */
+enum { ESC_CSV_INT64 = 0, ESC_CSV_DECIMAL = 1, ESC_CSV_DATE = 2, ESC_CSV_TEXT = 3 };
+size_t esc_csv_workspace_bytes(int64_t nbytes);
+int esc_csv_count(const uint8_t* d_bytes, int64_t nbytes, uint64_t* d_totals, void* d_ws, size_t ws_bytes,
+                  void* stream);
+int esc_csv_fields(const uint8_t* d_bytes, int64_t nbytes, int64_t* d_field_end, uint8_t* d_field_kind,
+                   int64_t* d_rec_end_field, void* d_ws, size_t ws_bytes, void* stream);
+int esc_csv_parse(const uint8_t* d_bytes, const int64_t* d_field_end, const uint8_t* d_field_kind, int64_t first_field,
+                  int64_t nrows, int32_t ncols, int32_t col, int32_t kind, int32_t scale, int64_t* d_values,
+                  int64_t* d_lengths, uint8_t* d_nulls, uint64_t* d_first_error, void* stream);
+/* TEXT dictionary check: d_bad |= 1 when a cell's content differs from its group representative's
+ * (rep[row], -1 for NULL) — i.e. a 64-bit hash collision. */
+int esc_csv_verify_text(const uint8_t* d_bytes, const int64_t* d_field_end, const uint8_t* d_field_kind,
+                        int64_t first_field, int64_t nrows, int32_t ncols, int32_t col, const int64_t* d_rep,
+                        uint32_t* d_bad, void* stream);
+
 /* ---- misc ------------------------------------------------------------------------------- */
 
 const char* esc_last_error(void);

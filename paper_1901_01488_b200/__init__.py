@@ -13,6 +13,7 @@ from .engine import Engine, OptimizeResult, QueryResult
 from .errors import EscdbError
 from .executor import RowSelection, count_star, eval_predicate, execute_count, materialize
 from .histogram import EquiDepthHistogram, build_histogram, estimate_selectivity
+from .ingest import append_rows, dump_csv, load_csv
 from .join import BuildStep, ExecStats, HashTableIndex, build_hash, execute_plan, probe_joins
 from .optimizer import (
     EscConfig,
@@ -30,7 +31,7 @@ from .storage import Column, ColumnKind, ColumnTable, Dictionary
 __version__ = "0.1.0"
 
 __all__ = [
-    "BuildStep", "Catalog", "EquiDepthHistogram", "build_histogram", "estimate_selectivity", "Column", "ColumnKind", "ColumnTable", "Dictionary", "Engine", "EscConfig",
+    "BuildStep", "Catalog", "EquiDepthHistogram", "append_rows", "dump_csv", "load_csv", "build_histogram", "estimate_selectivity", "Column", "ColumnKind", "ColumnTable", "Dictionary", "Engine", "EscConfig",
     "EscdbError", "ExecStats", "HashTableIndex", "OptimizeResult", "QueryResult", "RowSelection",
     "__version__", "build_hash", "build_join_graph", "execute_plan", "probe_joins",
     "compute_exact_selectivity", "count_star", "decide_pushdown", "eval_predicate",

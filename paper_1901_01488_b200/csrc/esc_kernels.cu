@@ -1030,3 +1030,4 @@ int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t n
 }  // extern "C"
 
 #include "esc_join.cuh"
+#include "esc_csv.cuh"

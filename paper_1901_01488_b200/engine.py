@@ -50,6 +50,16 @@ class Engine:
     def register_udf(self, name: str, arity: int, fn):
         self.catalog.register_udf(name, arity, fn)
 
+    def load_csv_file(self, path: str, table: str, schema_spec: str, has_header: bool = False) -> ColumnTable:
+        """Load a CSV file with a ``name:kind,name:kind`` schema spec into a device table and
+        register it (reference ``engine.py:41-49``); parsing runs on the device."""
+        from .ingest import load_csv
+
+        with open(path, "rb") as fh:
+            loaded = load_csv(fh.read(), table, parse_schema_spec(schema_spec), has_header=has_header)
+        self.catalog.register(loaded)
+        return loaded
+
     def run(self, ra) -> QueryResult:
         """Plan with ESC and execute on the device — reference ``Engine.run`` (``engine.py:56-77``)
         minus the SQL text frontend: ``ra`` is an analyzed tree (``ra.query`` builds one).  The
@@ -73,3 +83,24 @@ class Engine:
             if not keep_temps:
                 self.catalog.temps.sweep()
         return OptimizeResult(p, elapsed, optimizer.esc_overhead_ms(p))
+
+
+def parse_schema_spec(spec: str) -> list:
+    """``"o_orderkey:int64,o_totalprice:decimal(15,2)"`` -> [(name, ColumnKind)]; commas inside
+    ``decimal(p,s)`` do not split (reference ``engine.py:80-99``)."""
+    from .storage import parse_kind
+
+    items, pending = [], []
+    for part in spec.split(","):
+        pending.append(part)
+        chunk = ",".join(pending)
+        if chunk.count("(") != chunk.count(")"):
+            continue
+        name, sep, kind = chunk.partition(":")
+        if not sep or not name.strip():
+            raise ValueError(f"bad schema item {chunk!r} (expected name:kind)")
+        items.append((name.strip(), parse_kind(kind)))
+        pending = []
+    if pending:
+        raise ValueError(f"bad schema item {','.join(pending)!r} (unbalanced parentheses)")
+    return items

@@ -366,6 +366,25 @@ def histogram_known():
     return out
 
 
+def csv_known():
+    """Reference load_csv on tests/golden/csv_cases.py: column values / NULL masks / dictionary
+    words, or the exception type and message."""
+    sys.path.insert(0, HERE)
+    import csv_cases
+    from escdb.engine import parse_schema_spec as rspec
+    from escdb.storage import load_csv as rload
+
+    out = {}
+    for name, text, spec, header in csv_cases.CASES:
+        try:
+            t = rload(text, "t", rspec(spec), has_header=header)
+            out[name] = {"columns": [[c.name, np.asarray(c.values).tolist(), np.asarray(c.null_mask).tolist(),
+                                      c.dictionary.strings() if c.kind.is_text else None] for c in t.columns]}
+        except Exception as exc:  # noqa: BLE001 — the reference's own exception is the fixture
+            out[name] = {"error": type(exc).__name__, "message": str(exc)}
+    return out
+
+
 def star_execute_known():
     """The config-3 star query executed by the reference: plan with ESC, execute_plan COUNT."""
     from escdb.optimizer import execute_plan as rexec
@@ -407,6 +426,7 @@ def main():
         known["joins"] = join_known()
         known["histogram"] = histogram_known()
         known["shop"] = shop_known()
+        known["csv"] = csv_known()
         if "--skip-star" not in sys.argv:
             known["star_execute"] = star_execute_known()
         with open(path, "w") as fh:
@@ -431,7 +451,7 @@ def main():
     with open(os.path.join(HERE, "corpus.json"), "w") as fh:
         json.dump(corpus, fh, separators=(",", ":"))
     known = {"configs": config_known(), "shop": shop_known(), "star": star_known(), "joins": join_known(),
-             "histogram": histogram_known(),
+             "histogram": histogram_known(), "csv": csv_known(),
              "star_execute": star_execute_known(),
              "generator": "reference escdb 0.1.0 (pkg/src/escdb), numpy " + np.__version__}
     with open(os.path.join(HERE, "known.json"), "w") as fh:
