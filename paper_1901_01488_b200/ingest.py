@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes as C
 import csv
 import io
+import warnings
 
 import numpy as np
 import torch
@@ -162,8 +163,13 @@ def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=N
         raise N.NativeUnavailable(f"load_csv needs a CUDA device, got {dev}")
     stream = torch.cuda.current_stream(dev)
     sp = C.c_void_p(stream.cuda_stream)
-    host = torch.frombuffer(bytearray(data) or bytearray(1), dtype=torch.uint8)
-    d_bytes = host.pin_memory().to(dev, non_blocking=True) if n else torch.zeros(1, dtype=torch.uint8, device=dev)
+    if n:
+        with warnings.catch_warnings():  # read-only view of the caller's bytes; only copied from
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.frombuffer(data, dtype=torch.uint8)
+        d_bytes = host.pin_memory().to(dev, non_blocking=True)
+    else:
+        d_bytes = torch.zeros(1, dtype=torch.uint8, device=dev)
     ws_bytes = int(lib.esc_csv_workspace_bytes(n))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     totals = torch.zeros(3, dtype=torch.int64, device=dev)
