@@ -289,7 +289,6 @@ def run_ours(args, rank, world, local_rank):
         step()
     barrier()
     stream = torch.cuda.current_stream()
-    executor.KERNEL_EVENTS = []
     from paper_1901_01488_b200 import _native
 
     launches0 = _native.load_library().esc_launch_count()
@@ -302,11 +301,17 @@ def run_ours(args, rank, world, local_rank):
     e1.record(stream)
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    launches = _native.load_library().esc_launch_count() - launches0  # the library's own counter
+    # per-kernel breakdown (roofline): the same steps again with CUDA events around each launch —
+    # a separate loop, so the event records do not weigh on the timed steps above
+    executor.KERNEL_EVENTS = []
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     events = executor.KERNEL_EVENTS
     executor.KERNEL_EVENTS = None
     sel_ms = [a.elapsed_time(b) for a, b, k in events if k == "select"]
     mat_ms = [a.elapsed_time(b) for a, b, k in events if k == "materialize"]
-    launches = _native.load_library().esc_launch_count() - launches0  # the library's own counter
     kern_avg = statistics.mean(sel_ms)
     mat_avg = statistics.mean(mat_ms) if mat_ms else 0.0
     k_local = local

@@ -149,6 +149,11 @@ _SIGNATURES = {
     "esc_expand": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                              C.c_void_p]),
     "esc_join_count": (C.c_int, [C.POINTER(EscJoin), C.c_void_p, C.c_void_p]),
+    "esc_step_plan_create": (C.c_int, [C.POINTER(EscProgram), C.c_void_p, C.c_int32, C.c_int64,
+                                       C.POINTER(EscSelection), C.c_void_p, C.c_int32, C.POINTER(EscOutputs),
+                                       C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "esc_step_plan_launch": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "esc_step_plan_destroy": (C.c_int, [C.c_void_p]),
     "esc_csv_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "esc_csv_count": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "esc_csv_fields": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
@@ -191,14 +196,20 @@ def load_library(path: str = LIB_PATH):
         return lib
 
 
+# tuning generation: bumped by every setting change, so prepared launch plans are re-prepared
+TUNING = [0]
+
+
 def set_jit(mode: int, min_rows: int = -1):
     """0 = interpreter only, 1 = JIT scans of >= min_rows rows, 2 = always JIT."""
     check(load_library().esc_set_jit(int(mode), int(min_rows)), "esc_set_jit")
+    TUNING[0] += 1
 
 
 def set_stream_div(div: int) -> int:
     """Dense-tile rule of the selection compaction (tile streamed when hits >= rows/div; <= 0 off);
     returns the previous setting."""
+    TUNING[0] += 1
     return int(load_library().esc_set_stream_div(int(div)))
 
 

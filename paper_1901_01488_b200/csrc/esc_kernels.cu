@@ -530,13 +530,27 @@ size_t smem_bytes_for(const KParams& kp) {
          2 * sizeof(uint32_t) + sizeof(unsigned long long);  // s_writers_done[2], s_cta_count
 }
 
+// A resolved scan launch (kernel, geometry, cooperative flag): prepared once, issued any number
+// of times with the same KParams (esc_step_plan_* re-issues it without rebuilding anything).
+struct ScanLaunch {
+  const void* func = nullptr;  // JIT cudaKernel_t or the ahead-of-time interpreter instantiation
+  unsigned grid = 1;
+  unsigned block = 0;
+  size_t smem = 0;
+  bool coop = false;
+};
+
 template <int C, bool COMPACT>
-int launch_c(const KParams& kp, cudaStream_t stream) {
+int prepare_c(const KParams& kp, ScanLaunch* L) {
   const size_t smem = smem_bytes_for(kp);
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   int64_t grid = kp.n_tiles < sms ? kp.n_tiles : sms;
   if (grid < 1) grid = 1;
+  L->grid = (unsigned)grid;
+  L->block = Layout<COMPACT>::kThreads;
+  L->smem = smem;
+  L->coop = COMPACT;  // the one-pass look-back relies on every CTA being resident
   // JIT tier: large scans whose tiles run the fast (staged) evaluator
   const int mode = jit::g_mode.load();
   if (mode == 2 || (mode == 1 && kp.nrows >= jit::g_min_rows.load())) {
@@ -544,51 +558,57 @@ int launch_c(const KParams& kp, cudaStream_t stream) {
       std::string why;
       cudaKernel_t k = jit::get_kernel(kp, COMPACT, smem, &why);
       if (k != nullptr) {
-        void* args[] = {const_cast<KParams*>(&kp)};
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)grid);
-        cfg.blockDim = dim3(Layout<COMPACT>::kThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = COMPACT ? 1 : 0;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        ++g_launches;
-        cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), args);
-        if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("JIT kernel launch: ") + cudaGetErrorString(e));
+        L->func = reinterpret_cast<const void*>(k);
         return ESC_OK;
       }
     }
   }
   auto kern = esc_scan_kernel<C, COMPACT, InterpPred>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  if (COMPACT) {  // cooperative: all CTAs co-resident (the static-schedule look-back relies on it)
-    void* args[] = {const_cast<KParams*>(&kp)};
-    ++g_launches;
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid),
-                                    dim3(Layout<COMPACT>::kThreads), args, smem, stream);
-  } else {
-    ++g_launches;
-    kern<<<(unsigned)grid, Layout<COMPACT>::kThreads, smem, stream>>>(kp);
-    e = cudaGetLastError();
+  static std::atomic<size_t> configured{0};
+  if (smem > configured.load()) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    configured = smem;
   }
+  L->func = reinterpret_cast<const void*>(kern);
+  return ESC_OK;
+}
+
+int issue_scan(const ScanLaunch& L, const KParams& kp, cudaStream_t stream) {
+  void* args[] = {const_cast<KParams*>(&kp)};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(L.block);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = L.coop ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ++g_launches;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, L.func, args);
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return ESC_OK;
 }
 
 template <bool COMPACT>
-int launch(const KParams& kp, cudaStream_t stream) {
+int prepare(const KParams& kp, ScanLaunch* L) {
   switch (kp.chunks) {
     case 8:
-      if constexpr (!COMPACT) return launch_c<8, false>(kp, stream);
+      if constexpr (!COMPACT) return prepare_c<8, false>(kp, L);
       return fail(ESC_ERR_INVALID, "internal: C=8 tiles are for count/selection scans only");
-    case 4: return launch_c<4, COMPACT>(kp, stream);
-    case 2: return launch_c<2, COMPACT>(kp, stream);
-    default: return launch_c<1, COMPACT>(kp, stream);
+    case 4: return prepare_c<4, COMPACT>(kp, L);
+    case 2: return prepare_c<2, COMPACT>(kp, L);
+    default: return prepare_c<1, COMPACT>(kp, L);
   }
+}
+
+template <bool COMPACT>
+int launch(const KParams& kp, cudaStream_t stream) {
+  ScanLaunch L;
+  const int rc = prepare<COMPACT>(kp, &L);
+  return rc != ESC_OK ? rc : issue_scan(L, kp, stream);
 }
 
 // ---- streamed compaction of dense tiles ------------------------------------------------------
@@ -679,69 +699,24 @@ bool plan_stream(StreamParams& tp, const SelParams& sp, const esc_column_t* cols
   return tp.stages >= 2;
 }
 
-}  // namespace
+// ---- selection compaction: prepared once, issued any number of times ---------------------------
+struct MatLaunch {
+  SelParams sp;
+  StreamParams tp;
+  bool streaming = false;
+  bool empty = true;
+  unsigned segs = 0;
+  const uint32_t* seg_counts = nullptr;
+  unsigned long long* partials = nullptr;
+  unsigned long long* offsets = nullptr;
+  size_t stream_smem = 0;
+  unsigned stream_grid = 1;
+  unsigned compact_grid = 1;
+};
 
-// ==========================================================================================
-// C ABI
-// ==========================================================================================
-extern "C" {
-
-size_t esc_workspace_bytes(int64_t nrows) { return ws_layout(nrows).total; }
-
-int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_segments, int64_t* cap_entries) {
-  const WsLayout L = ws_layout(nrows);
-  if (bitmap_words) *bitmap_words = L.bitmap_words;
-  if (max_segments) *max_segments = L.max_tiles;
-  // capture slots: 4*C per segment of 128*C rows (C <= 4), i.e. n/32 plus the tail tile's slack
-  if (cap_entries) *cap_entries = (nrows < 0 ? 0 : nrows) / 32 + 4 * 4 * (int64_t)kConsumerWarps * 2;
-  return ESC_OK;
-}
-
-int esc_workspace_init(void* d_ws, size_t ws_bytes, void* stream) {
-  if (d_ws == nullptr || ws_bytes < sizeof(WsHeader)) return fail(ESC_ERR_WORKSPACE, "workspace too small");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(d_ws, 0, ws_bytes, st);
-  if (e == cudaSuccess)
-    e = cudaMemsetAsync(static_cast<uint8_t*>(d_ws) + offsetof(WsHeader, fail), 0xFF,
-                        sizeof(unsigned long long) * ESC_MAX_UDFS, st);
-  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("workspace init: ") + cudaGetErrorString(e));
-  std::lock_guard<std::mutex> g(g_epoch_mu);
-  g_epochs[d_ws] = 0;
-  return ESC_OK;
-}
-
-int esc_scan_count(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
-                   const int64_t* d_row_ids, esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream) {
-  static thread_local KParams kp;
-  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, nullptr);
-  if (rc != ESC_OK) return rc;
-  return launch<false>(kp, static_cast<cudaStream_t>(stream));
-}
-
-int esc_scan_select(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
-                    const int64_t* d_row_ids, esc_selection_t* sel, esc_result_t* result, void* d_ws,
-                    size_t ws_bytes, void* stream) {
-  static thread_local KParams kp;
-  if (sel == nullptr || sel->bitmap == nullptr || sel->seg_counts == nullptr)
-    return fail(ESC_ERR_INVALID, "null selection output");
-  if (sel->n_cap < 0 || sel->n_cap > ESC_MAX_PROJ) return fail(ESC_ERR_INVALID, "n_cap out of range");
-  for (int k = 0; k < sel->n_cap; ++k)
-    if (sel->cap_slot[k] < 0 || sel->cap_slot[k] >= ncols || sel->cap_values[k] == nullptr)
-      return fail(ESC_ERR_INVALID, "bad capture slot / buffer");
-  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, nullptr);
-  if (rc != ESC_OK) return rc;
-  sel->seg_rows = kChunkRows * kp.chunks;
-  sel->cap_per_seg = 4 * kp.chunks;  // segments with <= 4*C hits (~3% of 128*C rows) are captured
-  if (kp.chunks > 4) sel->cap_per_seg = 0;  // (no capture with C = 8 tiles)
-  kp.sel_on = 1;
-  kp.sel = *sel;
-  return launch<false>(kp, static_cast<cudaStream_t>(stream));
-}
-
-int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const esc_column_t* cols, int32_t ncols,
-                              const int64_t* d_row_ids, const esc_outputs_t* outs, void* d_ws, size_t ws_bytes,
-                              void* stream) {
-  static thread_local SelParams sp;
+int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* cols, int32_t ncols,
+                const int64_t* d_row_ids, const esc_outputs_t* outs, void* d_ws, size_t ws_bytes, MatLaunch* M) {
+  SelParams& sp = M->sp;
   if (sel == nullptr || sel->bitmap == nullptr || sel->seg_counts == nullptr || outs == nullptr)
     return fail(ESC_ERR_INVALID, "null selection argument");
   if (nrows < 0 || ncols < 0 || ncols > ESC_MAX_COLS) return fail(ESC_ERR_INVALID, "bad sizes");
@@ -785,14 +760,16 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
     if (sp.cap_index[k] < 0) sp.need_bitmap_captured = 1;
   }
   sp.outs = *outs;
-  if (sp.n_segs == 0) return ESC_OK;
+  M->empty = sp.n_segs == 0;
+  if (M->empty) return ESC_OK;
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
-  unsigned long long* offsets = reinterpret_cast<unsigned long long*>(ws + L.offsets);
-  unsigned long long* partials = reinterpret_cast<unsigned long long*>(ws + L.partials);
-  sp.seg_offsets = offsets;
+  M->offsets = reinterpret_cast<unsigned long long*>(ws + L.offsets);
+  M->partials = reinterpret_cast<unsigned long long*>(ws + L.partials);
+  M->seg_counts = sel->seg_counts;
+  sp.seg_offsets = M->offsets;
   // dense stream tiles (no row-id chaining: the staged tile must be the physical rows)
-  static thread_local StreamParams tp;
-  const bool streaming = plan_stream(tp, sp, cols, outs, sel, nrows, d_row_ids);
+  StreamParams& tp = M->tp;
+  M->streaming = plan_stream(tp, sp, cols, outs, sel, nrows, d_row_ids);
   sp.rule.dense_min = 0xFFFFFFFFu;
   sp.rule.segs_per_tile = 8;
   sp.rule.n_tiles = 0;
@@ -804,7 +781,9 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
     if (sel->d_count == nullptr) return fail(ESC_ERR_INVALID, "ESC_OUT_SKIP_OVER_CAPACITY needs sel->d_count");
     sp.rule.skip_count = reinterpret_cast<const unsigned long long*>(sel->d_count);
   }
-  if (streaming) {
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  if (M->streaming) {
     sp.rule.dense_min = stream_dense_min(tp.tile_rows);
     sp.rule.segs_per_tile = tp.segs_per_tile;
     sp.rule.n_tiles = (nrows + tp.tile_rows - 1) / tp.tile_rows;
@@ -812,39 +791,163 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
     tp.dense_list = sp.rule.dense_list;
     tp.n_dense = sp.rule.n_dense;
     tp.bitmap = sel->bitmap;
-    tp.seg_offsets = offsets;
+    tp.seg_offsets = M->offsets;
     tp.outs = *outs;
-  }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const unsigned segs = (unsigned)((sp.n_segs + kScanSeg - 1) / kScanSeg);
-  ++g_launches;
-  tile_scan_partials<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, sp.rule.n_dense,
-                                                     sp.rule.skip_count, sp.rule.skip_capacity);
-  ++g_launches;
-  tile_scan_apply<<<segs, kScanThreads, 0, st>>>(sel->seg_counts, sp.n_segs, partials, offsets, sp.rule);
-  const int sms = sm_count_cached();
-  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
-  if (streaming) {
-    const size_t smem = (size_t)tp.stages * tp.stage_bytes + 2 * kMaxStages * sizeof(uint64_t) +
-                        kMaxStages * sizeof(long long);
-    static thread_local int configured = 0;
-    if (configured < (int)smem) {
-      cudaError_t e = cudaFuncSetAttribute(sel_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    M->stream_smem = (size_t)tp.stages * tp.stage_bytes + 2 * kMaxStages * sizeof(uint64_t) +
+                     kMaxStages * sizeof(long long);
+    static std::atomic<size_t> configured{0};
+    if (M->stream_smem > configured.load()) {
+      cudaError_t e = cudaFuncSetAttribute(sel_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)M->stream_smem);
       if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-      configured = (int)smem;
+      configured = M->stream_smem;
     }
-    int64_t tiles = sp.rule.n_tiles;
-    const unsigned grid = (unsigned)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
-    ++g_launches;
-    sel_stream_kernel<<<grid, (1 + kStreamConsumers) * 32, smem, st>>>(tp);
+    const int64_t tiles = sp.rule.n_tiles;
+    M->stream_grid = (unsigned)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
   }
+  M->segs = (unsigned)((sp.n_segs + kScanSeg - 1) / kScanSeg);
   const int64_t want = (sp.n_segs + 32 * kSelWarps - 1) / (32 * kSelWarps);  // 32 segments per warp
-  const int64_t grid = want < (int64_t)sms * 16 ? want : (int64_t)sms * 16;
+  M->compact_grid = (unsigned)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
+  return ESC_OK;
+}
+
+int issue_mat(const MatLaunch& M, cudaStream_t st) {
+  if (M.empty) return ESC_OK;
+  const SelParams& sp = M.sp;
   ++g_launches;
-  sel_compact_kernel<<<(unsigned)grid, kSelWarps * 32, 0, st>>>(sp);
+  tile_scan_partials<<<M.segs, kScanThreads, 0, st>>>(M.seg_counts, sp.n_segs, M.partials, sp.rule.n_dense,
+                                                       sp.rule.skip_count, sp.rule.skip_capacity);
+  ++g_launches;
+  tile_scan_apply<<<M.segs, kScanThreads, 0, st>>>(M.seg_counts, sp.n_segs, M.partials, M.offsets, sp.rule);
+  if (M.streaming) {
+    ++g_launches;
+    sel_stream_kernel<<<M.stream_grid, (1 + kStreamConsumers) * 32, M.stream_smem, st>>>(M.tp);
+  }
+  ++g_launches;
+  sel_compact_kernel<<<M.compact_grid, kSelWarps * 32, 0, st>>>(sp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("selection compaction launch: ") + cudaGetErrorString(e));
   return ESC_OK;
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+extern "C" {
+
+size_t esc_workspace_bytes(int64_t nrows) { return ws_layout(nrows).total; }
+
+int esc_selection_sizes(int64_t nrows, int64_t* bitmap_words, int64_t* max_segments, int64_t* cap_entries) {
+  const WsLayout L = ws_layout(nrows);
+  if (bitmap_words) *bitmap_words = L.bitmap_words;
+  if (max_segments) *max_segments = L.max_tiles;
+  // capture slots: 4*C per segment of 128*C rows (C <= 4), i.e. n/32 plus the tail tile's slack
+  if (cap_entries) *cap_entries = (nrows < 0 ? 0 : nrows) / 32 + 4 * 4 * (int64_t)kConsumerWarps * 2;
+  return ESC_OK;
+}
+
+int esc_workspace_init(void* d_ws, size_t ws_bytes, void* stream) {
+  if (d_ws == nullptr || ws_bytes < sizeof(WsHeader)) return fail(ESC_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_ws, 0, ws_bytes, st);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(static_cast<uint8_t*>(d_ws) + offsetof(WsHeader, fail), 0xFF,
+                        sizeof(unsigned long long) * ESC_MAX_UDFS, st);
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("workspace init: ") + cudaGetErrorString(e));
+  std::lock_guard<std::mutex> g(g_epoch_mu);
+  g_epochs[d_ws] = 0;
+  return ESC_OK;
+}
+
+int esc_scan_count(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
+                   const int64_t* d_row_ids, esc_result_t* result, void* d_ws, size_t ws_bytes, void* stream) {
+  static thread_local KParams kp;
+  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, nullptr);
+  if (rc != ESC_OK) return rc;
+  return launch<false>(kp, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+namespace {
+int prepare_select(KParams& kp, const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
+                   const int64_t* d_row_ids, esc_selection_t* sel, esc_result_t* result, void* d_ws,
+                   size_t ws_bytes) {
+  if (sel == nullptr || sel->bitmap == nullptr || sel->seg_counts == nullptr)
+    return fail(ESC_ERR_INVALID, "null selection output");
+  if (sel->n_cap < 0 || sel->n_cap > ESC_MAX_PROJ) return fail(ESC_ERR_INVALID, "n_cap out of range");
+  for (int k = 0; k < sel->n_cap; ++k)
+    if (sel->cap_slot[k] < 0 || sel->cap_slot[k] >= ncols || sel->cap_values[k] == nullptr)
+      return fail(ESC_ERR_INVALID, "bad capture slot / buffer");
+  int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, nullptr);
+  if (rc != ESC_OK) return rc;
+  sel->seg_rows = kChunkRows * kp.chunks;
+  sel->cap_per_seg = 4 * kp.chunks;  // segments with <= 4*C hits (~3% of 128*C rows) are captured
+  if (kp.chunks > 4) sel->cap_per_seg = 0;  // (no capture with C = 8 tiles)
+  kp.sel_on = 1;
+  kp.sel = *sel;
+  return ESC_OK;
+}
+
+// A queued ESC step (esc_step_plan_*): the scan and the compaction fully prepared.
+struct StepPlanImpl {
+  KParams kp;
+  ScanLaunch scan;
+  MatLaunch mat;
+};
+}  // namespace
+
+extern "C" {
+
+int esc_scan_select(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
+                    const int64_t* d_row_ids, esc_selection_t* sel, esc_result_t* result, void* d_ws,
+                    size_t ws_bytes, void* stream) {
+  static thread_local KParams kp;
+  int rc = prepare_select(kp, prog, cols, ncols, nrows, d_row_ids, sel, result, d_ws, ws_bytes);
+  return rc != ESC_OK ? rc : launch<false>(kp, static_cast<cudaStream_t>(stream));
+}
+
+int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
+                         esc_selection_t* sel, const esc_column_t* mat_cols, int32_t mat_ncols,
+                         const esc_outputs_t* outs, esc_result_t* result, void* d_ws, size_t ws_bytes,
+                         void** out_plan) {
+  if (out_plan == nullptr) return fail(ESC_ERR_INVALID, "null plan output");
+  *out_plan = nullptr;
+  StepPlanImpl* plan = new (std::nothrow) StepPlanImpl();
+  if (plan == nullptr) return fail(ESC_ERR_INVALID, "out of host memory");
+  int rc = prepare_select(plan->kp, prog, cols, ncols, nrows, nullptr, sel, result, d_ws, ws_bytes);
+  if (rc == ESC_OK) rc = prepare<false>(plan->kp, &plan->scan);
+  if (rc == ESC_OK) rc = prepare_mat(sel, nrows, mat_cols, mat_ncols, nullptr, outs, d_ws, ws_bytes, &plan->mat);
+  if (rc != ESC_OK) {
+    delete plan;
+    return rc;
+  }
+  *out_plan = plan;
+  return ESC_OK;
+}
+
+int esc_step_plan_launch(void* plan, int32_t parts, void* stream) {
+  if (plan == nullptr) return fail(ESC_ERR_INVALID, "null plan");
+  if (parts < 1 || parts > 3) return fail(ESC_ERR_INVALID, "parts must be 1 (scan), 2 (compaction) or 3");
+  const StepPlanImpl* p = static_cast<const StepPlanImpl*>(plan);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = (parts & 1) ? issue_scan(p->scan, p->kp, st) : ESC_OK;
+  return (rc != ESC_OK || !(parts & 2)) ? rc : issue_mat(p->mat, st);
+}
+
+int esc_step_plan_destroy(void* plan) {
+  delete static_cast<StepPlanImpl*>(plan);
+  return ESC_OK;
+}
+
+int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const esc_column_t* cols, int32_t ncols,
+                              const int64_t* d_row_ids, const esc_outputs_t* outs, void* d_ws, size_t ws_bytes,
+                              void* stream) {
+  static thread_local MatLaunch M;
+  const int rc = prepare_mat(sel, nrows, cols, ncols, d_row_ids, outs, d_ws, ws_bytes, &M);
+  return rc != ESC_OK ? rc : issue_mat(M, static_cast<cudaStream_t>(stream));
 }
 
 int esc_compact(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,

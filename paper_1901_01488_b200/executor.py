@@ -543,16 +543,42 @@ def launch_step(table: ColumnTable, pred: ex.Expr, needed, capacity: int, materi
             return PendingStep(table, None, proj, cap, "done", result=(sel.count, None))
         return PendingStep(table, None, proj, cap, "done", result=(sel.count, materialize_selection(sel, needed)))
     plan = _step_plan(cp, table, proj, cap, ws)
-    ev0 = _ev_start(stream)
-    N.check(lib.esc_scan_select(C.byref(cp.program), cp.column_array(), cp.ncols, n, None, C.byref(plan.sel.desc),
-                                res, C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp), "esc_scan_select")
-    _ev_end(stream, ev0, "select")
-    ev0 = _ev_start(stream)
-    N.check(lib.esc_materialize_selection(C.byref(plan.sel.desc), n, plan.mat_cols, plan.mat_ncols, None,
-                                          C.byref(plan.outs), C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
-            "esc_materialize_selection")
-    _ev_end(stream, ev0, "materialize")
+    ckey = (slot, ws_ptr, N.TUNING[0])
+    handle = plan.c_plans.get(ckey) if plan.c_plans is not None else None
+    if handle is None:  # prepare the scan + compaction launches once (lowering, geometry, JIT lookup)
+        h = C.c_void_p()
+        N.check(lib.esc_step_plan_create(C.byref(cp.program), cp.column_array(), cp.ncols, n, C.byref(plan.sel.desc),
+                                         plan.mat_cols, plan.mat_ncols, C.byref(plan.outs), res, C.c_void_p(ws_ptr),
+                                         C.c_size_t(ws_bytes), C.byref(h)), "esc_step_plan_create")
+        handle = _CPlan(h.value, lib)
+        if plan.c_plans is None:
+            plan.c_plans = {}
+        plan.c_plans[ckey] = handle
+    if KERNEL_EVENTS is None:
+        N.check(lib.esc_step_plan_launch(C.c_void_p(handle.ptr), 3, sp), "esc_step_plan_launch")
+    else:  # profiling: events between the scan and the compaction
+        for part, kind in ((1, "select"), (2, "materialize")):
+            ev0 = _ev_start(stream)
+            N.check(lib.esc_step_plan_launch(C.c_void_p(handle.ptr), part, sp), "esc_step_plan_launch")
+            _ev_end(stream, ev0, kind)
     return PendingStep(table, cp, proj, cap, "queued", slot, plan)
+
+
+class _CPlan:
+    """Owner of an esc_step_plan handle (destroyed with the Python plan that holds it)."""
+
+    __slots__ = ("ptr", "lib")
+
+    def __init__(self, ptr, lib):
+        self.ptr, self.lib = ptr, lib
+
+    def __del__(self):
+        if self.ptr:
+            try:
+                self.lib.esc_step_plan_destroy(self.ptr)
+            except Exception:  # noqa: BLE001 — interpreter shutdown: the process frees it
+                pass
+            self.ptr = None
 
 
 def finish_step(ps: PendingStep):
@@ -603,6 +629,7 @@ class _StepPlan:
     mat_cols: object
     mat_ncols: int
     nbytes: int = 0
+    c_plans: dict | None = None   # (result slot, workspace) -> prepared esc_step_plan
 
 
 def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: int, ws) -> _StepPlan:
