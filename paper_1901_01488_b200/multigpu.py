@@ -13,6 +13,7 @@ table data crosses NVLink; the sharded temp stays where it was produced.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 from fractions import Fraction
 
@@ -117,6 +118,53 @@ def _global_replay(st: ShardedTable, cp, local_fails: list, group):
     executor.raise_udf_errors(st.local, cp, fails, None, st.global_rows, count_fn=_GlobalCount())
 
 
+def _queued_sharded(st: ShardedTable, cp, needed, gcap: int, group):
+    """Device-resident sharded ESC step, one host wait: K1 select writes the local count to the
+    device; an NCCL all_gather of that word (stream-ordered, no host round trip) gives every rank
+    the per-rank counts; a device flag = (global count <= global capacity) gates the compaction
+    queued behind it.  Returns (local count, fails, per-rank counts, columns or None)."""
+    import ctypes as C
+
+    from . import _native as N
+
+    lib = N.load_library()
+    table = st.local
+    n = table.row_count
+    stream = executor._stream(table.device)
+    ws = N.workspace(table.device, stream)
+    ws_ptr, ws_bytes = ws.ensure(n, stream.cuda_stream)
+    proj = [table.column(c) for c in needed]
+    cap = min(gcap, n)
+    plan = executor._step_plan(cp, table, proj, cap, ws)
+    sp = C.c_void_p(stream.cuda_stream)
+    res = C.c_void_p(ws.result_ptr(1))
+    N.check(lib.esc_scan_select(C.byref(cp.program), cp.column_array(), cp.ncols, n, None, C.byref(plan.sel.desc),
+                                res, C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp), "esc_scan_select")
+    every = torch.empty(dist.get_world_size(group), dtype=torch.int64, device=table.device)
+    dist.all_gather_into_tensor(every, ws.dcount, group=group)
+    if not hasattr(ws, "dflag"):
+        ws.dflag = torch.zeros(1, dtype=torch.int64, device=table.device)
+    # compaction gate: 0 (run) when the GLOBAL count fits the global capacity, else "over"
+    ws.dflag.copy_(torch.where(every.sum(dim=0, keepdim=True) <= gcap, torch.zeros_like(ws.dflag),
+                               torch.full_like(ws.dflag, 1 << 62)))
+    gate = N.EscSelection.from_buffer_copy(plan.sel.desc)
+    gate.d_count = ws.dflag.data_ptr()
+    outs = N.EscOutputs.from_buffer_copy(plan.outs)
+    outs.capacity = cap
+    N.check(lib.esc_materialize_selection(C.byref(gate), n, plan.mat_cols, plan.mat_ncols, None, C.byref(outs),
+                                          C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp), "esc_materialize_selection")
+    stream.synchronize()
+    local, fails = ws.read_result(cp.n_udfs, 1)
+    counts = [int(x) for x in every.cpu().tolist()]
+    cols = None
+    if sum(counts) <= gcap:
+        ps = executor.PendingStep(table, cp, proj, cap, "queued", 1, plan)
+        cols = executor._take_outputs(ps, ws, local)
+    else:
+        executor._plan_checkin(ws, plan)
+    return local, fails, counts, cols
+
+
 def sharded_esc_subquery(st: ShardedTable, predicate, needed, config: EscConfig, group=None) -> ShardedDecision:
     """The fused ESC step on every rank's shard + one count exchange."""
     if predicate is None or _trivially_true(predicate):
@@ -125,6 +173,20 @@ def sharded_esc_subquery(st: ShardedTable, predicate, needed, config: EscConfig,
     fused = config.materialize and rc > 0 and rc >= config.min_table_size
     cp = compile_predicate(st.local, predicate)
     n = st.local.row_count
+    gcap = math.floor(Fraction(config.max_selectivity) * rc)
+    proj_bytes = sum(st.local.column(c).values.element_size() + 1 for c in needed) if fused else 0
+    if (fused and dist.get_backend(group) == "nccl" and st.local.device.type == "cuda" and n > 0
+            and min(gcap, n) * max(proj_bytes, 1) <= executor.SPECULATE_BYTES):
+        try:
+            local, fails, counts, cols = _queued_sharded(st, cp, list(needed), gcap, group)
+            if cp.unbound or cp.may_fail:
+                _global_replay(st, cp, fails, group)
+        except EscdbError as exc:
+            raise ExecutionError(f"count sub-query on {st.name!r} failed: {exc}") from exc
+        total = sum(counts)
+        qualified = decide_pushdown(rc, total, config)
+        return ShardedDecision(st.name, total, rc, Fraction(total, rc) if rc else Fraction(0), qualified, local,
+                               exclusive_offsets(counts)[st.rank], counts, cols if qualified else None)
     try:
         if fused:
             local, fails, sel = executor.launch_select(cp, st.local, None, n, capture=needed)
