@@ -91,3 +91,47 @@ def test_jit_sources_compile_with_nvrtc(native_lib):
     if rc == 4 and b"unavailable" in native_lib.esc_last_error().lower():
         pytest.skip("NVRTC not installed")
     assert rc == 0, native_lib.esc_last_error().decode(errors="replace")[:4000]
+
+
+def test_join_csv_plan_entry_points_validate_arguments(native_lib):
+    """The hash-join, CSV, batched-copy and step-plan entry points reject malformed arguments with
+    a status and a message before touching a device (no GPU needed)."""
+    from paper_1901_01488_b200 import _native as N
+
+    def err(rc, text):
+        assert rc != 0, text
+        assert text.encode() in native_lib.esc_last_error(), native_lib.esc_last_error()
+
+    slots = (C.c_int64 * 8)()
+    err(native_lib.esc_hash_insert(None, 0, slots, 6, None), "power of two")
+    err(native_lib.esc_hash_insert(None, 8, slots, 8, None), "exceed")
+    err(native_lib.esc_hash_probe(slots, 8, None, None, N.DTYPE_CODES["F32"] if hasattr(N, "DTYPE_CODES") else 4,
+                                  None, None, None, 3, None, None), "null probe buffers")
+    err(native_lib.esc_expand(None, None, 5, None, None, None, None, None), "null expansion buffers")
+    j = N.EscJoin()
+    j.n_steps, j.n_stages, j.nrows = 1, 1, 10
+    j.stage_of[0] = 2
+    out = (C.c_uint64 * 2)()
+    err(native_lib.esc_join_count(C.byref(j), out, None), "stage_of")
+    j.stage_of[0] = 1
+    j.steps[0].key_data = 1
+    j.steps[0].key_dtype = 4  # float32 keys
+    err(native_lib.esc_join_count(C.byref(j), out, None), "integer")
+    j.steps[0].key_dtype = 2
+    j.steps[0].mode = N.JOIN_DENSE
+    j.star = 0
+    err(native_lib.esc_join_count(C.byref(j), out, None), "star")
+    tot = (C.c_uint64 * 3)()
+    err(native_lib.esc_csv_count(None, 10, tot, None, 0, None), "bad CSV arguments")
+    ws = (C.c_uint8 * 16)()
+    err(native_lib.esc_csv_count(b"a,b\n", 4, tot, ws, 16, None), "workspace too small")
+    err(native_lib.esc_csv_parse(None, None, None, 0, 5, 2, 3, 0, 0, None, None, None, None, None), "bad CSV parse")
+    err(native_lib.esc_csv_parse(None, None, None, 0, 5, 2, 1, 1, 19, None, None, None, None, None), "bad CSV parse")
+    err(native_lib.esc_copy_regions(N.MAX_REGIONS + 1 if hasattr(N, "MAX_REGIONS") else 73, None, None, None, None),
+        "region count")
+    err(native_lib.esc_step_plan_launch(None, 3, None), "null plan")
+    h = C.c_void_p()
+    err(native_lib.esc_step_plan_create(None, None, 0, 10, None, None, 0, None, None, None, 0, C.byref(h)),
+        "null selection output")
+    assert h.value is None
+    assert native_lib.esc_csv_workspace_bytes(1 << 30) > native_lib.esc_csv_workspace_bytes(1 << 10)
