@@ -444,6 +444,13 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
   } else {
     g.stages = (int)(kSmemBudget / off);
     if (g.stages > kMaxStages) g.stages = kMaxStages;
+    // ~96 KB of TMA in flight per SM (at least 3 stages) streams best: a 1-column int32 scan
+    // (32 KB stages) runs at 5.9 TB/s with 3 stages and 5.4 TB/s with 6 (tools/stage_sweep.py)
+    {
+      const int want = (int)((96u * 1024u + off - 1) / off);
+      const int cap = want < 3 ? 3 : want;
+      if (outs == nullptr && g.stages > cap) g.stages = cap;
+    }
     if (const char* e = getenv("ESC_STAGES")) {  // tuning override (experiments only)
       const int v = atoi(e);
       if (v >= 1 && v < g.stages) g.stages = v;
