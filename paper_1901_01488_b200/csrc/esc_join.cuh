@@ -339,6 +339,124 @@ __global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_bits_kerne
   }
 }
 
+// Dense-factor star (any integer key widths, NULL keys, factors of any width): a thread owns 4
+// consecutive rows; every step's 4 keys are loaded up front (16/32-byte vector loads for
+// int32/int64 keys) and the per-row stage products stay in registers.  (Its hash branch is kept
+// for completeness; stars with hash steps run join_count_kernel, which measured faster.)
+__device__ __forceinline__ void quad_keys(const JoinStepK& s, int64_t row0, int64_t nrows, bool full,
+                                          long long (&k)[4], uint32_t& valid) {
+  if (full && s.dtype == ESC_I32) {
+    const int4 v = __ldg(reinterpret_cast<const int4*>(s.keys) + (row0 >> 2));
+    k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+  } else if (full && s.dtype == ESC_I64) {
+    const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(s.keys) + (row0 >> 1));
+    const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(s.keys) + (row0 >> 1) + 1);
+    k[0] = a.x; k[1] = a.y; k[2] = b.x; k[3] = b.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) k[j] = row0 + j < nrows ? ld_key(s.keys, s.dtype, row0 + j) : 0;
+  }
+  if (s.nulls != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (row0 + j < nrows && s.nulls[row0 + j]) valid &= ~(1u << j);
+  }
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kJoinThreads, 1) join_quad_kernel(const __grid_constant__ JoinParams p) {
+  extern __shared__ __align__(16) uint8_t jsm[];
+  for (int t = 0; t < NS; ++t) {
+    const JoinStepK& s = p.steps[t];
+    if (s.mode != ESC_JOIN_DENSE || s.smem_off == kNoSmem) continue;
+    const long long bytes = s.fbits == 1 ? ((s.dlen + 31) / 32) * 4 : s.dlen * (s.fbits / 8);
+    const long long words = (bytes + 15) / 16;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x)
+      reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(reinterpret_cast<const uint4*>(s.factor) + i);
+  }
+  __syncthreads();
+  unsigned long long acc[NS + 1];
+#pragma unroll
+  for (int i = 0; i <= NS; ++i) acc[i] = 0;
+  const int64_t nquads = (p.nrows + 3) / 4;
+  const int64_t full_q = p.nrows / 4;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nquads; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row0 = q * 4;
+    const bool full = q < full_q;
+    uint32_t sel = full ? 0xFu : (0xFu >> (4 - (p.nrows - row0)));
+    if (p.bitmap != nullptr) sel &= (__ldg(p.bitmap + (row0 >> 5)) >> (row0 & 31)) & 0xFu;
+    if (sel == 0) continue;
+    long long k[NS][4];
+    uint32_t valid[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      valid[t] = sel;
+      quad_keys(p.steps[t], row0, p.nrows, full, k[t], valid[t]);
+    }
+    acc[0] += __popc(sel);
+    unsigned long long run[4] = {1, 1, 1, 1};
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const JoinStepK& s = p.steps[t];
+      unsigned long long f[4] = {0, 0, 0, 0};
+      if (s.mode == ESC_JOIN_DENSE) {
+        const uint8_t* base = s.smem_off != kNoSmem ? jsm + s.smem_off : s.factor;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const long long i = k[t][j] - s.dmin;
+          if (((valid[t] >> j) & 1u) && run[j] != 0 && i >= 0 && i < s.dlen) f[j] = factor_at(base, s.fbits, i);
+        }
+      } else {
+        // interleaved probes: the 4 rows' slot loads are independent
+        unsigned long long pos[4];
+        long long slot[4];
+        bool open[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          open[j] = ((valid[t] >> j) & 1u) && run[j] != 0;
+          pos[j] = splitmix64((unsigned long long)k[t][j]) & s.mask;
+        }
+        bool any = open[0] || open[1] || open[2] || open[3];
+        while (any) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) slot[j] = open[j] ? __ldg(s.slots + pos[j]) : -1;
+          any = false;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (!open[j]) continue;
+            if (slot[j] < 0) { open[j] = false; continue; }
+            if (__ldg(s.uk + slot[j]) == k[t][j]) {
+              f[j] = __ldg(s.weight[t + 1] + slot[j]);
+              open[j] = false;
+              continue;
+            }
+            pos[j] = (pos[j] + 1) & s.mask;
+            any = true;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) run[j] *= f[j];
+      acc[t + 1] += run[0] + run[1] + run[2] + run[3];
+    }
+  }
+  __shared__ unsigned long long red[kJoinThreads / 32][ESC_MAX_STEPS + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int st = 0; st <= NS; ++st) {
+    unsigned long long v = acc[st];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+    if (lane == 0) red[warp][st] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x <= NS) {
+    unsigned long long v = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) v += red[w2][threadIdx.x];
+    if (v) atomicAdd(p.out + threadIdx.x, v);
+  }
+}
+
 }  // namespace esc
 
 // ==========================================================================================
@@ -499,10 +617,19 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
       nullptr, esc::join_bits_kernel<1>, esc::join_bits_kernel<2>, esc::join_bits_kernel<3>,
       esc::join_bits_kernel<4>, esc::join_bits_kernel<5>, esc::join_bits_kernel<6>, esc::join_bits_kernel<7>,
       esc::join_bits_kernel<8>};
+  static void (*const quad_kernels[ESC_MAX_STEPS + 1])(const esc::JoinParams) = {
+      nullptr, esc::join_quad_kernel<1>, esc::join_quad_kernel<2>, esc::join_quad_kernel<3>,
+      esc::join_quad_kernel<4>, esc::join_quad_kernel<5>, esc::join_quad_kernel<6>, esc::join_quad_kernel<7>,
+      esc::join_quad_kernel<8>};
   if (p.n_steps == 0) p.bits = 0;
-  auto kern = p.bits ? bits_kernels[p.n_steps] : esc::join_count_kernel;
-  static thread_local uint32_t configured[ESC_MAX_STEPS + 1] = {};
-  const int ci = p.bits ? p.n_steps : 0;
+  // semi-join bitmaps -> join_bits_kernel; any other star -> join_quad_kernel; snowflake
+  // (stage-dependent weights) -> join_count_kernel
+  bool quad = !p.bits && p.star && p.n_steps > 0;  // (hash steps: the one-row kernel measured faster)
+  for (int t = 0; t < p.n_steps; ++t)
+    if (p.steps[t].mode != ESC_JOIN_DENSE) quad = false;
+  auto kern = p.bits ? bits_kernels[p.n_steps] : quad ? quad_kernels[p.n_steps] : esc::join_count_kernel;
+  static thread_local uint32_t configured[2 * ESC_MAX_STEPS + 2] = {};
+  const int ci = p.bits ? p.n_steps : quad ? ESC_MAX_STEPS + 1 + p.n_steps : 0;
   if (smem > 48 * 1024 && smem > configured[ci]) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -512,7 +639,7 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, esc::kJoinThreads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  const int64_t units = p.bits ? (j->nrows + 3) / 4 / 32 + 1 : (j->nrows + 31) / 32;  // warps of work
+  const int64_t units = (p.bits || quad) ? (j->nrows + 3) / 4 / 32 + 1 : (j->nrows + 31) / 32;  // warps of work
   int64_t blocks = (units + esc::kJoinThreads / 32 - 1) / (esc::kJoinThreads / 32);
   if (blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;
   if (blocks < 1) blocks = 1;
