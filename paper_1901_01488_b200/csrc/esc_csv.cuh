@@ -4,7 +4,8 @@
 // file's bytes are copied to HBM once and tokenised, validated and converted there, so a table
 // never crosses PCIe again (the columns stay resident for every ESC sub-query).
 //
-//   pass 1  esc_csv_count   per 16 KB chunk and per 1 KB warp slice: quote parity and the
+//   pass 1  esc_csv_count   per 16 KB chunk and per 1 KB warp slice (16 bytes per lane, one
+//                           16-byte load each): quote parity and the
 //                           separators / record ends outside quotes for BOTH possible starting
 //                           quote states (composable summaries), then one block scans the chunk
 //                           summaries: every chunk's starting state, field and record offsets.
@@ -42,34 +43,98 @@ __device__ __forceinline__ CsvSum csv_combine(const CsvSum& a, const CsvSum& b) 
   return c;
 }
 
-// byte classes: 1 ',' ; 2 record end ('\n' not after '\r', or '\r' not before '\n' is also 2);
-// 3 "\r\n" record end (the '\r'; the '\n' after it is no separator)
-__device__ __forceinline__ int csv_class(const uint8_t* b, int64_t n, int64_t i) {
-  const uint8_t c = b[i];
-  if (c == ',') return 1;
-  if (c == '\r') return (i + 1 < n && b[i + 1] == '\n') ? 3 : 2;
-  if (c == '\n') return (i > 0 && b[i - 1] == '\r') ? 0 : 2;
-  return 0;
+// 16 consecutive bytes per lane (one 16-byte load; a warp covers 512 bytes per step): the lane
+// walks its bytes with the quote state it inherits from the lanes before it (XOR-scan of their
+// quote-count parities via one ballot).
+struct CsvLane {
+  uint8_t c[16];
+  uint8_t prev, next;  // the bytes just before / after the lane's 16 (0 outside the text)
+  int real;            // bytes of the text in c (< 16 only at its end)
+  int cnt;             // bytes this lane processes (<= real: stops at the slice end)
+};
+
+__device__ __forceinline__ void csv_load_lane(const uint8_t* b, int64_t n, int64_t i0, int64_t s1, CsvLane& L) {
+  L.real = i0 >= n ? 0 : (i0 + 16 <= n ? 16 : (int)(n - i0));
+  if (L.real == 16 && (reinterpret_cast<uintptr_t>(b + i0) & 15) == 0) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(b + i0));
+    memcpy(L.c, &v, 16);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) L.c[k] = k < L.real ? b[i0 + k] : 0;
+  }
+  L.prev = (i0 > 0 && i0 <= n) ? b[i0 - 1] : 0;
+  L.next = (i0 + 16 < n) ? b[i0 + 16] : 0;
+  L.cnt = i0 >= s1 ? 0 : (i0 + L.real > s1 ? (int)(s1 - i0) : L.real);
+}
+
+// SWAR classification of a lane's 16 bytes into 16-bit masks (bit k = byte k)
+__device__ __forceinline__ uint32_t eq_mask4(uint32_t w, uint32_t pat) {
+  const uint32_t e = __vcmpeq4(w, pat);  // 0xFF in every byte equal to the pattern byte
+  return ((e >> 7) & 1u) | ((e >> 14) & 2u) | ((e >> 21) & 4u) | ((e >> 28) & 8u);
+}
+
+struct CsvMasks {
+  uint32_t quote, sep, rec, cr3, valid;
+};
+
+__device__ __forceinline__ CsvMasks csv_masks(const CsvLane& L) {
+  uint32_t w[4];
+  memcpy(w, L.c, 16);
+  uint32_t q = 0, comma = 0, cr = 0, lf = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    q |= eq_mask4(w[i], 0x22222222u) << (4 * i);
+    comma |= eq_mask4(w[i], 0x2C2C2C2Cu) << (4 * i);
+    cr |= eq_mask4(w[i], 0x0D0D0D0Du) << (4 * i);
+    lf |= eq_mask4(w[i], 0x0A0A0A0Au) << (4 * i);
+  }
+  const uint32_t real = L.real >= 16 ? 0xFFFFu : ((1u << L.real) - 1u);
+  q &= real; comma &= real; cr &= real; lf &= real;
+  CsvMasks m;
+  m.valid = L.cnt >= 16 ? 0xFFFFu : ((1u << L.cnt) - 1u);
+  const uint32_t cr_before = (cr << 1) | (L.prev == '\r' ? 1u : 0u);   // byte k-1 is '\r'
+  const uint32_t lf_after = (lf >> 1) | (L.next == '\n' ? 0x8000u : 0u);  // byte k+1 is '\n'
+  m.quote = q & m.valid;
+  m.rec = ((lf & ~cr_before) | cr) & m.valid;  // '\n' not after '\r', every '\r'
+  m.cr3 = cr & lf_after & m.valid;             // "\r\n": the '\r' ends the record
+  m.sep = (comma & m.valid) | m.rec;
+  return m;
+}
+
+// bit k = parity of the quotes strictly before byte k (quote state relative to the lane start)
+__device__ __forceinline__ uint32_t quote_state(uint32_t q) {
+  uint32_t x = q;
+  x ^= x << 1;
+  x ^= x << 2;
+  x ^= x << 4;
+  x ^= x << 8;
+  return (x << 1) & 0xFFFFu;
 }
 
 __device__ CsvSum csv_slice_sum(const uint8_t* b, int64_t n, int64_t s0, int64_t s1, int lane) {
   CsvSum acc = {0, 0, 0, 0, 0};
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t base = s0; base < s1; base += 32) {
-    const int64_t i = base + lane;
-    const bool in = i < s1;
-    const uint8_t c = in ? b[i] : 0;
-    const unsigned qm = __ballot_sync(0xFFFFFFFFu, c == '"');
-    const int cls = in ? csv_class(b, n, i) : 0;
-    const unsigned rel = (unsigned)((acc.flip ^ __popc(qm & lt)) & 1u);  // quote state relative to the slice start
-    const unsigned sm = __ballot_sync(0xFFFFFFFFu, cls != 0);
-    const unsigned rm = __ballot_sync(0xFFFFFFFFu, cls >= 2);
-    const unsigned relm = __ballot_sync(0xFFFFFFFFu, rel != 0);  // lanes inside (if started outside)
-    acc.f_e += __popc(sm & ~relm);
-    acc.f_o += __popc(sm & relm);
-    acc.r_e += __popc(rm & ~relm);
-    acc.r_o += __popc(rm & relm);
-    acc.flip ^= __popc(qm) & 1u;
+  for (int64_t base = s0; base < s1; base += 512) {
+    CsvLane L;
+    const int64_t i0 = base + 16 * lane;
+    csv_load_lane(b, n, i0, s1, L);
+    const CsvMasks m = csv_masks(L);
+    const unsigned odd = __ballot_sync(0xFFFFFFFFu, __popc(m.quote) & 1);
+    const uint32_t inside = quote_state(m.quote) ^ (((acc.flip ^ __popc(odd & lt)) & 1u) ? 0xFFFFu : 0u);
+    unsigned fe = __popc(m.sep & ~inside), fo = __popc(m.sep & inside);
+    unsigned re = __popc(m.rec & ~inside), ro = __popc(m.rec & inside);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      fe += __shfl_xor_sync(0xFFFFFFFFu, fe, d);
+      fo += __shfl_xor_sync(0xFFFFFFFFu, fo, d);
+      re += __shfl_xor_sync(0xFFFFFFFFu, re, d);
+      ro += __shfl_xor_sync(0xFFFFFFFFu, ro, d);
+    }
+    acc.f_e += fe;  // counts relative to the slice start state (the combine step's form)
+    acc.f_o += fo;
+    acc.r_e += re;
+    acc.r_o += ro;
+    acc.flip ^= __popc(odd) & 1u;
   }
   return acc;
 }
@@ -155,26 +220,36 @@ __global__ void __launch_bounds__(kCsvWarps * 32) csv_fields_kernel(const uint8_
   const int64_t s0 = (int64_t)blockIdx.x * kCsvChunk + (int64_t)warp * kCsvSlice;
   const int64_t s1 = s0 + kCsvSlice < n ? s0 + kCsvSlice : n;
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t base = s0; base < s1; base += 32) {
-    const int64_t i = base + lane;
-    const bool in = i < s1;
-    const uint8_t c = in ? b[i] : 0;
-    const unsigned qm = __ballot_sync(0xFFFFFFFFu, c == '"');
-    const int cls = in ? csv_class(b, n, i) : 0;
-    const bool quoted = (in_q ^ __popc(qm & lt)) & 1u;
-    const bool sep = cls != 0 && !quoted;
-    const bool rec = cls >= 2 && !quoted;
-    const unsigned sm = __ballot_sync(0xFFFFFFFFu, sep);
-    const unsigned rm = __ballot_sync(0xFFFFFFFFu, rec);
-    if (sep) {
-      const unsigned long long f = fidx + __popc(sm & lt);
-      field_end[f] = i;
-      field_kind[f] = (uint8_t)cls;
-      if (rec) rec_end_field[ridx + __popc(rm & lt)] = (long long)f;
+  for (int64_t base = s0; base < s1; base += 512) {
+    CsvLane L;
+    const int64_t i0 = base + 16 * lane;
+    csv_load_lane(b, n, i0, s1, L);
+    const CsvMasks m = csv_masks(L);
+    const unsigned odd = __ballot_sync(0xFFFFFFFFu, __popc(m.quote) & 1);
+    const uint32_t inside = quote_state(m.quote) ^ (((in_q ^ __popc(odd & lt)) & 1u) ? 0xFFFFu : 0u);
+    const uint32_t out_sep = m.sep & ~inside, out_rec = m.rec & ~inside;
+    const unsigned ns = __popc(out_sep), nr = __popc(out_rec);
+    // exclusive offsets of the lane's separators within the warp's 512 bytes
+    unsigned es = ns, er = nr;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned ts = __shfl_up_sync(0xFFFFFFFFu, es, d);
+      const unsigned tr = __shfl_up_sync(0xFFFFFFFFu, er, d);
+      if (lane >= d) { es += ts; er += tr; }
     }
-    fidx += __popc(sm);
-    ridx += __popc(rm);
-    in_q ^= __popc(qm) & 1u;
+    const unsigned tot_s = __shfl_sync(0xFFFFFFFFu, es, 31), tot_r = __shfl_sync(0xFFFFFFFFu, er, 31);
+    unsigned long long f = fidx + es - ns, r = ridx + er - nr;
+    for (uint32_t mm = out_sep; mm; mm &= mm - 1) {
+      const int k = __ffs(mm) - 1;
+      const uint32_t bit = 1u << k;
+      field_end[f] = i0 + k;
+      field_kind[f] = (uint8_t)((out_rec & bit) ? ((m.cr3 & bit) ? 3 : 2) : 1);
+      if (out_rec & bit) rec_end_field[r++] = (long long)f;
+      ++f;
+    }
+    fidx += tot_s;
+    ridx += tot_r;
+    in_q ^= __popc(odd) & 1u;
   }
 }
 

@@ -48,6 +48,20 @@ def main():
         for m, title in METRICS:
             if m in hdr:
                 lines.append(f"| {title} (`{m}`) | {r[hdr.index(m)]} {units[hdr.index(m)]} |")
+        try:  # achieved DRAM bandwidth of this launch (read + write over its duration)
+            def _val(m, scale):
+                v = float(r[hdr.index(m)])
+                u = units[hdr.index(m)].lower()
+                return v * scale.get(u, 1.0)
+            nbytes = (_val("dram__bytes_read.sum", {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}) +
+                      _val("dram__bytes_write.sum", {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}))
+            secs = _val("gpu__time_duration.sum", {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6,
+                                                    "msecond": 1e-3, "ms": 1e-3, "second": 1.0})
+            gbs = nbytes / secs / 1e9
+            lines.append(f"| achieved DRAM GB/s (read+write / duration) | {gbs:.0f} GB/s = {gbs / 8000:.2f} of 8 TB/s "
+                         f"nominal, {gbs / 6538.3:.2f} of the measured 6538 GB/s copy peak (cold-cache replay) |")
+        except (ValueError, KeyError, ZeroDivisionError):
+            pass
         stalls = sorted(((float(r[i] or 0), h.replace("smsp__pcsamp_warps_issue_stalled_", ""))
                          for i, h in enumerate(hdr)
                          if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")),

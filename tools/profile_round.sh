@@ -1,16 +1,20 @@
 #!/bin/bash
 # Round profiling captures (run on the GPU box from the repo root); outputs in gpurun_out/prof/.
+# Every capture is one launch after warm-up: ncu --set full --clock-control none --import-source on.
 set -u
 mkdir -p gpurun_out/prof
 B="python bench.py --steps 2 --warmup 1 --no-extras --no-e2e --no-cpu-baseline"
+N="ncu --set full --clock-control none --import-source on"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv \
     --log-file gpurun_out/prof/launches_config4.csv $B > gpurun_out/prof/launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:esc_scan_kernel --launch-skip 1 --launch-count 1 \
-    -o gpurun_out/prof/k1_select_config4 $B > gpurun_out/prof/k1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sel_compact --launch-skip 1 --launch-count 1 \
-    -o gpurun_out/prof/selcompact_config4 $B > gpurun_out/prof/selc.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sel_stream --launch-skip 2 --launch-count 1 \
-    -o gpurun_out/prof/stream_config5_s0.5 python tools/kprof_stream.py 0.5 200000000 > gpurun_out/prof/stream.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:join_bits --launch-skip 3 --launch-count 1 \
-    -o gpurun_out/prof/join_bits_star python tools/diag_join.py > gpurun_out/prof/join.log 2>&1
+$N -k regex:esc_scan_kernel --launch-skip 1 --launch-count 1 -o gpurun_out/prof/k1_select_config4 $B > gpurun_out/prof/k1.log 2>&1
+$N -k regex:sel_compact --launch-skip 1 --launch-count 1 -o gpurun_out/prof/selcompact_config4 $B > gpurun_out/prof/selc.log 2>&1
+$N -k regex:esc_scan_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/prof/k1_count_config5_single \
+    python tools/kprof_count.py > gpurun_out/prof/k1c.log 2>&1
+$N -k regex:sel_stream --launch-skip 2 --launch-count 1 -o gpurun_out/prof/stream_config5_s0.5 \
+    python tools/kprof_stream.py 0.5 200000000 > gpurun_out/prof/stream.log 2>&1
+$N -k regex:join_bits --launch-skip 3 --launch-count 1 -o gpurun_out/prof/join_bits_star python tools/diag_join.py \
+    > gpurun_out/prof/join.log 2>&1
+$N -k regex:csv_ --launch-skip 8 --launch-count 4 -o gpurun_out/prof/csv_ingest python tools/diag_ingest.py \
+    > gpurun_out/prof/csv.log 2>&1
 ls -la gpurun_out/prof
