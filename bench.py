@@ -144,7 +144,7 @@ def _cpu_chunk(bounds):
     t = O.OTable("t", {k: O.OColumn(v[lo:hi], np.zeros(hi - lo, bool)) for k, v in st["cols"].items()})
     count = O.count_star(t, st["pred"], st["udfs"])
     mat = O.materialize(t, st["pred"], st["project"], st["udfs"])  # reference re-scans
-    return count, sum(c.values.nbytes for c in mat.values())
+    return count, [mat[c].values for c in st["project"]]
 
 
 def cpu_reference_run(cols: dict, pred, project, udfs, rows: int, procs: int, reps: int = 1):
@@ -162,7 +162,18 @@ def cpu_reference_run(cols: dict, pred, project, udfs, rows: int, procs: int, re
             res = pool.map(_cpu_chunk, bounds)
             times.append(time.perf_counter() - t0)
             count = sum(r[0] for r in res)
+    # the materialised columns of the sample, chunks concatenated in row order (parity digest)
+    cpu_reference_run.last_columns = [np.concatenate([r[1][k] for r in res]) for k in range(len(project))]
     return times, count
+
+
+def columns_digest(arrays) -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
 
 
 def default_cpu_rows(procs: int) -> int:
@@ -231,16 +242,17 @@ def run_ours(args, rank, world, local_rank):
     gen_s = time.perf_counter() - t0
 
     # CPU baseline BEFORE any CUDA context exists (the pool forks)
-    cpu_baseline = None
+    cpu_baseline, cpu_parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
         rows = min(m, args.cpu_sample_rows or default_cpu_rows(procs))
         cols = {k: v[1] for k, v in w.columns.items()}
-        times, _ = cpu_reference_run(cols, w.pred, w.project, w.udfs, rows, procs, reps=2)
+        times, cpu_count = cpu_reference_run(cols, w.pred, w.project, w.udfs, rows, procs, reps=2)
         per = min(times[1:]) if len(times) > 1 else times[0]
         cpu_baseline = {"value": rows / per, "unit": "rows/s", "cores": procs, "kind": "port",
                         "sample": f"first {rows} rows of this config-4 shard; numpy port of the reference "
                                   f"(count sub-query + materialization) in {procs} processes"}
+        cpu_parity = (rows, cpu_count, columns_digest(cpu_reference_run.last_columns))
 
     import torch.distributed as dist
 
@@ -264,6 +276,15 @@ def run_ours(args, rank, world, local_rank):
     cat = Catalog()
     cat.register(table)
     st = multigpu.ShardedTable("t", table, n, lo, rank, world)
+
+    parity = None
+    if cpu_parity is not None:  # the device path on the same sample: count and row-order digest
+        srows, scount, sdigest = cpu_parity
+        sample = ColumnTable("t", [Column(c.name, c.kind, c.values[:srows]) for c in table.columns])
+        dcount, dcols = executor.count_and_materialize(sample, pred, list(w.project), srows)
+        ddigest = columns_digest([c.values.cpu().numpy() for c in dcols])
+        parity = {"sample_rows": srows, "count_reference_port": scount, "count_device": dcount,
+                  "rows_digest_equal": ddigest == sdigest, "bit_exact": dcount == scount and ddigest == sdigest}
 
     def step():
         if world > 1:
@@ -396,6 +417,7 @@ def run_ours(args, rank, world, local_rank):
                      "note": "one predicate pass (count + selection bitmap) + one gather pass over the "
                              "selection (only the hit rows of the projected columns)"},
             "cpu_baseline": cpu_baseline,
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
