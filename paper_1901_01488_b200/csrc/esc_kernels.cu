@@ -652,7 +652,7 @@ bool plan_stream(StreamParams& tp, const SelParams& sp, const esc_column_t* cols
     per_row += w + (want_nulls ? 1 : 0);
   }
   tp.seg_rows = sel->seg_rows;
-  int spt = kConsumerWarps;
+  int spt = kConsumerWarps < 8 ? kConsumerWarps : 8;  // the dense-tile rule handles 2, 4 or 8 segments
   auto stage_for = [&](int s) {
     const uint32_t rows = (uint32_t)s * (uint32_t)tp.seg_rows;
     uint32_t b = rows / 8;                 // bitmap words
