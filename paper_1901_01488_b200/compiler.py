@@ -398,6 +398,7 @@ def _key(pred: ex.Expr):
 
 def compile_predicate(table, pred: ex.Expr) -> CompiledPredicate:
     """Compile (or fetch from the per-table cache) the device program of ``pred``."""
+    pred = ex.adopt(pred)  # trees from the reference analyzer drive the engine unchanged
     key = _key(pred)
     with _cache_lock:
         per_table = _cache.setdefault(table, {})

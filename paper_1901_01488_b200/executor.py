@@ -797,6 +797,9 @@ def take_column(col: Column, indices) -> Column:
 def execute_count(ra, catalog) -> int:
     """Single-table COUNT tree: Aggregate over optional Select over optional Project over a
     Scan / TempScan (reference ``executor.py:232-250``)."""
+    from .ra import adopt as adopt_ra
+
+    ra = adopt_ra(ra)
     node = ra.child if isinstance(ra, RaAggregate) else ra
     pred = None
     if isinstance(node, RaSelect):

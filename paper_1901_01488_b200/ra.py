@@ -156,3 +156,28 @@ def query(catalog, tables, where: ex.Expr | None = None, select=None):
         return RaAggregate(node, "count_star", (COUNT_COLUMN,))
     cols = node.schema if select == "*" else tuple(select)
     return RaProject(node, cols, cols)
+
+
+def adopt(node):
+    """This package's RA tree for one built by the reference analyzer (``frontend.py:511-557``:
+    same class names and fields); predicates and column refs are adopted too."""
+    if node is None:
+        return None
+    name = type(node).__name__
+    if isinstance(node, (RaScan, RaTempScan, RaSelect, RaProject, RaJoin, RaAggregate)):
+        return node
+    schema = tuple(ex.adopt_ref(c) for c in getattr(node, "schema", ()))
+    if name == "RaScan":
+        return RaScan(node.table, node.alias, schema)
+    if name == "RaTempScan":
+        return RaTempScan(node.handle, node.alias, schema)
+    if name == "RaSelect":
+        return RaSelect(adopt(node.child), ex.adopt(node.predicate), schema)
+    if name == "RaProject":
+        return RaProject(adopt(node.child), tuple(ex.adopt_ref(c) for c in node.columns), schema)
+    if name == "RaJoin":
+        return RaJoin(adopt(node.left), adopt(node.right),
+                      tuple((ex.adopt_ref(a), ex.adopt_ref(b)) for a, b in node.pairs), schema)
+    if name == "RaAggregate":
+        return RaAggregate(adopt(node.child), node.agg, schema)
+    raise TypeError(f"not an RA node: {node!r}")
