@@ -408,6 +408,11 @@ int esc_jit_stats(int64_t* out);
  * tile_rows / div hits.  div <= 0 turns streaming off; default 32 (env ESC_STREAM_DIV).
  * Returns the previous setting. */
 int esc_set_stream_div(int div);
+/* Diagnostics: when d_stamps (device, >= 8 x grid uint64) is non-null, every later scan launch
+ * writes per-CTA %globaltimer stamps (start, first tile, consumers done, producer done, CTA
+ * finished; last CTA: finalisation begin / end) into it.
+ * nullptr turns it off (the default). */
+int esc_debug_trace(void* d_stamps);
 /* sizeof() of the ABI structs, for binding checks: 0 program, 1 instr, 2 udf, 3 udf_op,
  * 4 column, 5 result, 6 outputs, 7 selection, 8 join step, 9 join; -1 for an unknown id. */
 int esc_struct_size(int which);

@@ -142,6 +142,7 @@ _SIGNATURES = {
     "esc_jit_stats": (C.c_int, [C.POINTER(C.c_int64)]),
     "esc_jit_selftest": (C.c_int, []),
     "esc_set_stream_div": (C.c_int, [C.c_int]),
+    "esc_debug_trace": (C.c_int, [C.c_void_p]),
     "esc_copy_regions": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "esc_hash_insert": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
     "esc_hash_probe": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,

@@ -105,7 +105,14 @@ struct KParams {
   int32_t sel_on;             // K1 records the selection into `sel`
   esc_selection_t sel;
   uint32_t rows_off;     // stage offset of the u16 row-index scratch (row-id outputs)
+  unsigned long long* trace;  // diagnostics (esc_debug_trace): per-CTA %globaltimer stamps, or nullptr
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // ------------------------------------------------------------------------------------------
 // PTX helpers: mbarrier, bulk copy, release/acquire
@@ -800,6 +807,7 @@ __device__ __forceinline__ void finish_cta(const KParams& p, unsigned long long 
   __threadfence();
   const unsigned long long prev = atomicAdd(&p.hdr->done, 1ull);
   if (prev == gridDim.x - 1) {
+    if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 5] = gtimer();
     __threadfence();
     volatile WsHeader* h = p.hdr;
     p.result->count = h->count;
@@ -811,7 +819,9 @@ __device__ __forceinline__ void finish_cta(const KParams& p, unsigned long long 
     h->count = 0;
     h->ticket = 0;
     h->done = 0;
-    __threadfence_system();
+    // no system-scope fence: the host reads the result only after the kernel has completed (a
+    // stream/event wait), and kernel completion makes every write visible (the fence cost ~5 us)
+    if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 6] = gtimer();
   }
 }
 
@@ -842,6 +852,7 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
 
   if (threadIdx.x < kMaxStages) s_tsum[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
+    if (p.trace != nullptr) p.trace[blockIdx.x * 8] = gtimer();
     *s_writers_done = 0;
     *s_cta_count = 0;
     for (int s = 0; s < S; ++s) {
@@ -888,11 +899,41 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
             if (col.nulls_staged)
               bulk_g2s(dst + col.smem_null_off, col.nulls + row0, (uint32_t)p.tile_rows, &full_bar[s], policy);
           }
+        } else if (!COMPACT && p.tma_bytes != 0) {
+          // the partial tail tile is staged too (a cold per-row read of it was a ~20 us tail on
+          // the CTA that drew it): 16-byte multiples by TMA, the last < 16 bytes of each region
+          // by this lane (ordered before the arrive, whose release covers them)
+          uint8_t* dst = ring + (size_t)s * p.stage_bytes;
+          const int64_t row0 = tile * p.tile_rows;
+          const uint32_t rows = (uint32_t)(p.nrows - row0);
+          uint32_t tx = 0;
+          for (int i = 0; i < p.ncols; ++i) {
+            const KCol& col = p.cols[i];
+            if (col.staged) {
+              const uint32_t b = rows * (uint32_t)col.width, a = b & ~15u;
+              const uint8_t* src = col.data + (size_t)row0 * col.width;
+              for (uint32_t j = a; j < b; ++j) dst[col.smem_off + j] = src[j];
+              tx += a;
+            }
+            if (col.nulls_staged) {
+              const uint32_t a = rows & ~15u;
+              for (uint32_t j = a; j < rows; ++j) dst[col.smem_null_off + j] = col.nulls[row0 + j];
+              tx += a;
+            }
+          }
+          mbar_arrive_expect_tx(&full_bar[s], tx);
+          for (int i = 0; i < p.ncols; ++i) {
+            const KCol& col = p.cols[i];
+            const uint32_t a = (rows * (uint32_t)col.width) & ~15u, an = rows & ~15u;
+            if (col.staged && a) bulk_g2s(dst + col.smem_off, col.data + (size_t)row0 * col.width, a, &full_bar[s], policy);
+            if (col.nulls_staged && an) bulk_g2s(dst + col.smem_null_off, col.nulls + row0, an, &full_bar[s], policy);
+          }
         } else {
           mbar_arrive(&full_bar[s]);
         }
         tile += gridDim.x;
       }
+      if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 3] = gtimer();
     }
     return;
   }
@@ -995,17 +1036,21 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
   uint32_t ph = 0;
   for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
     mbar_wait(&full_bar[s], ph);
+    if (p.trace != nullptr && cw == 0 && lane == 0 && my_count == 0 && s == 0 && ph == 0)
+      p.trace[blockIdx.x * 8 + 1] = gtimer();
     const int64_t tile = tile_of[s];
     if (tile < 0) break;
     RowRef rr;
-    rr.stage = (tile < p.n_full_tiles) ? ring + (size_t)s * p.stage_bytes : nullptr;
+    const bool full = tile < p.n_full_tiles;
+    rr.stage = (full || (!COMPACT && p.tma_bytes != 0)) ? ring + (size_t)s * p.stage_bytes : nullptr;
     rr.local0 = local0;
     rr.grow0 = tile * p.tile_rows + local0;
     rr.nrows = p.nrows;
     rr.ids = p.row_ids;
     uint32_t bits;
     if (rr.stage != nullptr && p.all_staged) {
-      bits = Pred::template eval<C>(p, rr, (4 * C == 32) ? 0xFFFFFFFFu : ((1u << (4 * C)) - 1u));
+      bits = Pred::template eval<C>(p, rr, full ? ((4 * C == 32) ? 0xFFFFFFFFu : ((1u << (4 * C)) - 1u))
+                                                : valid_bits(rr.grow0, p.nrows, C));
     } else {
       bits = eval_direct<C>(p, rr, valid_bits(rr.grow0, p.nrows, C));
     }
@@ -1141,7 +1186,9 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
     if (cw == 0 && lane == 0) {
       unsigned long long tot = 0;
       for (int w = 0; w < kConsumerWarps; ++w) tot += s_red[w];
+      if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 2] = gtimer();
       finish_cta(p, tot);
+      if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 4] = gtimer();
     }
   }
 }
@@ -1291,6 +1338,7 @@ struct SelParams {
   int32_t cap_per_seg;
   int32_t n_proj;
   int32_t need_bitmap_captured;  // captured segments still need the bitmap (row ids / uncaptured columns)
+  int32_t sparse_in_a;           // phase A also writes sparse segments (grids that fill the GPU)
   KCol cols[ESC_MAX_PROJ];  // projected columns (data, nulls, width)
   int32_t cap_index[ESC_MAX_PROJ];      // capture holding projection k, -1 = gather it
   const void* cap_values[ESC_MAX_PROJ];
@@ -1338,12 +1386,77 @@ __device__ __forceinline__ void gather4(const uint8_t* data, void* out, const bo
   for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<T*>(out)[pos[j]] = v[j];
 }
 
-// One warp per 32 consecutive segments (seg_rows = 128*C rows = 4*C <= 32 bitmap words each):
-//  - captured segments: each LANE copies its own segment's captured hits (<= 4*C per column);
-//  - sparse segments (<= one hit per 32 rows): C lanes per segment, each walking one 128-row
-//    chunk, so a warp keeps 32 independent chunks' gathers in flight;
-//  - dense segments: the whole warp, one row per lane of each word (contiguous reads/writes).
-// Segments of dense stream tiles are skipped (sel_stream_kernel writes them).
+// Two grid-stride phases over the selection (segments of dense stream tiles are skipped:
+// sel_stream_kernel writes them):
+//  A. one warp per 32 consecutive segments (seg_rows = 128*C rows = 4*C <= 32 bitmap words):
+//     captured segments - each LANE copies its own segment's captured hits (<= 4*C per column);
+//     dense segments (> one hit per 32 rows) - the whole warp, one row per lane of each word;
+//  B. sparse segments, one LANE per 128-row chunk (4 bitmap words): a 16-byte bitmap load, a
+//     width-CPS segmented scan for the chunk's output base, then the chunk's hits four at a time
+//     (every column's loads in flight before the stores).  Spreading chunks, not segments, over
+//     the warps keeps small selections from running on a handful of SMs.  When the segment
+//     groups alone fill the GPU (sparse_in_a), phase A writes its own sparse segments the same
+//     way, chunk by chunk, and phase B is skipped: no second pass over the segment counts.
+// The hits of one 128-row chunk (4 bitmap words `w4` of segment `seg`, chunk `sub`), written
+// from output position `pos` on, four at a time: every column's loads in flight before the stores.
+__device__ __forceinline__ void sparse_chunk(const SelParams& p, int64_t seg, int sub, uint4 w4,
+                                             unsigned long long pos, bool scap) {
+  const int W = p.seg_rows / 32;
+  const long long cap = p.outs.capacity;
+  unsigned long long lo = ((unsigned long long)w4.y << 32) | w4.x;
+  unsigned long long hi = ((unsigned long long)w4.w << 32) | w4.z;
+  const int64_t row_base = (seg * W + sub * 4) * 32;
+  while (lo | hi) {
+    bool hit[4];
+    unsigned long long ps[4];
+    int64_t prow[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int bit = -1;
+      if (lo) { bit = __ffsll((long long)lo) - 1; lo &= lo - 1; }
+      else if (hi) { bit = 64 + __ffsll((long long)hi) - 1; hi &= hi - 1; }
+      hit[j] = bit >= 0 && (long long)pos < cap;
+      ps[j] = pos;
+      pos += bit >= 0 ? 1 : 0;
+      const int64_t row = row_base + (bit < 0 ? 0 : bit);
+      prow[j] = (hit[j] && p.row_ids) ? __ldg(p.row_ids + row) : row;
+    }
+    for (int k = 0; k < p.n_proj; ++k) {
+      if (scap && p.cap_index[k] >= 0) continue;
+      const KCol& col = p.cols[k];
+      switch (col.width) {
+        case 1: gather4<uint8_t>(col.data, p.outs.out_values[k], hit, prow, ps); break;
+        case 2: gather4<uint16_t>(col.data, p.outs.out_values[k], hit, prow, ps); break;
+        case 4: gather4<uint32_t>(col.data, p.outs.out_values[k], hit, prow, ps); break;
+        default: gather4<unsigned long long>(col.data, p.outs.out_values[k], hit, prow, ps); break;
+      }
+      if (p.outs.out_nulls[k] != nullptr) {
+        uint8_t nb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) nb[j] = (hit[j] && col.nulls) ? __ldg(col.nulls + prow[j]) : (uint8_t)0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) if (hit[j]) p.outs.out_nulls[k][ps[j]] = nb[j];
+      }
+    }
+    if (p.outs.out_row_ids != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (hit[j]) p.outs.out_row_ids[ps[j]] = prow[j];
+    }
+  }
+}
+
+__device__ __forceinline__ bool in_dense_tile(const SelParams& p, int64_t seg) {
+  if (p.rule.dense_min == 0xFFFFFFFFu) return false;
+  const int64_t t = seg >> (__ffs(p.rule.segs_per_tile) - 1);  // segs_per_tile: a power of two
+  if (t >= p.rule.n_tiles) return false;
+  uint32_t ts = 0;
+  for (int j = 0; j < p.rule.segs_per_tile; ++j) {
+    const int64_t q = t * p.rule.segs_per_tile + j;
+    if (q < p.n_segs) ts += __ldg(p.seg_counts + q) & ~ESC_SEG_CAPTURED;
+  }
+  return ts >= p.rule.dense_min;
+}
+
 __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1353,6 +1466,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t sparse_max = (uint32_t)W;
   if (skip_materialize(p.rule)) return;
+  // ---------------- A: captured and dense segments ----------------
   for (int64_t seg0 = gwarp * 32; seg0 < p.n_segs; seg0 += nwarps * 32) {
     const int64_t myseg = seg0 + lane;
     const uint32_t raw = myseg < p.n_segs ? p.seg_counts[myseg] : 0u;
@@ -1360,11 +1474,12 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
     if (p.rule.dense_min != 0xFFFFFFFFu) {
       uint32_t ts = cnt;  // hits of my stream tile (segments_per_tile consecutive lanes)
       for (int d = 1; d < p.rule.segs_per_tile; d <<= 1) ts += __shfl_xor_sync(0xFFFFFFFFu, ts, d);
-      if (ts >= p.rule.dense_min && myseg / p.rule.segs_per_tile < p.rule.n_tiles) cnt = 0;
+      if (ts >= p.rule.dense_min && (myseg >> (__ffs(p.rule.segs_per_tile) - 1)) < p.rule.n_tiles) cnt = 0;
     }
     const bool captured = (raw & ESC_SEG_CAPTURED) != 0;
-    const unsigned long long myoff = cnt ? p.seg_offsets[myseg] : 0ull;
-    // ---- captured segments: lane-parallel copies of the hits the scan captured ----
+    const bool bitmap_work = cnt > 0 && (!captured || p.need_bitmap_captured);
+    const bool dense_work = bitmap_work && cnt > sparse_max;
+    const unsigned long long myoff = (captured || dense_work) && cnt ? p.seg_offsets[myseg] : 0ull;
     if (captured && cnt > 0) {
       for (int k = 0; k < p.n_proj; ++k) {
         const int ci = p.cap_index[k];
@@ -1381,56 +1496,32 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
         }
       }
     }
-    const bool bitmap_work = cnt > 0 && (!captured || p.need_bitmap_captured);
-    // ---- sparse segments: C lanes per segment, one 128-row chunk (4 bitmap words) each: a
-    //      16-byte bitmap load per lane, a width-C segmented scan for the chunk's output base,
-    //      then the chunk's hits (32 * C chunks in flight per warp instead of 32 segments) ----
-    {
+    if (p.sparse_in_a) {
+      // large selections: this warp's own sparse segments, C lanes per segment, one 128-row chunk
+      // each (32 chunks in flight per round); small ones leave them to phase B's wider spread
       const bool sparse_work = bitmap_work && cnt <= sparse_max;
-      const int CPS = W / 4;  // chunks per segment (1, 2, 4, 8): a power of two
+      const unsigned long long soff_l = sparse_work ? p.seg_offsets[myseg] : 0ull;
+      const int CPS = W / 4;
       for (int b = 0; b < CPS; ++b) {
         const int c = b * 32 + lane;
         const int sl = c / CPS;  // lane owning the chunk's segment
         const int sub = c % CPS;
         const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
-        const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, myoff, sl);
+        const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, soff_l, sl);
         const bool scap = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, sl) != 0;
         const int64_t seg = seg0 + sl;
         uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
-        if (work) w4 = *reinterpret_cast<const uint4*>(p.bitmap + seg * W + sub * 4);
+        if (work) w4 = __ldg(reinterpret_cast<const uint4*>(p.bitmap + seg * W + sub * 4));
         const uint32_t pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
         uint32_t incl = pc;
         for (int d = 1; d < CPS; d <<= 1) {
           const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d, CPS);
           if ((lane & (CPS - 1)) >= d) incl += t;
         }
-        if (!work || pc == 0) continue;
-        unsigned long long pos = soff + incl - pc;
-        const uint32_t words[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int wi = 0; wi < 4; ++wi) {
-          uint32_t word = words[wi];
-          while (word) {
-            const int bit = __ffs(word) - 1;
-            word &= word - 1;
-            if ((long long)pos < cap) {
-              const int64_t row = (seg * W + sub * 4 + wi) * 32 + bit;
-              const int64_t prow = p.row_ids ? __ldg(p.row_ids + row) : row;
-              for (int k = 0; k < p.n_proj; ++k) {
-                if (scap && p.cap_index[k] >= 0) continue;
-                const KCol& col = p.cols[k];
-                st_bits(col.width, p.outs.out_values[k], pos, ld_bits(col, prow));
-                if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = col.nulls ? __ldg(col.nulls + prow) : 0;
-              }
-              if (p.outs.out_row_ids != nullptr) p.outs.out_row_ids[pos] = prow;
-            }
-            ++pos;
-          }
-        }
+        if (work && pc != 0) sparse_chunk(p, seg, sub, w4, soff + incl - pc, scap);
       }
     }
-    // ---- dense segments: the whole warp, one row per lane of each word ----
-    uint32_t dense = __ballot_sync(0xFFFFFFFFu, bitmap_work && cnt > sparse_max);
+    uint32_t dense = __ballot_sync(0xFFFFFFFFu, dense_work);
     while (dense) {
       const int l = __ffs(dense) - 1;
       dense &= dense - 1;
@@ -1483,6 +1574,35 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
         }
       }
     }
+  }
+  // ---------------- B: sparse segments, one lane per 128-row chunk ----------------
+  if (p.sparse_in_a) return;
+  const int CPS = W / 4;  // chunks per segment (1, 2, 4, 8): a power of two dividing 32
+  const int cps_log = __ffs(CPS) - 1;  // shifts, not 64-bit divisions, in the loop below
+  const int64_t n_chunks = p.n_segs * CPS;
+  const int64_t stride = nwarps * 32;
+  // the next iteration's segment count is loaded one iteration ahead: most chunks have no sparse
+  // work (captured, dense or empty), and their iterations should not each wait on a load
+  uint32_t raw_next = gwarp * 32 + lane < n_chunks ? __ldg(p.seg_counts + ((gwarp * 32 + lane) >> cps_log)) : 0u;
+  for (int64_t c0 = gwarp * 32; c0 < n_chunks; c0 += stride) {
+    const int64_t c = c0 + lane;
+    const int64_t seg = c >> cps_log;
+    const int sub = (int)(c & (CPS - 1));
+    const uint32_t raw = raw_next;
+    raw_next = c + stride < n_chunks ? __ldg(p.seg_counts + ((c + stride) >> cps_log)) : 0u;
+    const uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
+    const bool scap = (raw & ESC_SEG_CAPTURED) != 0;
+    const bool work = cnt > 0 && cnt <= sparse_max && (!scap || p.need_bitmap_captured) && !in_dense_tile(p, seg);
+    uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
+    if (work) w4 = __ldg(reinterpret_cast<const uint4*>(p.bitmap + seg * W + sub * 4));
+    const uint32_t pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+    uint32_t incl = pc;
+    for (int d = 1; d < CPS; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d, CPS);
+      if ((lane & (CPS - 1)) >= d) incl += t;
+    }
+    if (!work || pc == 0) continue;
+    sparse_chunk(p, seg, sub, w4, p.seg_offsets[seg] + incl - pc, scap);
   }
 }
 

@@ -56,6 +56,7 @@ using namespace esc;
 
 thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};  // kernels this library has launched (esc_launch_count)
+unsigned long long* g_trace = nullptr;           // esc_debug_trace stamps (diagnostics only)
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -527,6 +528,7 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
   kp.hdr = static_cast<WsHeader*>(d_ws);
   kp.status = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(d_ws) + sizeof(WsHeader));
   kp.result = result;
+  kp.trace = g_trace;
   return ESC_OK;
 }
 
@@ -813,7 +815,12 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
     M->stream_grid = (unsigned)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
   }
   M->segs = (unsigned)((sp.n_segs + kScanSeg - 1) / kScanSeg);
-  const int64_t want = (sp.n_segs + 32 * kSelWarps - 1) / (32 * kSelWarps);  // 32 segments per warp
+  // phase A: 32 segments per warp; when those groups alone give every SM 4+ CTAs, phase A also
+  // writes the sparse segments; otherwise phase B spreads 128-row chunks (32 per warp)
+  const int64_t groups_ctas = (sp.n_segs + 32 * kSelWarps - 1) / (32 * kSelWarps);
+  sp.sparse_in_a = groups_ctas >= 4LL * sms ? 1 : 0;
+  const int64_t chunks = sp.n_segs * (sp.seg_rows / kChunkRows);
+  const int64_t want = sp.sparse_in_a ? groups_ctas : (chunks + 32 * kSelWarps - 1) / (32 * kSelWarps);
   M->compact_grid = (unsigned)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
   return ESC_OK;
 }
@@ -1099,6 +1106,11 @@ int esc_jit_stats(int64_t* out) {
   out[2] = jit::g_failures.load();
   out[3] = jit::g_compile_us.load();
   out[4] = jit::nvrtc().ok ? 1 : 0;
+  return ESC_OK;
+}
+
+int esc_debug_trace(void* d_stamps) {
+  g_trace = static_cast<unsigned long long*>(d_stamps);
   return ESC_OK;
 }
 
