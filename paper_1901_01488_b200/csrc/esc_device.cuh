@@ -1339,6 +1339,7 @@ struct SelParams {
   int32_t n_proj;
   int32_t need_bitmap_captured;  // captured segments still need the bitmap (row ids / uncaptured columns)
   int32_t sparse_in_a;           // phase A also writes sparse segments (grids that fill the GPU)
+  int32_t a_split;               // warps per 32-segment group in phase A (power of two; 1 if sparse_in_a)
   KCol cols[ESC_MAX_PROJ];  // projected columns (data, nulls, width)
   int32_t cap_index[ESC_MAX_PROJ];      // capture holding projection k, -1 = gather it
   const void* cap_values[ESC_MAX_PROJ];
@@ -1389,7 +1390,7 @@ __device__ __forceinline__ void gather4(const uint8_t* data, void* out, const bo
 // Two grid-stride phases over the selection (segments of dense stream tiles are skipped:
 // sel_stream_kernel writes them):
 //  A. one warp per 32 consecutive segments (seg_rows = 128*C rows = 4*C <= 32 bitmap words):
-//     captured segments - each LANE copies its own segment's captured hits (<= 4*C per column);
+//     captured segments - the group's captured hits (<= 4*C per segment) spread over the lanes;
 //     dense segments (> one hit per 32 rows) - the whole warp, one row per lane of each word;
 //  B. sparse segments, one LANE per 128-row chunk (4 bitmap words): a 16-byte bitmap load, a
 //     width-CPS segmented scan for the chunk's output base, then the chunk's hits four at a time
@@ -1467,7 +1468,14 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
   const uint32_t sparse_max = (uint32_t)W;
   if (skip_materialize(p.rule)) return;
   // ---------------- A: captured and dense segments ----------------
-  for (int64_t seg0 = gwarp * 32; seg0 < p.n_segs; seg0 += nwarps * 32) {
+  // a_split (R, a power of two) warps share a group: warp r of it takes captured entries
+  // r*32 + lane (mod 32R) and every R-th dense segment, so small selections use the whole grid
+  const int R = p.a_split;
+  const int r_log = __ffs(R) - 1;
+  const int64_t n_units = ((p.n_segs + 31) >> 5) << r_log;
+  for (int64_t u = gwarp; u < n_units; u += nwarps) {
+    const int64_t seg0 = (u >> r_log) * 32;
+    const int r = (int)(u & (R - 1));
     const int64_t myseg = seg0 + lane;
     const uint32_t raw = myseg < p.n_segs ? p.seg_counts[myseg] : 0u;
     uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
@@ -1480,19 +1488,56 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
     const bool bitmap_work = cnt > 0 && (!captured || p.need_bitmap_captured);
     const bool dense_work = bitmap_work && cnt > sparse_max;
     const unsigned long long myoff = (captured || dense_work) && cnt ? p.seg_offsets[myseg] : 0ull;
-    if (captured && cnt > 0) {
-      for (int k = 0; k < p.n_proj; ++k) {
-        const int ci = p.cap_index[k];
-        if (ci < 0) continue;
-        const int w = p.cols[k].width;
-        const uint8_t* src = static_cast<const uint8_t*>(p.cap_values[ci]) + (size_t)myseg * p.cap_per_seg * w;
-        void* dst = p.outs.out_values[k];
-        for (uint32_t e = 0; e < cnt; ++e)
-          if ((long long)(myoff + e) < cap) st_bits(w, dst, myoff + e, ld_w(w, src, e));
-        if (p.outs.out_nulls[k] != nullptr) {
-          const uint8_t* ns = p.cap_nulls[ci] ? p.cap_nulls[ci] + (size_t)myseg * p.cap_per_seg : nullptr;
-          for (uint32_t e = 0; e < cnt; ++e)
-            if ((long long)(myoff + e) < cap) p.outs.out_nulls[k][myoff + e] = ns ? ns[e] : 0;
+    // captured hits: the group's entries are spread over the lanes (lane e: entries e, e+32, ...
+    // of the group's concatenated captured lists), four columns' loads in flight per entry
+    {
+      const uint32_t ccnt = captured ? cnt : 0u;
+      uint32_t incl = ccnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      for (uint32_t e0 = (uint32_t)r * 32; e0 < total; e0 += 32u * R) {
+        const uint32_t e = e0 + lane;
+        // owning lane: the first whose inclusive count exceeds e (binary search over the lanes)
+        int sl = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, sl + step - 1);
+          if (v <= e) sl += step;
+        }
+        const uint32_t s_incl = __shfl_sync(0xFFFFFFFFu, incl, sl);
+        const uint32_t s_cnt = __shfl_sync(0xFFFFFFFFu, ccnt, sl);
+        const unsigned long long s_off = __shfl_sync(0xFFFFFFFFu, myoff, sl);
+        if (e >= total) continue;
+        const uint32_t idx = e - (s_incl - s_cnt);
+        const unsigned long long pos = s_off + idx;
+        if ((long long)pos >= cap) continue;
+        const size_t slot = (size_t)(seg0 + sl) * p.cap_per_seg + idx;
+        for (int k0 = 0; k0 < p.n_proj; k0 += 4) {
+          unsigned long long v[4];
+          uint8_t nb[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = k0 + j;
+            const int ci = k < p.n_proj ? p.cap_index[k] : -1;
+            v[j] = 0;
+            nb[j] = 0;
+            if (ci >= 0) {
+              v[j] = ld_w(p.cols[k].width, static_cast<const uint8_t*>(p.cap_values[ci]) + slot * p.cols[k].width, 0);
+              if (p.outs.out_nulls[k] != nullptr && p.cap_nulls[ci] != nullptr) nb[j] = p.cap_nulls[ci][slot];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = k0 + j;
+            if (k < p.n_proj && p.cap_index[k] >= 0) {
+              st_bits(p.cols[k].width, p.outs.out_values[k], pos, v[j]);
+              if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = nb[j];
+            }
+          }
         }
       }
     }
@@ -1522,9 +1567,10 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
       }
     }
     uint32_t dense = __ballot_sync(0xFFFFFFFFu, dense_work);
-    while (dense) {
+    for (int di = 0; dense; ++di) {
       const int l = __ffs(dense) - 1;
       dense &= dense - 1;
+      if ((di & (R - 1)) != r) continue;
       const int64_t seg = seg0 + l;
       const bool seg_captured = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, l) != 0;
       const unsigned long long base = __shfl_sync(0xFFFFFFFFu, myoff, l);

@@ -822,6 +822,11 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   const int64_t chunks = sp.n_segs * (sp.seg_rows / kChunkRows);
   const int64_t want = sp.sparse_in_a ? groups_ctas : (chunks + 32 * kSelWarps - 1) / (32 * kSelWarps);
   M->compact_grid = (unsigned)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
+  sp.a_split = 1;
+  if (!sp.sparse_in_a) {
+    const int64_t groups = (sp.n_segs + 31) / 32, warps = (int64_t)M->compact_grid * kSelWarps;
+    while (sp.a_split < 8 && groups * sp.a_split * 2 <= warps) sp.a_split *= 2;
+  }
   return ESC_OK;
 }
 
