@@ -278,12 +278,18 @@ int esc_materialize_selection(const esc_selection_t* sel, int64_t nrows, const e
 /* A queued ESC step — esc_scan_select + esc_materialize_selection with the same arguments —
  * prepared ONCE (program lowering, tile geometry, JIT kernel lookup, compaction plan) and then
  * re-issued by esc_step_plan_launch with no host work beyond the launches.  Every pointer is
- * captured: the plan is valid while those buffers (workspace, selection, outputs, result) are. */
+ * captured: the plan is valid while those buffers (workspace, selection, outputs, result) are.
+ * sel == NULL (mat_cols unused) prepares the one-pass variant instead — esc_compact_onepass with
+ * the same arguments — whose outputs esc_step_plan_rebind may later point at new buffers of the
+ * same shape (small tables hand their output buffers over as the temp, so each step has new
+ * ones; the prepared launch stays). */
 int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, int32_t ncols, int64_t nrows,
                          esc_selection_t* sel, const esc_column_t* mat_cols, int32_t mat_ncols,
                          const esc_outputs_t* outs, esc_result_t* result, void* d_ws, size_t ws_bytes,
                          void** out_plan);
 int esc_step_plan_launch(void* plan, int32_t parts, void* stream); /* parts: 1 scan, 2 compaction, 3 both */
+int esc_step_plan_rebind(void* plan, const esc_outputs_t* outs); /* one-pass plans; same n_proj,
+                                                                     slots, capacity, null outputs */
 int esc_step_plan_destroy(void* plan);
 
 /* out[i] = col[idx[i]] (values and, when present, nulls).  replaces Column.take

@@ -155,6 +155,7 @@ _SIGNATURES = {
                                        C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "esc_step_plan_launch": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "esc_step_plan_destroy": (C.c_int, [C.c_void_p]),
+    "esc_step_plan_rebind": (C.c_int, [C.c_void_p, C.c_void_p]),
     "esc_csv_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "esc_csv_count": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "esc_csv_fields": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,

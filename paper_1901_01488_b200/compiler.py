@@ -58,6 +58,7 @@ class CompiledPredicate:
     n_udfs: int
     may_fail: bool                # some UDF is evaluated densely (can raise)
     col_array: object = field(default=None, repr=False)
+    c_plans: dict = field(default_factory=dict, repr=False)  # prepared one-pass launches (executor)
 
     @property
     def ncols(self) -> int:
@@ -398,18 +399,26 @@ def _key(pred: ex.Expr):
 
 def compile_predicate(table, pred: ex.Expr) -> CompiledPredicate:
     """Compile (or fetch from the per-table cache) the device program of ``pred``."""
+    with _cache_lock:
+        per_table = _cache.setdefault(table, {})
+        seen = per_table.get(("id", id(pred)))  # the same tree object again: no re-keying
+    if seen is not None and seen[0] is pred:
+        return seen[1]
+    orig = pred
     pred = ex.adopt(pred)  # trees from the reference analyzer drive the engine unchanged
     key = _key(pred)
     with _cache_lock:
-        per_table = _cache.setdefault(table, {})
         hit = per_table.get(key)
     if hit is not None:
+        with _cache_lock:
+            per_table[("id", id(orig))] = (orig, hit)  # holds ``orig``: its id stays unique
         return hit
     cp = _Builder(table, pred).build()
     with _cache_lock:
-        if len(per_table) > 256:
+        if len(per_table) > 512:
             per_table.clear()
         per_table[key] = cp
+        per_table[("id", id(orig))] = (orig, cp)
     return cp
 
 

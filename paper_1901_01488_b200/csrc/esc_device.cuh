@@ -1022,8 +1022,11 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
     if (w < S && lane == 0) {
       atomicAdd(s_cta_count, my_count);
       __threadfence_block();
-      if (atomicAdd(s_writers_done, 1u) == (uint32_t)(S - 1))
+      if (atomicAdd(s_writers_done, 1u) == (uint32_t)(S - 1)) {
+        if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 2] = gtimer();
         finish_cta(p, *reinterpret_cast<volatile unsigned long long*>(s_cta_count));
+        if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 4] = gtimer();
+      }
     }
     return;
   }

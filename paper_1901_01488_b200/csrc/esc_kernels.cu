@@ -559,7 +559,7 @@ int prepare_c(const KParams& kp, ScanLaunch* L) {
   L->grid = (unsigned)grid;
   L->block = Layout<COMPACT>::kThreads;
   L->smem = smem;
-  L->coop = COMPACT;  // the one-pass look-back relies on every CTA being resident
+  L->coop = COMPACT && getenv("ESC_NO_COOP") == nullptr;  // the one-pass look-back relies on every CTA being resident
   // JIT tier: large scans whose tiles run the fast (staged) evaluator
   const int mode = jit::g_mode.load();
   if (mode == 2 || (mode == 1 && kp.nrows >= jit::g_min_rows.load())) {
@@ -915,7 +915,23 @@ struct StepPlanImpl {
   KParams kp;
   ScanLaunch scan;
   MatLaunch mat;
+  bool onepass = false;  // one launch of the look-back kernel (no selection, no queued compaction)
 };
+
+// next look-back epoch of a workspace (status words carry it, so they need no clearing per launch)
+int next_epoch(KParams& kp, int64_t nrows, void* d_ws, cudaStream_t stream) {
+  std::lock_guard<std::mutex> g(g_epoch_mu);
+  uint32_t& ep = g_epochs[d_ws];
+  ep = (ep + 1) & 0xFFFFu;
+  if (ep == 0) {
+    // epoch wrapped: stale status words could alias, clear them
+    cudaError_t e = cudaMemsetAsync(kp.status, 0, status_words(nrows) * sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("status clear: ") + cudaGetErrorString(e));
+    ep = 1;
+  }
+  kp.epoch = ep;
+  return ESC_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -936,6 +952,21 @@ int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, in
   *out_plan = nullptr;
   StepPlanImpl* plan = new (std::nothrow) StepPlanImpl();
   if (plan == nullptr) return fail(ESC_ERR_INVALID, "out of host memory");
+  if (sel == nullptr) {  // one-pass plan: the look-back kernel compacts `outs` directly
+    if (outs == nullptr) {
+      delete plan;
+      return fail(ESC_ERR_INVALID, "null outputs");
+    }
+    int rc = build_params(plan->kp, prog, cols, ncols, nrows, nullptr, d_ws, ws_bytes, result, outs);
+    if (rc == ESC_OK) rc = prepare<true>(plan->kp, &plan->scan);
+    if (rc != ESC_OK) {
+      delete plan;
+      return rc;
+    }
+    plan->onepass = true;
+    *out_plan = plan;
+    return ESC_OK;
+  }
   int rc = prepare_select(plan->kp, prog, cols, ncols, nrows, nullptr, sel, result, d_ws, ws_bytes);
   if (rc == ESC_OK) rc = prepare<false>(plan->kp, &plan->scan);
   if (rc == ESC_OK) rc = prepare_mat(sel, nrows, mat_cols, mat_ncols, nullptr, outs, d_ws, ws_bytes, &plan->mat);
@@ -950,10 +981,30 @@ int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, in
 int esc_step_plan_launch(void* plan, int32_t parts, void* stream) {
   if (plan == nullptr) return fail(ESC_ERR_INVALID, "null plan");
   if (parts < 1 || parts > 3) return fail(ESC_ERR_INVALID, "parts must be 1 (scan), 2 (compaction) or 3");
-  const StepPlanImpl* p = static_cast<const StepPlanImpl*>(plan);
+  StepPlanImpl* p = static_cast<StepPlanImpl*>(plan);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  p->kp.trace = g_trace;
+  if (p->onepass) {
+    const int rc = next_epoch(p->kp, p->kp.nrows, p->kp.hdr, st);
+    return rc != ESC_OK ? rc : issue_scan(p->scan, p->kp, st);
+  }
   int rc = (parts & 1) ? issue_scan(p->scan, p->kp, st) : ESC_OK;
   return (rc != ESC_OK || !(parts & 2)) ? rc : issue_mat(p->mat, st);
+}
+
+int esc_step_plan_rebind(void* plan, const esc_outputs_t* outs) {
+  if (plan == nullptr || outs == nullptr) return fail(ESC_ERR_INVALID, "null plan or outputs");
+  StepPlanImpl* p = static_cast<StepPlanImpl*>(plan);
+  if (!p->onepass) return fail(ESC_ERR_INVALID, "only one-pass plans take new outputs");
+  const esc_outputs_t& o = p->kp.outs;
+  bool same = outs->n_proj == o.n_proj && outs->capacity == o.capacity && outs->flags == o.flags &&
+              (outs->out_row_ids == nullptr) == (o.out_row_ids == nullptr);
+  for (int k = 0; same && k < o.n_proj; ++k)
+    same = outs->slot[k] == o.slot[k] && (outs->out_nulls[k] == nullptr) == (o.out_nulls[k] == nullptr) &&
+           (outs->out_values[k] == nullptr) == (o.out_values[k] == nullptr);
+  if (!same) return fail(ESC_ERR_INVALID, "outputs differ in shape from the plan's");
+  p->kp.outs = *outs;
+  return ESC_OK;
 }
 
 int esc_step_plan_destroy(void* plan) {
@@ -993,19 +1044,8 @@ int esc_compact_onepass(const esc_program_t* prog, const esc_column_t* cols, int
   if (outs == nullptr) return fail(ESC_ERR_INVALID, "null outputs");
   int rc = build_params(kp, prog, cols, ncols, nrows, d_row_ids, d_ws, ws_bytes, result, outs);
   if (rc != ESC_OK) return rc;
-  {
-    std::lock_guard<std::mutex> g(g_epoch_mu);
-    uint32_t& ep = g_epochs[d_ws];
-    ep = (ep + 1) & 0xFFFFu;
-    if (ep == 0) {
-      // epoch wrapped: stale status words could alias, clear them
-      cudaError_t e = cudaMemsetAsync(kp.status, 0, status_words(nrows) * sizeof(unsigned long long),
-                                      static_cast<cudaStream_t>(stream));
-      if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("status clear: ") + cudaGetErrorString(e));
-      ep = 1;
-    }
-    kp.epoch = ep;
-  }
+  rc = next_epoch(kp, nrows, d_ws, static_cast<cudaStream_t>(stream));
+  if (rc != ESC_OK) return rc;
   return launch<true>(kp, static_cast<cudaStream_t>(stream));
 }
 

@@ -79,10 +79,21 @@ class RowSelection:
 # ------------------------------------------------------------------------------------------------
 # launches
 # ------------------------------------------------------------------------------------------------
+_STREAMS: dict = {}
+
+
 def _stream(device: torch.device) -> torch.cuda.Stream:
+    """The device's current stream; the Stream object is cached per (stream id, device) — the
+    public ``torch.cuda.current_stream`` builds a new one per call (several microseconds, and
+    an ESC step asks for it a few times)."""
     if device.type != "cuda":
         raise N.NativeUnavailable(f"table lives on {device}; the ESC kernels need a CUDA device")
-    return torch.cuda.current_stream(device)
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    key = torch._C._cuda_getCurrentStream(idx)
+    s = _STREAMS.get(key)
+    if s is None:
+        s = _STREAMS[key] = torch.cuda.current_stream(idx)
+    return s
 
 
 def _row_ids(selection: RowSelection | None):
@@ -530,10 +541,20 @@ def launch_step(table: ColumnTable, pred: ex.Expr, needed, capacity: int, materi
     cap = max(0, min(int(capacity), n))
     if n <= ONEPASS_MAX_ROWS:
         plan = _onepass_plan(cp, table, proj, cap, ws)
+        # the prepared launch lives with the compiled predicate (same table, so same columns);
+        # output buffers handed over as the temp are replaced by rebinding the new ones
+        ckey = (plan.key[3:], n, slot, ws_ptr, N.TUNING[0])
+        handle = cp.c_plans.get(ckey)
+        if handle is None:
+            h = C.c_void_p()
+            N.check(lib.esc_step_plan_create(C.byref(cp.program), plan.mat_cols, plan.mat_ncols, n, None, None, 0,
+                                             C.byref(plan.outs), res, C.c_void_p(ws_ptr), C.c_size_t(ws_bytes),
+                                             C.byref(h)), "esc_step_plan_create")
+            handle = cp.c_plans[ckey] = _CPlan(h.value, lib)
+        else:
+            N.check(lib.esc_step_plan_rebind(C.c_void_p(handle.ptr), C.byref(plan.outs)), "esc_step_plan_rebind")
         ev0 = _ev_start(stream)
-        N.check(lib.esc_compact_onepass(C.byref(cp.program), plan.mat_cols, plan.mat_ncols, n, None,
-                                        C.byref(plan.outs), res, C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), sp),
-                "esc_compact_onepass")
+        N.check(lib.esc_step_plan_launch(C.c_void_p(handle.ptr), 3, sp), "esc_step_plan_launch")
         _ev_end(stream, ev0, "compact")
         return PendingStep(table, cp, proj, cap, "onepass", slot, plan)
     row_bytes = sum(c.values.element_size() + (1 if c.nulls is not None else 0) for c in proj)
@@ -609,7 +630,9 @@ def _take_outputs(ps: PendingStep, ws, k: int) -> list[Column]:
     if ps.kind == "onepass" and plan.nbytes <= SMALL_OUTPUT_BYTES:
         return [Column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
                 for c, v, m in zip(ps.proj, plan.out_values, plan.out_nulls)]
-    cols = _trim(ps.proj, plan.out_values, plan.out_nulls, k, _stream(ps.table.device))
+    if plan.trim_cache is None:
+        plan.trim_cache = {}
+    cols = _trim(ps.proj, plan.out_values, plan.out_nulls, k, _stream(ps.table.device), plan.trim_cache)
     _plan_checkin(ws, plan)
     return cols
 
@@ -630,6 +653,7 @@ class _StepPlan:
     mat_ncols: int
     nbytes: int = 0
     c_plans: dict | None = None   # (result slot, workspace) -> prepared esc_step_plan
+    trim_cache: dict | None = None  # _trim's ctypes arguments (sources are the fixed outputs)
 
 
 def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: int, ws) -> _StepPlan:
@@ -737,39 +761,38 @@ def _onepass_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacit
     return plan
 
 
-def _trim(proj: list, values: list, nulls: list, count: int, stream) -> list[Column]:
-    """Exact-size temp columns: the first ``count`` rows of each capacity-sized output, carved
-    from ONE allocation by ONE batched copy launch (esc_copy_regions)."""
-    regions = []
-    for v, m in zip(values, nulls):
-        regions.append((v, count * v.element_size()))
-        if m is not None:
-            regions.append((m, count))
-    offs, total = [], 0
-    for _, nb in regions:
-        offs.append(total)
-        total += (nb + 255) & ~255
-    dev = values[0].device if values else None
-    out = []
-    if not regions:
-        return out
-    buf = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
-    k = len(regions)
+def _trim(proj: list, values: list, nulls: list, count: int, stream, cache: dict | None = None) -> list[Column]:
+    """Exact-size temp columns: the first ``count`` rows of each capacity-sized output, copied
+    by ONE batched launch (esc_copy_regions).  ``cache`` (a plan's dict) keeps the ctypes
+    argument arrays — the sources are the plan's fixed buffers — so a step only fills in the
+    destinations and sizes."""
+    srcs = [t for v, m in zip(values, nulls) for t in ((v,) if m is None else (v, m))]
+    k = len(srcs)
+    if not k:
+        return []
+    dev = values[0].device
+    outs = [torch.empty(count, dtype=t.dtype, device=dev) for t in srcs]
     if count:
-        dst = (C.c_void_p * k)(*[buf.data_ptr() + o for o in offs])
-        src = (C.c_void_p * k)(*[t.data_ptr() for t, _ in regions])
-        nbytes = (C.c_int64 * k)(*[nb for _, nb in regions])
+        arrs = cache.get("trim") if cache is not None else None
+        if arrs is None:
+            arrs = ((C.c_void_p * k)(), (C.c_void_p * k)(*[t.data_ptr() for t in srcs]), (C.c_int64 * k)())
+            if cache is not None:
+                cache["trim"] = arrs
+        dst, src, nbytes = arrs
+        for i, t in enumerate(outs):
+            dst[i] = t.data_ptr()
+            nbytes[i] = count * t.element_size()
         N.check(N.load_library().esc_copy_regions(k, dst, src, nbytes, C.c_void_p(stream.cuda_stream)),
                 "esc_copy_regions")
-    r = 0
-    for c, v, m in zip(proj, values, nulls):
-        vv = buf[offs[r]: offs[r] + count * v.element_size()].view(v.dtype)
+    out, r = [], 0
+    for c, m in zip(proj, nulls):
+        vv = outs[r]
         r += 1
         mm = None
         if m is not None:
-            mm = buf[offs[r]: offs[r] + count].view(torch.bool)
+            mm = outs[r]
             r += 1
-        out.append(Column(c.name, c.kind, vv, mm, c.dictionary))
+        out.append(Column.device_column(c.name, c.kind, vv, mm, c.dictionary))
     return out
 
 

@@ -211,6 +211,20 @@ class Column:
         self.dictionary = dictionary
         self._zero_mask = None
 
+    @classmethod
+    def device_column(cls, name: str, kind: ColumnKind, values: torch.Tensor, nulls: torch.Tensor | None,
+                      dictionary: "Dictionary | None") -> "Column":
+        """Internal: wrap device tensors the kernels just produced (contiguous, native dtype, on
+        the column's device) without re-validating them; a null mask still goes through the
+        normal path (it is dropped when it holds no NULL)."""
+        if nulls is not None or values.dtype == torch.bool:
+            return cls(name, kind, values, nulls, dictionary)
+        c = cls.__new__(cls)
+        c.name, c.kind, c.values, c.nulls = name, kind, values, None
+        c.dictionary = Dictionary() if kind.is_text and dictionary is None else dictionary
+        c._zero_mask = None
+        return c
+
     # -- reference-compatible surface ------------------------------------------------------
     @property
     def null_mask(self) -> torch.Tensor:

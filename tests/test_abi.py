@@ -132,6 +132,7 @@ def test_join_csv_plan_entry_points_validate_arguments(native_lib):
     err(native_lib.esc_step_plan_launch(None, 3, None), "null plan")
     h = C.c_void_p()
     err(native_lib.esc_step_plan_create(None, None, 0, 10, None, None, 0, None, None, None, 0, C.byref(h)),
-        "null selection output")
+        "null outputs")  # sel == NULL asks for the one-pass plan, which needs outputs
     assert h.value is None
+    err(native_lib.esc_step_plan_rebind(None, None), "null plan or outputs")
     assert native_lib.esc_csv_workspace_bytes(1 << 30) > native_lib.esc_csv_workspace_bytes(1 << 10)
