@@ -20,16 +20,42 @@ conj = [ex.ColumnCompare(ex.ColumnRef("fact", a), "=", ex.ColumnRef(names.get(di
         for _, a, dim, b in datagen.CONFIG3_EDGES]
 conj += [serde.from_json(j, names.get(dim, dim)) for dim, j in datagen.CONFIG3_WHERE.items()]
 q = ra.query(eng.catalog, ["fact", "dates", "customer", "supplier", "part"], ex.And(tuple(conj)))
+import functools
+from collections import defaultdict
+acc = defaultdict(float)
+def timed(mod, name, label):
+    f = getattr(mod, name)
+    @functools.wraps(f)
+    def w(*a, **k):
+        t0 = time.perf_counter()
+        try:
+            return f(*a, **k)
+        finally:
+            acc[label] += time.perf_counter() - t0
+    setattr(mod, name, w)
+from paper_1901_01488_b200.catalog import Catalog
+timed(executor, "launch_step", "launch_step")
+timed(executor, "_onepass_plan", "  _onepass_plan")
+timed(executor, "compile_predicate", "  compile_predicate")
+timed(executor, "finish_step", "finish_step")
+timed(executor, "_take_outputs", "  _take_outputs")
+timed(optimizer, "_esc_batch", "_esc_batch")
+timed(optimizer, "build_join_graph", "build_join_graph")
+timed(optimizer, "order_builds", "order_builds")
+timed(Catalog, "materialize_temp", "materialize_temp")
+timed(torch.cuda.Stream, "synchronize", "stream sync (wait)")
 def once():
     p = optimizer.plan(q, eng.catalog, cfg)
     eng.catalog.temps.sweep()
     return p
 for _ in range(10): once()
+acc.clear()
 walls, ovs = [], []
 for _ in range(50):
     torch.cuda.synchronize(); t0 = time.perf_counter(); p = once(); walls.append((time.perf_counter() - t0) * 1e6)
     ovs.append(optimizer.esc_overhead_ms(p) * 1e3)
 print(f"plan wall median {statistics.median(walls):.1f} us, esc overhead median {statistics.median(ovs):.1f} us")
+for k, v in acc.items(): print(f"  {k:24s} {v/50*1e6:8.1f} us per plan")
 executor.KERNEL_EVENTS = []
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
