@@ -17,4 +17,10 @@ $N -k regex:join_bits --launch-skip 3 --launch-count 1 -o gpurun_out/prof/join_b
     > gpurun_out/prof/join.log 2>&1
 $N -k regex:csv_ --launch-skip 8 --launch-count 4 -o gpurun_out/prof/csv_ingest python tools/diag_ingest.py \
     > gpurun_out/prof/csv.log 2>&1
+$N -k regex:esc_scan_kernel --launch-skip 30 --launch-count 1 -o gpurun_out/prof/k1_config2 python tools/diag_config2.py \
+    > gpurun_out/prof/k1c2.log 2>&1
+$N -k regex:sel_compact --launch-skip 10 --launch-count 1 -o gpurun_out/prof/selc_config2 python tools/diag_config2.py \
+    > gpurun_out/prof/selc2.log 2>&1
+$N -k regex:esc_scan_kernel --launch-skip 60 --launch-count 1 -o gpurun_out/prof/onepass_dim python tools/diag_onepass2.py \
+    > gpurun_out/prof/op.log 2>&1
 ls -la gpurun_out/prof
