@@ -667,9 +667,17 @@ def run_sweep(args, dev, peak):
             mms = sum(x for x, kk in tm if kk in ("select", "materialize")) / 3
             bc = wl.algorithmic_bytes(k, materialize=False)
             bm = wl.algorithmic_bytes(k, materialize=True)
+            # DRAM floor at 128-byte-line granularity (what a scattered hit really costs: ncu shows
+            # one line fetched per gathered value): the scan's columns + bitmap write and read +
+            # every projected column's lines that hold a hit + the output
+            se = k / n
+            pw = [t.column(c).values.element_size() for c in wl.project]
+            lines = sum(n * w * (1.0 - (1.0 - se) ** (128 // w)) for w in pw)
+            floor = bc + n / 4 + lines + k * sum(pw)
             res.append({"pred": "conj4" if conj4 else "single", "s": s, "count": k, "count_ms": cms,
                         "count_GBps": bc / cms / 1e6, "count_frac": bc / cms / 1e6 / peak,
-                        "compact_ms": mms, "compact_GBps": bm / mms / 1e6, "compact_frac": bm / mms / 1e6 / peak})
+                        "compact_ms": mms, "compact_GBps": bm / mms / 1e6, "compact_frac": bm / mms / 1e6 / peak,
+                        "line_floor_ms": floor / peak / 1e6, "line_floor_frac": floor / peak / 1e6 / mms})
             torch.cuda.empty_cache()
     return {"rows": n, "peak_GBps": peak, "results": res}
 
