@@ -869,10 +869,15 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
     // ===================== producer =====================
     if (lane == 0) {
       const uint64_t policy = evict_first_policy();
-      // static round-robin schedule: round r of every CTA covers tiles [r*G, (r+1)*G), so a
+      // K2: static round-robin schedule: round r of every CTA covers tiles [r*G, (r+1)*G), so a
       // tile's look-back predecessors are evaluated concurrently in the same round (K2 is a
-      // cooperative launch: every CTA is resident, no look-back waits on an unscheduled CTA)
+      // cooperative launch: every CTA is resident, no look-back waits on an unscheduled CTA).
+      // K1: after its first tile a CTA takes tickets from the header's counter (one tile ahead,
+      // so the atomic's latency hides behind the ring wait): a CTA that DRAM serves late at the
+      // start (first tiles arrive 2-120 us apart across CTAs) takes fewer tiles instead of
+      // finishing last (600M rows: the static schedule's last CTA ended 37 us after the median)
       int64_t tile = blockIdx.x;
+      int64_t next = COMPACT ? 0 : (int64_t)atomicAdd(&p.hdr->ticket, 1ull) + gridDim.x;
       int s = 0;
       uint32_t ph = 0;
       int sentinels = 0;
@@ -931,7 +936,12 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
         } else {
           mbar_arrive(&full_bar[s]);
         }
-        tile += gridDim.x;
+        if (COMPACT) {
+          tile += gridDim.x;
+        } else {
+          tile = next;
+          if (tile < p.n_tiles) next = (int64_t)atomicAdd(&p.hdr->ticket, 1ull) + gridDim.x;
+        }
       }
       if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 3] = gtimer();
     }
