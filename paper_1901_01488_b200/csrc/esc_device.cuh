@@ -809,16 +809,23 @@ __device__ __forceinline__ void finish_cta(const KParams& p, unsigned long long 
   if (prev == gridDim.x - 1) {
     if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 5] = gtimer();
     __threadfence();
-    volatile WsHeader* h = p.hdr;
-    p.result->count = h->count;
-    if (p.sel_on && p.sel.d_count != nullptr) *p.sel.d_count = h->count;
+    // the header's words are read from L2 (ld.global.cg) all at once: one round trip, where
+    // volatile reads went one by one
+    WsHeader* h = p.hdr;
+    const unsigned long long count = __ldcg(&h->count);
+    unsigned long long fail[ESC_MAX_UDFS];
+#pragma unroll
+    for (int i = 0; i < ESC_MAX_UDFS; ++i) fail[i] = __ldcg(&h->fail[i]);
+    p.result->count = count;
+    if (p.sel_on && p.sel.d_count != nullptr) *p.sel.d_count = count;
+#pragma unroll
     for (int i = 0; i < ESC_MAX_UDFS; ++i) {
-      p.result->udf_fail[i] = h->fail[i];
-      h->fail[i] = ~0ull;
+      p.result->udf_fail[i] = fail[i];
+      __stcg(&h->fail[i], ~0ull);
     }
-    h->count = 0;
-    h->ticket = 0;
-    h->done = 0;
+    __stcg(&h->count, 0ull);
+    __stcg(&h->ticket, 0ull);
+    __stcg(&h->done, 0ull);
     // no system-scope fence: the host reads the result only after the kernel has completed (a
     // stream/event wait), and kernel completion makes every write visible (the fence cost ~5 us)
     if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 6] = gtimer();
