@@ -238,8 +238,10 @@ int esc_compact_onepass(const esc_program_t* prog, const esc_column_t* cols, int
  *  - bitmap: bit i of word i/32 = logical row i qualifies (row-linear);
  *  - seg_counts: hits per warp segment of seg_rows rows (set by the scan), OR-ed with
  *    ESC_SEG_CAPTURED when the segment was sparse enough (<= seg_rows/32 hits) for the scan to
- *    CAPTURE the hits' projected values into cap_values (cap_per_seg slots per segment), so the
- *    materialisation copies them instead of gathering rows from HBM again. */
+ *    CAPTURE the hits' projected values into cap_values (cap_per_seg slots per segment, stored
+ *    slot-major: hit j of segment s is entry j * cap_stride + s, so the compaction's reads of the
+ *    few slots sparse segments use are contiguous), and the materialisation copies them instead
+ *    of gathering rows from HBM again. */
 #define ESC_SEG_CAPTURED 0x80000000u
 typedef struct {
   uint32_t* bitmap;
@@ -247,7 +249,7 @@ typedef struct {
   int32_t seg_rows;     /* out: rows per segment                                  */
   int32_t cap_per_seg;  /* out: capture slots per segment (seg_rows / 32)         */
   int32_t n_cap;        /* in: captured projections (0 = none)                     */
-  int32_t pad;
+  int32_t cap_stride;   /* out: entries between a segment's consecutive slots      */
   int32_t cap_slot[ESC_MAX_PROJ];   /* in: column slot (of the scan's cols) per capture */
   void* cap_values[ESC_MAX_PROJ];   /* in: esc_selection_sizes().cap_entries values each */
   uint8_t* cap_nulls[ESC_MAX_PROJ]; /* in: null bytes per capture, or NULL                */

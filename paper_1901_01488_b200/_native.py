@@ -84,7 +84,7 @@ class EscOutputs(C.Structure):
 
 class EscSelection(C.Structure):
     _fields_ = [("bitmap", C.c_void_p), ("seg_counts", C.c_void_p), ("seg_rows", C.c_int32),
-                ("cap_per_seg", C.c_int32), ("n_cap", C.c_int32), ("pad", C.c_int32),
+                ("cap_per_seg", C.c_int32), ("n_cap", C.c_int32), ("cap_stride", C.c_int32),
                 ("cap_slot", C.c_int32 * MAX_PROJ), ("cap_values", C.c_void_p * MAX_PROJ),
                 ("cap_nulls", C.c_void_p * MAX_PROJ), ("d_count", C.c_void_p)]
 

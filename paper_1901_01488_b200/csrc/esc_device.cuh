@@ -594,10 +594,11 @@ __device__ __noinline__ uint32_t eval_direct(const KParams& p, const RowRef& rr,
 template <int C>
 __device__ __noinline__ void capture_generic(const KParams& p, const RowRef& rr, uint32_t bits, uint32_t excl,
                                              uint32_t wtp, int64_t seg) {
+  const size_t stride = (size_t)p.sel.cap_stride;  // slot-major: hit r of segment seg at r * stride + seg
   for (int k = 0; k < p.sel.n_cap; ++k) {
     const KCol& col = p.cols[p.sel.cap_slot[k]];
-    uint8_t* dst = static_cast<uint8_t*>(p.sel.cap_values[k]) + (size_t)seg * p.sel.cap_per_seg * col.width;
-    uint8_t* dn = p.sel.cap_nulls[k] ? p.sel.cap_nulls[k] + (size_t)seg * p.sel.cap_per_seg : nullptr;
+    uint8_t* dst = static_cast<uint8_t*>(p.sel.cap_values[k]) + (size_t)seg * col.width;
+    uint8_t* dn = p.sel.cap_nulls[k] ? p.sel.cap_nulls[k] + (size_t)seg : nullptr;
     uint32_t cb = 0;
     for (int c = 0; c < C; ++c) {
       uint32_t r = cb + ((excl >> (8 * c)) & 0xFFu);
@@ -607,15 +608,16 @@ __device__ __noinline__ void capture_generic(const KParams& p, const RowRef& rr,
         const int bit = 4 * c + __ffs(m) - 1;
         m &= m - 1;
         const uint8_t* src = value_ptr(col, rr, bit);
+        const size_t e = (size_t)r * stride;
         switch (col.width) {
-          case 1: dst[r] = *src; break;
-          case 2: reinterpret_cast<uint16_t*>(dst)[r] = *reinterpret_cast<const uint16_t*>(src); break;
-          case 4: reinterpret_cast<uint32_t*>(dst)[r] = *reinterpret_cast<const uint32_t*>(src); break;
+          case 1: dst[e] = *src; break;
+          case 2: reinterpret_cast<uint16_t*>(dst)[e] = *reinterpret_cast<const uint16_t*>(src); break;
+          case 4: reinterpret_cast<uint32_t*>(dst)[e] = *reinterpret_cast<const uint32_t*>(src); break;
           default:
-            reinterpret_cast<unsigned long long*>(dst)[r] = *reinterpret_cast<const unsigned long long*>(src);
+            reinterpret_cast<unsigned long long*>(dst)[e] = *reinterpret_cast<const unsigned long long*>(src);
             break;
         }
-        if (dn) dn[r] = is_null(col, rr, bit) ? 1 : 0;
+        if (dn) dn[e] = is_null(col, rr, bit) ? 1 : 0;
         ++r;
       }
     }
@@ -1356,6 +1358,7 @@ struct SelParams {
   int64_t n_segs;
   int32_t seg_rows;
   int32_t cap_per_seg;
+  int32_t cap_stride;                    // slot-major captures: entry = slot * cap_stride + segment
   int32_t n_proj;
   int32_t need_bitmap_captured;  // captured segments still need the bitmap (row ids / uncaptured columns)
   int32_t sparse_in_a;           // phase A also writes sparse segments (grids that fill the GPU)
@@ -1496,11 +1499,32 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
   const int R = p.a_split;
   const int r_log = __ffs(R) - 1;
   const int64_t n_units = ((p.n_segs + 31) >> 5) << r_log;
+  // a group's segment counts and offsets are loaded together, one group ahead (the offsets
+  // unconditionally: 256 contiguous bytes cost less than a second dependent round trip)
+  uint32_t raw_n = 0;
+  unsigned long long off_n = 0;
+  {
+    const int64_t sg = ((gwarp >> r_log) * 32) + lane;
+    if (gwarp < n_units && sg < p.n_segs) {
+      raw_n = __ldcg(p.seg_counts + sg);
+      off_n = __ldcg(p.seg_offsets + sg);
+    }
+  }
   for (int64_t u = gwarp; u < n_units; u += nwarps) {
     const int64_t seg0 = (u >> r_log) * 32;
     const int r = (int)(u & (R - 1));
     const int64_t myseg = seg0 + lane;
-    const uint32_t raw = myseg < p.n_segs ? p.seg_counts[myseg] : 0u;
+    const uint32_t raw = raw_n;
+    const unsigned long long off_l = off_n;
+    {
+      const int64_t un = u + nwarps, sg = ((un >> r_log) * 32) + lane;
+      raw_n = 0;
+      off_n = 0;
+      if (un < n_units && sg < p.n_segs) {
+        raw_n = __ldcg(p.seg_counts + sg);
+        off_n = __ldcg(p.seg_offsets + sg);
+      }
+    }
     uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
     if (p.rule.dense_min != 0xFFFFFFFFu) {
       uint32_t ts = cnt;  // hits of my stream tile (segments_per_tile consecutive lanes)
@@ -1510,7 +1534,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
     const bool captured = (raw & ESC_SEG_CAPTURED) != 0;
     const bool bitmap_work = cnt > 0 && (!captured || p.need_bitmap_captured);
     const bool dense_work = bitmap_work && cnt > sparse_max;
-    const unsigned long long myoff = (captured || dense_work) && cnt ? p.seg_offsets[myseg] : 0ull;
+    const unsigned long long myoff = off_l;
     // captured hits: the group's entries are spread over the lanes (lane e: entries e, e+32, ...
     // of the group's concatenated captured lists), four columns' loads in flight per entry
     {
@@ -1538,7 +1562,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
         const uint32_t idx = e - (s_incl - s_cnt);
         const unsigned long long pos = s_off + idx;
         if ((long long)pos >= cap) continue;
-        const size_t slot = (size_t)(seg0 + sl) * p.cap_per_seg + idx;
+        const size_t slot = (size_t)idx * p.cap_stride + (size_t)(seg0 + sl);
         for (int k0 = 0; k0 < p.n_proj; k0 += 4) {
           unsigned long long v[4];
           uint8_t nb[4];
@@ -1564,16 +1588,17 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
         }
       }
     }
-    if (p.sparse_in_a) {
+    const bool sparse_work = bitmap_work && cnt <= sparse_max;
+    if (p.sparse_in_a && __any_sync(0xFFFFFFFFu, sparse_work)) {
       // large selections: this warp's own sparse segments, C lanes per segment, one 128-row chunk
       // each (32 chunks in flight per round); small ones leave them to phase B's wider spread
-      const bool sparse_work = bitmap_work && cnt <= sparse_max;
-      const unsigned long long soff_l = sparse_work ? p.seg_offsets[myseg] : 0ull;
+      const unsigned long long soff_l = off_l;
       const int CPS = W / 4;
+      const int cps_log = __ffs(CPS) - 1;
       for (int b = 0; b < CPS; ++b) {
         const int c = b * 32 + lane;
-        const int sl = c / CPS;  // lane owning the chunk's segment
-        const int sub = c % CPS;
+        const int sl = c >> cps_log;  // lane owning the chunk's segment
+        const int sub = c & (CPS - 1);
         const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
         const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, soff_l, sl);
         const bool scap = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, sl) != 0;

@@ -340,7 +340,7 @@ void gen_capture(const KParams& kp, std::ostringstream& o) {
   }
   o << "    if (rr.stage == nullptr) { capture_generic<C>(p, rr, bits, excl, wtp, seg); return; }\n"
     << "    const uint8_t* st = rr.stage;\n"
-    << "    const size_t base = (size_t)seg * (4 * C);\n";
+    << "    const size_t base = (size_t)seg, stride = (size_t)p.sel.cap_stride;  // slot-major\n";
   for (int k = 0; k < ncap; ++k) {
     const KCol& c = kp.cols[kp.sel.cap_slot[k]];
     o << "    " << ctype_of(c.dtype) << "* cv" << k << " = static_cast<" << ctype_of(c.dtype) << "*>(p.sel.cap_values["
@@ -356,15 +356,15 @@ void gen_capture(const KParams& kp, std::ostringstream& o) {
     const int slot = kp.sel.cap_slot[k];
     const KCol& c = kp.cols[slot];
     if (c.staged)
-      o << "        cv" << k << "[r] = *reinterpret_cast<const " << ctype_of(c.dtype) << "*>(st + " << c.smem_off
+      o << "        cv" << k << "[(size_t)r * stride] = *reinterpret_cast<const " << ctype_of(c.dtype) << "*>(st + " << c.smem_off
         << "u + (size_t)lr * " << c.width << ");\n";
     else
-      o << "        cv" << k << "[r] = *reinterpret_cast<const " << ctype_of(c.dtype) << "*>(value_ptr(p.cols[" << slot
+      o << "        cv" << k << "[(size_t)r * stride] = *reinterpret_cast<const " << ctype_of(c.dtype) << "*>(value_ptr(p.cols[" << slot
         << "], rr, 4 * c + j));\n";
     if (kp.sel.cap_nulls[k] != nullptr) {
-      if (c.nulls == nullptr) o << "        cn" << k << "[r] = 0;\n";
-      else if (c.nulls_staged) o << "        cn" << k << "[r] = st[" << c.smem_null_off << "u + lr];\n";
-      else o << "        cn" << k << "[r] = is_null(p.cols[" << slot << "], rr, 4 * c + j) ? 1 : 0;\n";
+      if (c.nulls == nullptr) o << "        cn" << k << "[(size_t)r * stride] = 0;\n";
+      else if (c.nulls_staged) o << "        cn" << k << "[(size_t)r * stride] = st[" << c.smem_null_off << "u + lr];\n";
+      else o << "        cn" << k << "[(size_t)r * stride] = is_null(p.cols[" << slot << "], rr, 4 * c + j) ? 1 : 0;\n";
     }
   }
   o << "        ++r;\n      }\n    }\n  }\n";

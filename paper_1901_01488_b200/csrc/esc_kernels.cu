@@ -742,6 +742,7 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   sp.nrows = nrows;
   sp.seg_rows = sel->seg_rows;
   sp.cap_per_seg = sel->cap_per_seg;
+  sp.cap_stride = sel->cap_stride;
   // segments cover whole tiles: tile = kConsumerWarps segments
   const int64_t tile_rows = (int64_t)sel->seg_rows * kConsumerWarps;
   sp.n_segs = ((nrows + tile_rows - 1) / tile_rows) * kConsumerWarps;
@@ -821,7 +822,14 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   sp.sparse_in_a = groups_ctas >= 4LL * sms ? 1 : 0;
   const int64_t chunks = sp.n_segs * (sp.seg_rows / kChunkRows);
   const int64_t want = sp.sparse_in_a ? groups_ctas : (chunks + 32 * kSelWarps - 1) / (32 * kSelWarps);
-  M->compact_grid = (unsigned)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
+  // one wave of resident CTAs: warps loop over groups with the next group's loads in flight
+  static const int resident = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sel_compact_kernel, kSelWarps * 32, 0);
+    return b > 0 ? b : 4;
+  }();
+  const int64_t cap_grid = (int64_t)sms * resident;
+  M->compact_grid = (unsigned)(want < cap_grid ? want : cap_grid);
   sp.a_split = 1;
   if (!sp.sparse_in_a) {
     const int64_t groups = (sp.n_segs + 31) / 32, warps = (int64_t)M->compact_grid * kSelWarps;
@@ -905,6 +913,9 @@ int prepare_select(KParams& kp, const esc_program_t* prog, const esc_column_t* c
   sel->seg_rows = kChunkRows * kp.chunks;
   sel->cap_per_seg = 4 * kp.chunks;  // segments with <= 4*C hits (~3% of 128*C rows) are captured
   if (kp.chunks > 4) sel->cap_per_seg = 0;  // (no capture with C = 8 tiles)
+  const int64_t n_segs = kp.n_tiles * kConsumerWarps;
+  if (n_segs > INT32_MAX) sel->cap_per_seg = 0;  // slot-major index would overflow the stride
+  sel->cap_stride = (int32_t)(n_segs > INT32_MAX ? 0 : n_segs);
   kp.sel_on = 1;
   kp.sel = *sel;
   return ESC_OK;
