@@ -559,7 +559,7 @@ int prepare_c(const KParams& kp, ScanLaunch* L) {
   L->grid = (unsigned)grid;
   L->block = Layout<COMPACT>::kThreads;
   L->smem = smem;
-  L->coop = COMPACT && getenv("ESC_NO_COOP") == nullptr;  // the one-pass look-back relies on every CTA being resident
+  L->coop = COMPACT;  // the one-pass look-back relies on every CTA being resident
   // JIT tier: large scans whose tiles run the fast (staged) evaluator
   const int mode = jit::g_mode.load();
   if (mode == 2 || (mode == 1 && kp.nrows >= jit::g_min_rows.load())) {
