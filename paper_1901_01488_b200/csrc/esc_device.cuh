@@ -108,6 +108,13 @@ struct KParams {
   unsigned long long* trace;  // diagnostics (esc_debug_trace): per-CTA %globaltimer stamps, or nullptr
 };
 
+// Programmatic dependent launch: the compaction chain's kernels are launched with
+// programmaticStreamSerialization, so each may be scheduled while its predecessor still runs; it
+// waits (griddepcontrol.wait) before touching anything the predecessor writes, and lets its own
+// dependents launch early.  Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -859,6 +866,7 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
   const int lane = threadIdx.x & 31;
   constexpr int kW = Layout<COMPACT>::kWriters;
 
+  pdl_trigger();  // every CTA is resident from the start: the compaction chain may queue behind
   if (threadIdx.x < kMaxStages) s_tsum[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     if (p.trace != nullptr) p.trace[blockIdx.x * 8] = gtimer();
@@ -1276,6 +1284,8 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_partials(const uint32_
                                                                    uint32_t* __restrict__ n_dense,
                                                                    const unsigned long long* skip_count,
                                                                    long long skip_capacity) {
+  pdl_wait();
+  pdl_trigger();
   const bool skip = skip_count != nullptr && (long long)*skip_count > skip_capacity;
   __shared__ unsigned long long sh[33];
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_dense = 0;
@@ -1297,6 +1307,8 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* 
                                                                 const DenseRule rule) {
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long carry;
+  pdl_wait();
+  pdl_trigger();
   if (skip_materialize(rule)) return;
   if (threadIdx.x < 32) {  // one warp sums the earlier blocks' partials (independent loads in flight)
     unsigned long long c = 0;
@@ -1485,6 +1497,8 @@ __device__ __forceinline__ bool in_dense_tile(const SelParams& p, int64_t seg) {
 }
 
 __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1793,6 +1807,8 @@ __device__ __forceinline__ void stream_words(const StreamParams& p, const uint8_
 
 __global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_kernel(const __grid_constant__ StreamParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  pdl_wait();
+  pdl_trigger();
   const int S = p.stages;
   uint8_t* ring = smem;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);

@@ -39,6 +39,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <utility>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -838,21 +839,36 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   return ESC_OK;
 }
 
+// launch with programmatic stream serialization (the kernel waits for its predecessor itself)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ++g_launches;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 int issue_mat(const MatLaunch& M, cudaStream_t st) {
   if (M.empty) return ESC_OK;
   const SelParams& sp = M.sp;
-  ++g_launches;
-  tile_scan_partials<<<M.segs, kScanThreads, 0, st>>>(M.seg_counts, sp.n_segs, M.partials, sp.rule.n_dense,
-                                                       sp.rule.skip_count, sp.rule.skip_capacity);
-  ++g_launches;
-  tile_scan_apply<<<M.segs, kScanThreads, 0, st>>>(M.seg_counts, sp.n_segs, M.partials, M.offsets, sp.rule);
-  if (M.streaming) {
-    ++g_launches;
-    sel_stream_kernel<<<M.stream_grid, (1 + kStreamConsumers) * 32, M.stream_smem, st>>>(M.tp);
-  }
-  ++g_launches;
-  sel_compact_kernel<<<M.compact_grid, kSelWarps * 32, 0, st>>>(sp);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(tile_scan_partials, M.segs, kScanThreads, 0, st, M.seg_counts, sp.n_segs, M.partials,
+                             sp.rule.n_dense, sp.rule.skip_count, sp.rule.skip_capacity);
+  if (e == cudaSuccess)
+    e = launch_pdl(tile_scan_apply, M.segs, kScanThreads, 0, st, M.seg_counts, sp.n_segs,
+                   static_cast<const unsigned long long*>(M.partials), M.offsets, sp.rule);
+  if (e == cudaSuccess && M.streaming)
+    e = launch_pdl(sel_stream_kernel, M.stream_grid, (1 + kStreamConsumers) * 32, M.stream_smem, st, M.tp);
+  if (e == cudaSuccess) e = launch_pdl(sel_compact_kernel, M.compact_grid, kSelWarps * 32, 0, st, sp);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("selection compaction launch: ") + cudaGetErrorString(e));
   return ESC_OK;
 }
