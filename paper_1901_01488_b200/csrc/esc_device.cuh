@@ -106,6 +106,7 @@ struct KParams {
   esc_selection_t sel;
   uint32_t rows_off;     // stage offset of the u16 row-index scratch (row-id outputs)
   unsigned long long* trace;  // diagnostics (esc_debug_trace): per-CTA %globaltimer stamps, or nullptr
+  int32_t ticket_tiles;       // K1: consecutive tiles per ticket (>= ~128 KB of staged data per ticket)
 };
 
 // Programmatic dependent launch: the compaction chain's kernels are launched with
@@ -893,8 +894,12 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
       // so the atomic's latency hides behind the ring wait): a CTA that DRAM serves late at the
       // start (first tiles arrive 2-120 us apart across CTAs) takes fewer tiles instead of
       // finishing last (600M rows: the static schedule's last CTA ended 37 us after the median)
-      int64_t tile = blockIdx.x;
-      int64_t next = COMPACT ? 0 : (int64_t)atomicAdd(&p.hdr->ticket, 1ull) + gridDim.x;
+      // K1 tickets cover ticket_tiles consecutive tiles (small tiles would otherwise wait on the
+      // atomic's round trip): batch b = tiles [b*kb, (b+1)*kb); CTA i starts with batch i
+      const int64_t kb = COMPACT ? 1 : p.ticket_tiles;
+      int64_t tile = COMPACT ? blockIdx.x : blockIdx.x * kb;
+      int64_t batch_end = tile + kb;
+      int64_t next = COMPACT ? 0 : ((int64_t)atomicAdd(&p.hdr->ticket, 1ull) + gridDim.x) * kb;
       int s = 0;
       uint32_t ph = 0;
       int sentinels = 0;
@@ -956,8 +961,11 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
         if (COMPACT) {
           tile += gridDim.x;
         } else {
-          tile = next;
-          if (tile < p.n_tiles) next = (int64_t)atomicAdd(&p.hdr->ticket, 1ull) + gridDim.x;
+          if (++tile >= batch_end) {
+            tile = next;
+            batch_end = tile + kb;
+            if (tile < p.n_tiles) next = ((int64_t)atomicAdd(&p.hdr->ticket, 1ull) + gridDim.x) * kb;
+          }
         }
       }
       if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 3] = gtimer();

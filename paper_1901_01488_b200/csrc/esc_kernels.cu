@@ -506,6 +506,14 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
   kp.tma_bytes = g.tma_bytes;
   kp.n_tiles = (nrows + g.tile_rows - 1) / g.tile_rows;
   kp.n_full_tiles = (g.tma_bytes == 0) ? 0 : nrows / g.tile_rows;
+  {  // K1 tile tickets: >= 128 KB of staged data per ticket, at most 8 tiles
+    const int64_t per = g.tma_bytes > 0 ? g.tma_bytes : (int64_t)g.tile_rows * 4;
+    int64_t kb = (131072 + per - 1) / per;
+    const int sms = sm_count_cached() > 0 ? sm_count_cached() : 148;
+    const int64_t spread = kp.n_tiles / (2 * (int64_t)sms);  // small scans keep one tile per ticket
+    if (kb > spread) kb = spread;
+    kp.ticket_tiles = (int32_t)(kb < 1 ? 1 : (kb > 8 ? 8 : kb));
+  }
   rc = lower_program(prog, kp);
   if (rc != ESC_OK) return rc;
   // smem offsets into the lowered instructions; fast evaluation needs every program column staged
