@@ -314,6 +314,23 @@ int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const 
  * (executor.py:304-325). */
 int esc_hash_insert(const int64_t* unique_keys, int64_t n_unique, int64_t* slots, int64_t capacity, void* stream);
 
+/* The grouping half of a hash build (replaces np.unique + the stable argsort of
+ * HashTableIndex.__init__, executor.py:275-303): the build rows' keys (rows[i], or i when rows is
+ * NULL; NULL keys already excluded by the caller) are sorted stably, so out_group_rows holds the
+ * rows grouped by ascending key, each group in ascending row order; out_unique_keys[0..u) the
+ * keys, out_group_counts[0..u) their sizes, out_group_start[0..u] the exclusive offsets, and the
+ * device words out_stats[0..3] = {u, min key, max key, largest group} (read after a stream sync;
+ * many builds can share one).  out_group_counts and out_group_start hold n + 1 entries. */
+int esc_hash_build_temp_bytes(int64_t n, size_t* bytes);
+/* A star step's dense factor array over keys lo .. lo+span-1 (out_bytes >= span*bits/8, zeroed
+ * here): bits = 1 sets bit (key - lo) of every group's key (primary-key dimensions), 8/16/32/64
+ * store the group's size there (esc_join_step_t.factor / factor_bits). */
+int esc_factor_array(const int64_t* unique_keys, const int64_t* counts, int64_t u, int64_t lo, int64_t span,
+                     int32_t bits, void* out, size_t out_bytes, void* stream);
+int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int64_t n, int64_t* out_group_rows,
+                   int64_t* out_unique_keys, int64_t* out_group_counts, int64_t* out_group_start, int64_t* out_stats,
+                   void* d_temp, size_t temp_bytes, void* stream);
+
 /* out_groups[i] = g with unique_keys[g] == key(i), else -1 (absent, NULL key or !valid[i]).
  * key(i) = keys[rows ? rows[i] : i] at native integer width key_dtype; key_nulls (bool mask
  * indexed like keys), rows and valid (bool per i) are optional.  replaces

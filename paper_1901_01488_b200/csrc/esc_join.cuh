@@ -457,12 +457,194 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_quad_kernel(const __grid
   }
 }
 
+// ---- hash build grouping (esc_hash_build) ----------------------------------------------------
+__global__ void build_gather_kernel(const uint8_t* __restrict__ keys, int dtype, int width,
+                                    const int64_t* __restrict__ rows, int64_t n, long long* __restrict__ out_keys,
+                                    int64_t* __restrict__ out_rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows ? rows[i] : i;
+    out_keys[i] = ld_int(keys + (size_t)r * width, dtype);
+    out_rows[i] = r;
+  }
+}
+
+__global__ void build_stats_kernel(const long long* __restrict__ unique_keys, const long long* __restrict__ num_runs,
+                                   const long long* __restrict__ max_count, int64_t* __restrict__ stats) {
+  const long long u = *num_runs;
+  stats[0] = u;
+  stats[1] = u > 0 ? unique_keys[0] : 0;
+  stats[2] = u > 0 ? unique_keys[u - 1] : 0;
+  stats[3] = *max_count;
+}
+
+// dense factor array of a star step: bit / count of every key's group at key - lo
+__global__ void factor_array_kernel(const long long* __restrict__ unique_keys, const long long* __restrict__ counts,
+                                    int64_t u, long long lo, int bits, uint8_t* __restrict__ out) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < u; g += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long i = (unsigned long long)(unique_keys[g] - lo);
+    const long long c = counts[g];
+    switch (bits) {
+      case 1: atomicOr(reinterpret_cast<unsigned int*>(out) + (i >> 5), 1u << (i & 31)); break;
+      case 8: out[i] = (uint8_t)c; break;
+      case 16: reinterpret_cast<uint16_t*>(out)[i] = (uint16_t)c; break;
+      case 32: reinterpret_cast<uint32_t*>(out)[i] = (uint32_t)c; break;
+      default: reinterpret_cast<unsigned long long*>(out)[i] = (unsigned long long)c; break;
+    }
+  }
+}
+
+struct BuildTemp {  // esc_hash_build's scratch: intermediate arrays + the largest CUB temp need
+  size_t keys_in, rows_in, keys_sorted, num_runs, max_count, cub, total;
+  size_t cub_bytes;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline int build_temp_layout_q(int64_t n, BuildTemp* T);
+
+// CUB's temp-size queries cost host time per call: layouts are memoised per power-of-two size
+// class (the sizes grow with n, so the class's largest n covers every n in it)
+inline int build_temp_layout(int64_t n, BuildTemp* T) {
+  int64_t cls = 1024;
+  while (cls < n) cls <<= 1;
+  static std::mutex mu;
+  static std::unordered_map<int64_t, BuildTemp> memo;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = memo.find(cls);
+    if (it != memo.end()) {
+      *T = it->second;
+      return ESC_OK;
+    }
+  }
+  const int rc = build_temp_layout_q(cls, T);
+  if (rc == ESC_OK) {
+    std::lock_guard<std::mutex> g(mu);
+    memo[cls] = *T;
+  }
+  return rc;
+}
+
+inline int build_temp_layout_q(int64_t n, BuildTemp* T) {
+  size_t a = 0, b = 0, c = 0, d = 0;
+  const int nn = (int)n;
+  if (cub::DeviceRadixSort::SortPairs(nullptr, a, (const long long*)nullptr, (long long*)nullptr,
+                                      (const int64_t*)nullptr, (int64_t*)nullptr, nn) != cudaSuccess ||
+      cub::DeviceRunLengthEncode::Encode(nullptr, b, (const long long*)nullptr, (long long*)nullptr,
+                                         (long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess ||
+      cub::DeviceScan::ExclusiveSum(nullptr, c, (const long long*)nullptr, (long long*)nullptr, nn + 1) != cudaSuccess ||
+      cub::DeviceReduce::Max(nullptr, d, (const long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess)
+    return fail(ESC_ERR_CUDA, "CUB temp-size query failed");
+  T->cub_bytes = std::max(std::max(a, b), std::max(c, d));
+  size_t off = 0;
+  T->keys_in = off;     off += align256((size_t)n * 8);
+  T->rows_in = off;     off += align256((size_t)n * 8);
+  T->keys_sorted = off; off += align256((size_t)n * 8);
+  T->num_runs = off;    off += 256;
+  T->max_count = off;   off += 256;
+  T->cub = off;         off += align256(T->cub_bytes);
+  T->total = off;
+  return ESC_OK;
+}
+
 }  // namespace esc
 
 // ==========================================================================================
 // C ABI (joins)
 // ==========================================================================================
 extern "C" {
+
+int esc_factor_array(const int64_t* unique_keys, const int64_t* counts, int64_t u, int64_t lo, int64_t span,
+                     int32_t bits, void* out, size_t out_bytes, void* stream) {
+  if (u < 0 || span < 0 || (bits != 1 && bits != 8 && bits != 16 && bits != 32 && bits != 64))
+    return fail(ESC_ERR_INVALID, "bad factor array arguments");
+  if ((size_t)((span * bits + 7) / 8) > out_bytes) return fail(ESC_ERR_INVALID, "factor array buffer too small");
+  if (out == nullptr || (u > 0 && (unique_keys == nullptr || counts == nullptr)))
+    return fail(ESC_ERR_INVALID, "null factor array buffers");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(out, 0, out_bytes, st);
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("factor array init: ") + cudaGetErrorString(e));
+  if (u == 0) return ESC_OK;
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  int64_t blocks = (u + 255) / 256;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  ++g_launches;
+  esc::factor_array_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const long long*>(unique_keys),
+                                                             reinterpret_cast<const long long*>(counts), u, lo, bits,
+                                                             static_cast<uint8_t*>(out));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("factor array launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
+int esc_hash_build_temp_bytes(int64_t n, size_t* bytes) {
+  if (bytes == nullptr || n < 0 || n >= (1ll << 31)) return fail(ESC_ERR_INVALID, "bad hash build size");
+  esc::BuildTemp T;
+  const int rc = esc::build_temp_layout(n, &T);
+  if (rc == ESC_OK) *bytes = T.total;
+  return rc;
+}
+
+int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int64_t n, int64_t* out_group_rows,
+                   int64_t* out_unique_keys, int64_t* out_group_counts, int64_t* out_group_start, int64_t* out_stats,
+                   void* d_temp, size_t temp_bytes, void* stream) {
+  if (n < 0 || n >= (1ll << 31)) return fail(ESC_ERR_INVALID, "bad hash build size");
+  if (key_dtype == ESC_F32 || key_dtype == ESC_F64 || dtype_width(key_dtype) == 0)
+    return fail(ESC_ERR_UNSUPPORTED, "hash keys must be integer columns");
+  if (out_stats == nullptr || out_group_start == nullptr || out_group_counts == nullptr ||
+      (n > 0 && (keys == nullptr || out_group_rows == nullptr || out_unique_keys == nullptr || d_temp == nullptr)))
+    return fail(ESC_ERR_INVALID, "null hash build buffers");
+  esc::BuildTemp T;
+  int rc = esc::build_temp_layout(n, &T);
+  if (rc != ESC_OK) return rc;
+  if (n > 0 && temp_bytes < T.total) return fail(ESC_ERR_WORKSPACE, "hash build temp too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* t = static_cast<uint8_t*>(d_temp);
+  // counts are zeroed first: the scan and the max read past the u runs the encoder writes
+  cudaError_t e = cudaMemsetAsync(out_group_counts, 0, (size_t)(n + 1) * sizeof(int64_t), st);
+  if (e == cudaSuccess && n == 0) e = cudaMemsetAsync(out_stats, 0, 4 * sizeof(int64_t), st);
+  if (e == cudaSuccess && n == 0) e = cudaMemsetAsync(out_group_start, 0, sizeof(int64_t), st);
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash build init: ") + cudaGetErrorString(e));
+  if (n == 0) return ESC_OK;
+  long long* keys_in = reinterpret_cast<long long*>(t + T.keys_in);
+  int64_t* rows_in = reinterpret_cast<int64_t*>(t + T.rows_in);
+  long long* keys_sorted = reinterpret_cast<long long*>(t + T.keys_sorted);
+  long long* num_runs = reinterpret_cast<long long*>(t + T.num_runs);
+  long long* max_count = reinterpret_cast<long long*>(t + T.max_count);
+  void* cub_tmp = t + T.cub;
+  size_t cub_bytes = T.cub_bytes;
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  ++g_launches;
+  esc::build_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(keys), key_dtype,
+                                                             dtype_width(key_dtype), rows, n, keys_in, rows_in);
+  // stable (LSD radix) sort by key: equal keys keep ascending build-row order, as the
+  // reference's stable argsort; then runs = groups in ascending key order
+  const int nn = (int)n;
+  g_launches += 4;
+  e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys_in, keys_sorted, rows_in, out_group_rows, nn, 0,
+                                      64, st);
+  if (e == cudaSuccess)
+    e = cub::DeviceRunLengthEncode::Encode(cub_tmp, cub_bytes, keys_sorted,
+                                           reinterpret_cast<long long*>(out_unique_keys),
+                                           reinterpret_cast<long long*>(out_group_counts), num_runs, nn, st);
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, reinterpret_cast<const long long*>(out_group_counts),
+                                      reinterpret_cast<long long*>(out_group_start), nn + 1, st);
+  if (e == cudaSuccess)
+    e = cub::DeviceReduce::Max(cub_tmp, cub_bytes, reinterpret_cast<const long long*>(out_group_counts), max_count,
+                               nn, st);
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash build: ") + cudaGetErrorString(e));
+  ++g_launches;
+  esc::build_stats_kernel<<<1, 1, 0, st>>>(reinterpret_cast<const long long*>(out_unique_keys), num_runs, max_count,
+                                           out_stats);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash build stats: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
 
 int esc_hash_insert(const int64_t* unique_keys, int64_t n_unique, int64_t* slots, int64_t capacity, void* stream) {
   if (capacity <= 0 || (capacity & (capacity - 1)) != 0) return fail(ESC_ERR_INVALID, "capacity must be a power of two");

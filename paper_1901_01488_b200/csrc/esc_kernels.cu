@@ -25,6 +25,10 @@
 // Tiles that are not staged (tail tile, row-id selections, unaligned columns) run a separate,
 // cold, bounds-checked evaluator.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
 #include <dlfcn.h>
 #include <nvrtc.h>
 

@@ -70,34 +70,56 @@ class HashTableIndex:
     ``executor.py:275-350``): slots hold ids of key groups; a group's row indices sit contiguously,
     ascending, in ``group_rows``.  All arrays are device tensors."""
 
-    def __init__(self, table: ColumnTable, key: str, rows: torch.Tensor):
+    def __init__(self, table: ColumnTable, key: str, rows: torch.Tensor | None, _defer: bool = False):
+        """``rows``: build-row ids (None = every row).  The grouping (stable sort by key, runs,
+        offsets) is one ``esc_hash_build`` call; its statistics (distinct keys, key range,
+        largest group) stay on the device until :meth:`_finish` reads them — ``build_indexes``
+        reads every build of a plan at once."""
         self.table = table
         self.key = key
         col = table.column(key)
         if col.values.dtype in _FLOAT_DTYPES:
             raise ExecutionError(f"cannot hash-join on floating-point column {key!r}")
         dev = table.device
-        rows = rows.to(device=dev, dtype=torch.int64)
-        if col.nulls is not None and rows.numel():
-            rows = rows[~col.nulls[rows]]
-        self.n_entries = int(rows.numel())
-        keys = executor.take_column(col, rows).values.to(torch.int64) if self.n_entries else \
-            torch.empty(0, dtype=torch.int64, device=dev)
-        # stable: equal keys keep ascending row order (np.unique + stable argsort of the reference)
-        sorted_keys, perm = torch.sort(keys, stable=True)
-        self.group_rows = rows[perm]
-        if self.n_entries:
-            self.unique_keys, counts = torch.unique_consecutive(sorted_keys, return_counts=True)
-        else:
-            self.unique_keys, counts = sorted_keys, torch.empty(0, dtype=torch.int64, device=dev)
-        self.group_counts = counts.to(torch.int64)
-        self.group_start = torch.zeros(self.unique_keys.numel() + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(self.group_counts, 0, out=self.group_start[1:])
-        self.capacity = capacity_for(int(self.unique_keys.numel()))
+        if rows is not None:
+            rows = rows.to(device=dev, dtype=torch.int64).contiguous()
+        if col.nulls is not None and len(col):  # NULL keys never match: drop them first
+            rows = torch.arange(len(col), device=dev) if rows is None else rows
+            if rows.numel():
+                rows = rows[~col.nulls[rows]].contiguous()
+        n = len(col) if rows is None else int(rows.numel())
+        self.n_entries = n
+        lib = N.load_library()
+        temp_bytes = C.c_size_t()
+        N.check(lib.esc_hash_build_temp_bytes(n, C.byref(temp_bytes)), "esc_hash_build_temp_bytes")
+        temp = torch.empty(max(temp_bytes.value, 1), dtype=torch.uint8, device=dev)
+        self.group_rows = torch.empty(n, dtype=torch.int64, device=dev)
+        self._uk = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        self._cnt = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self._start = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self._stats = torch.empty(4, dtype=torch.int64, device=dev)
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None and t.numel() else None  # noqa: E731
+        N.check(lib.esc_hash_build(ptr(col.values), N.dtype_code(col.values), ptr(rows), n, ptr(self.group_rows),
+                                   ptr(self._uk), ptr(self._cnt), ptr(self._start), ptr(self._stats), ptr(temp),
+                                   temp_bytes.value, C.c_void_p(_stream(dev).cuda_stream)), "esc_hash_build")
+        self._temp = temp  # alive until the queued kernels ran (freed in _finish, stream-ordered)
+        if not _defer:
+            self._finish(self._stats.tolist())
+
+    def _finish(self, stats):
+        """Second half of the build once (distinct, min, max, largest group) are on the host."""
+        dev = self.table.device
+        u, lo, hi, most = (int(x) for x in stats)
+        self.key_range = (lo, hi, most) if u else None
+        self.unique_keys = self._uk[:u]
+        self.group_counts = self._cnt[:u]
+        self.group_start = self._start[: u + 1]
+        self._temp = self._stats = None
+        self.capacity = capacity_for(u)
         self.slots = torch.empty(self.capacity, dtype=torch.int64, device=dev)
         lib = N.load_library()
-        N.check(lib.esc_hash_insert(C.c_void_p(self.unique_keys.data_ptr()) if self.unique_keys.numel() else None,
-                                    int(self.unique_keys.numel()), C.c_void_p(self.slots.data_ptr()), self.capacity,
+        N.check(lib.esc_hash_insert(C.c_void_p(self.unique_keys.data_ptr()) if u else None, u,
+                                    C.c_void_p(self.slots.data_ptr()), self.capacity,
                                     C.c_void_p(_stream(dev).cuda_stream)), "esc_hash_insert")
 
     @property
@@ -150,8 +172,18 @@ class HashTableIndex:
 def build_hash(table: ColumnTable, key: str, residual: ex.Expr | None = None) -> HashTableIndex:
     """Hash index over rows passing ``residual`` (NULL keys excluded) — reference
     ``executor.py:353-358``; the rows come from the K1 scan on the device."""
-    rows = executor.eval_predicate(table, residual).to_indices()
-    return HashTableIndex(table, key, rows)
+    return HashTableIndex(table, key, executor.eval_predicate(table, residual).indices)
+
+
+def build_indexes(specs) -> list:
+    """``build_hash`` for several (table, key, residual): every build's grouping is queued, then
+    ONE host read of all their statistics finishes them (a plan's builds wait once together)."""
+    idx = [HashTableIndex(t, k, executor.eval_predicate(t, r).indices, _defer=True) for t, k, r in specs]
+    if idx:
+        vals = torch.stack([i._stats for i in idx]).tolist()
+        for i, v in zip(idx, vals):
+            i._finish(v)
+    return idx
 
 
 @dataclass
@@ -196,26 +228,28 @@ def _factor_array(index: HashTableIndex):
     u = index.distinct_keys
     if u == 0:
         return None
-    lo, hi = int(index.unique_keys[0]), int(index.unique_keys[-1])
+    lo, hi, most = index.key_range  # read with the build's statistics (no extra wait)
     span = hi - lo + 1
-    most = int(index.group_counts.max())
     bits = 1 if most <= 1 else 8 if most < 256 else 16 if most < 65536 else 32 if most < (1 << 32) else 64
     nbytes = span * bits // 8
     hash_bytes = index.capacity * 8 + u * 16
     if span > DENSE_SPAN_MAX or nbytes > max(DENSE_MAX_BYTES, DENSE_VS_HASH * hash_bytes):
         return None
     dev = index.table.device
-    idx = index.unique_keys - lo
+    # padded to 16 bytes (the probe kernels stage it with 16-byte copies); one native launch
     if most <= 1:
-        words = torch.zeros(((span + 31) // 32 + 3) // 4 * 4, dtype=torch.int64, device=dev)
-        words.scatter_add_(0, idx >> 5, torch.ones_like(idx) << (idx & 31))
-        return lo, span, words.to(torch.int32), 1
-    for bits, dt in ((8, torch.uint8), (16, torch.int16), (32, torch.int32), (64, torch.int64)):
-        if most < (1 << bits) or bits == 64:
-            pad = (16 * 8 // bits)
-            arr = torch.zeros((span + pad - 1) // pad * pad, dtype=torch.int64, device=dev)
-            arr[idx] = index.group_counts
-            return lo, span, arr.to(dt), bits
+        bits, dt, n_el = 1, torch.int32, ((span + 31) // 32 + 3) // 4 * 4
+    else:
+        bits, dt = next((b, d) for b, d in ((8, torch.uint8), (16, torch.int16), (32, torch.int32), (64, torch.int64))
+                        if most < (1 << b) or b == 64)
+        pad = 16 * 8 // bits
+        n_el = (span + pad - 1) // pad * pad
+    arr = torch.empty(n_el, dtype=dt, device=dev)
+    N.check(N.load_library().esc_factor_array(C.c_void_p(index.unique_keys.data_ptr()),
+                                              C.c_void_p(index.group_counts.data_ptr()), u, lo, span, bits,
+                                              C.c_void_p(arr.data_ptr()), arr.numel() * arr.element_size(),
+                                              C.c_void_p(_stream(dev).cuda_stream)), "esc_factor_array")
+    return lo, span, arr, bits
 
 
 def _stage_weights(steps: list, probe_alias: str) -> dict:
@@ -377,13 +411,15 @@ def execute_plan(plan_, catalog, workers: int = 1):
     """Run the pipeline of a PhysicalPlan; returns (result table or None, result count, stats)
     — reference ``optimizer.py:403-430``.  Pushed-down builds read their ESC temps in place."""
     probe_table = catalog.table(plan_.probe_source)
-    steps, build_ms = [], []
+    specs = []
     for b in plan_.builds:
         table = catalog.resolve_temp(b.source) if isinstance(b.source, TempTableHandle) else catalog.table(b.source)
-        t0 = time.perf_counter()
-        index = build_hash(table, b.build_key.name, b.residual)
-        build_ms.append((time.perf_counter() - t0) * 1000.0)
-        steps.append(BuildStep(b.alias, index, b.probe_key))
+        specs.append((table, b.build_key.name, b.residual))
+    t0 = time.perf_counter()
+    indexes = build_indexes(specs)  # the builds share one host wait; their time is split evenly
+    share = (time.perf_counter() - t0) * 1000.0 / max(len(specs), 1)
+    build_ms = [share] * len(specs)
+    steps = [BuildStep(b.alias, index, b.probe_key) for b, index in zip(plan_.builds, indexes)]
     result, stats = probe_joins(probe_table, plan_.probe_alias, plan_.probe_pred, steps, plan_.projection,
                                 workers=workers)
     stats.build_ms = build_ms

@@ -135,4 +135,10 @@ def test_join_csv_plan_entry_points_validate_arguments(native_lib):
         "null outputs")  # sel == NULL asks for the one-pass plan, which needs outputs
     assert h.value is None
     err(native_lib.esc_step_plan_rebind(None, None), "null plan or outputs")
+    nb = C.c_size_t()
+    err(native_lib.esc_hash_build_temp_bytes(-1, C.byref(nb)), "bad hash build size")
+    err(native_lib.esc_hash_build(None, 4, None, 10, None, None, None, None, None, None, 0, None), "integer")
+    err(native_lib.esc_hash_build(None, 2, None, 10, None, None, None, None, None, None, 0, None), "null hash build")
+    err(native_lib.esc_factor_array(None, None, 1, 0, 8, 3, None, 0, None), "bad factor array")
+    err(native_lib.esc_factor_array(None, None, 1, 0, 64, 8, None, 16, None), "too small")
     assert native_lib.esc_csv_workspace_bytes(1 << 30) > native_lib.esc_csv_workspace_bytes(1 << 10)
