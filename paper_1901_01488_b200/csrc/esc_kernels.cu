@@ -450,6 +450,7 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
   } else {
     g.stages = (int)(kSmemBudget / off);
     if (g.stages > kMaxStages) g.stages = kMaxStages;
+    const int max_stages = g.stages;
     // ~96 KB of TMA in flight per SM (at least 3 stages) streams best: a 1-column int32 scan
     // (32 KB stages) runs at 5.9 TB/s with 3 stages and 5.4 TB/s with 6 (tools/stage_sweep.py)
     {
@@ -459,7 +460,7 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     }
     if (const char* e = getenv("ESC_STAGES")) {  // tuning override (experiments only)
       const int v = atoi(e);
-      if (v >= 1 && v < g.stages) g.stages = v;
+      if (v >= 1 && v <= max_stages) g.stages = v;
     }
     if (g.stages < 1) g.stages = 1;
   }
