@@ -286,8 +286,12 @@ def _encode_text(data, d_bytes, field_end, field_kind, first_field, nrows, ncols
     words = []
     if vrows.numel():
         uniq, inverse = torch.unique(hashes[valid], return_inverse=True)
-        first = torch.full((uniq.numel(),), nrows, dtype=torch.int64, device=dev)
-        first.scatter_reduce_(0, inverse, vrows, reduce="amin")
+        # first appearance = the first row of each group after a stable sort by group (an
+        # atomic-min scatter serialised on the few hot groups of a low-cardinality column:
+        # 549 us for 1M rows of 6 strings, ncu)
+        counts = torch.bincount(inverse, minlength=uniq.numel())
+        starts = torch.cumsum(counts, 0) - counts
+        first = vrows[torch.argsort(inverse, stable=True)[starts]]
         order = torch.argsort(first)
         code_of = torch.empty_like(order)
         code_of[order] = torch.arange(order.numel(), device=dev)
