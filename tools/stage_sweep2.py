@@ -35,7 +35,11 @@ print("RESULT", out)
 '''
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 600_000_000
 res = []
-for c, s in [(None, None), ("4", "2"), ("4", "3"), ("2", "3"), ("2", "4"), ("2", "6"), ("1", "6"), ("1", "8"), ("1", "12"), ("8", "3"), ("8", "4"), ("8", "6")]:
+combos = [(None, None), ("4", "2"), ("4", "3"), ("2", "3"), ("2", "4"), ("2", "6"), ("1", "6"), ("1", "8"), ("1", "12"),
+          ("8", "3"), ("8", "4"), ("8", "6")]
+if len(sys.argv) > 2:  # a quick run: the default geometry only
+    combos = combos[:1]
+for c, s in combos:
     env = dict(os.environ)
     if c: env["ESC_CHUNKS"] = c
     if s: env["ESC_STAGES"] = s
