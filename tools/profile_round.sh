@@ -5,6 +5,8 @@ set -u
 mkdir -p gpurun_out/prof
 B="python bench.py --steps 2 --warmup 1 --no-extras --no-e2e --no-cpu-baseline"
 N="ncu --set full --clock-control none --import-source on"
+PART=${1:-1}   # two halves: gpurun copies back at most 64 MiB per call
+if [ "$PART" = 1 ]; then
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv \
     --log-file gpurun_out/prof/launches_config4.csv $B > gpurun_out/prof/launches.log 2>&1
 $N -k regex:esc_scan_kernel --launch-skip 1 --launch-count 1 -o gpurun_out/prof/k1_select_config4 $B > gpurun_out/prof/k1.log 2>&1
@@ -13,6 +15,7 @@ $N -k regex:esc_scan_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/prof/
     python tools/kprof_count.py > gpurun_out/prof/k1c.log 2>&1
 $N -k regex:sel_stream --launch-skip 2 --launch-count 1 -o gpurun_out/prof/stream_config5_s0.5 \
     python tools/kprof_stream.py 0.5 200000000 > gpurun_out/prof/stream.log 2>&1
+else
 $N -k regex:join_bits --launch-skip 3 --launch-count 1 -o gpurun_out/prof/join_bits_star python tools/diag_join.py \
     > gpurun_out/prof/join.log 2>&1
 $N -k regex:csv_ --launch-skip 8 --launch-count 4 -o gpurun_out/prof/csv_ingest python tools/diag_ingest.py \
@@ -23,4 +26,5 @@ $N -k regex:sel_compact --launch-skip 10 --launch-count 1 -o gpurun_out/prof/sel
     > gpurun_out/prof/selc2.log 2>&1
 $N -k regex:esc_scan_kernel --launch-skip 60 --launch-count 1 -o gpurun_out/prof/onepass_dim python tools/diag_onepass2.py \
     > gpurun_out/prof/op.log 2>&1
+fi
 ls -la gpurun_out/prof
