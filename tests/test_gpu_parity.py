@@ -364,3 +364,52 @@ def test_queued_compaction_checks_count_on_device(cuda):
             cy, cx = cols
             assert np.array_equal(cy.values.cpu().numpy(), y[want])
             assert np.array_equal(cx.values.cpu().numpy(), x[want])
+
+
+def test_onepass_plan_rebinds_new_outputs(cuda):
+    """A small table's ESC step reuses its prepared one-pass launch (esc_step_plan_rebind): every
+    run writes fresh output buffers, so the columns an earlier run handed over stay intact."""
+    from paper_1901_01488_b200 import ColumnTable, executor, expr as ex
+    from paper_1901_01488_b200.compiler import compile_predicate
+    from paper_1901_01488_b200.storage import KIND_INT32, KIND_INT64, Column
+
+    n = 40_000
+    g = np.random.default_rng(23)
+    k = np.arange(n, dtype=np.int64) * 3
+    r = g.integers(0, 25, n).astype(np.int32)
+    t = ColumnTable("t", [Column("k", KIND_INT64, k, device=cuda), Column("r", KIND_INT32, r, device=cuda)])
+    p = ex.Range(ex.ColumnRef("t", "r"), 3, 4)
+    want = np.flatnonzero((r >= 3) & (r <= 4))
+    first = executor.count_and_materialize(t, p, ["k", "r"], n)
+    keep = [c.values.cpu().numpy().copy() for c in first[1]]
+    for _ in range(3):
+        count, cols = executor.count_and_materialize(t, p, ["k", "r"], n)
+        assert count == want.size
+        assert np.array_equal(cols[0].values.cpu().numpy(), k[want])
+        assert np.array_equal(cols[1].values.cpu().numpy(), r[want])
+    assert np.array_equal(first[1][0].values.cpu().numpy(), keep[0])  # not overwritten by later runs
+    assert np.array_equal(first[1][1].values.cpu().numpy(), keep[1])
+    assert len(compile_predicate(t, p).c_plans) == 1  # one prepared launch, rebound each time
+
+
+@pytest.mark.parametrize("n", [600 * 8192 + 77, 2 * 148 * 4096 * 2 + 4096 * 3 + 5])
+def test_ticketed_scan_tails(cuda, n):
+    """K1 hands out multi-tile tickets on large scans; counts and selections stay exact when the
+    tile count is not a multiple of the ticket size (and the last tile is partial)."""
+    from paper_1901_01488_b200 import ColumnTable, count_star, executor, expr as ex
+    from paper_1901_01488_b200.storage import KIND_INT32, Column
+
+    g = np.random.default_rng(n % 1000)
+    cols = {c: g.integers(0, 1000, n).astype(np.int32) for c in ("a", "b", "c", "d")}
+    t = ColumnTable("t", [Column(c, KIND_INT32, v, device=cuda) for c, v in cols.items()])
+    r = lambda c: ex.ColumnRef("t", c)  # noqa: E731
+    p1 = ex.Range(r("a"), 0, 9)
+    assert count_star(t, p1) == int(np.count_nonzero(cols["a"] <= 9))
+    p4 = ex.And((ex.Range(r("a"), 0, 499), ex.Range(r("b"), 100, 999), ex.Comparison(r("c"), "<", 300),
+                 ex.Comparison(r("d"), ">=", 10)))
+    m = (cols["a"] <= 499) & (cols["b"] >= 100) & (cols["c"] < 300) & (cols["d"] >= 10)
+    want = np.flatnonzero(m)
+    count, out = executor.count_and_materialize(t, p4, ["d", "a"], n)
+    assert count == want.size
+    assert np.array_equal(out[0].values.cpu().numpy(), cols["d"][want])
+    assert np.array_equal(out[1].values.cpu().numpy(), cols["a"][want])
