@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_bits_kerne
         }
         m &= hit;
         acc[t + 1] += __popc(m);
+        if (t + 1 < NS && !__any_sync(__activemask(), m)) break;  // no survivor left among the active lanes
       }
     }
     q = qn;
