@@ -364,6 +364,89 @@ __device__ __forceinline__ void quad_keys(const JoinStepK& s, int64_t row0, int6
   }
 }
 
+// Star COUNT probe with small dense factors (every step 1-bit or 8-bit, int32 keys without NULLs,
+// factors in shared memory): join_bits_kernel's quad/pipelined structure with a running product
+// per row instead of a survivor mask, so dimensions with duplicate keys (8-bit group sizes) stay
+// on the fast path; the warp leaves the step chain once every product is zero.
+template <int NS>
+__global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_small_kernel(const __grid_constant__ JoinParams p) {
+  extern __shared__ __align__(16) uint8_t jsm[];
+  for (int t = 0; t < NS; ++t) {
+    const JoinStepK& s = p.steps[t];
+    const long long bytes = s.fbits == 1 ? ((s.dlen + 31) / 32) * 4 : s.dlen;
+    const long long words = (bytes + 15) / 16;
+    for (long long i = threadIdx.x; i < words; i += blockDim.x)
+      reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(reinterpret_cast<const uint4*>(s.factor) + i);
+  }
+  __syncthreads();
+  unsigned long long acc[ESC_MAX_STEPS + 1];
+#pragma unroll
+  for (int i = 0; i <= ESC_MAX_STEPS; ++i) acc[i] = 0;
+  const uint8_t* fac[NS];
+  int kmin[NS];
+  uint32_t klen[NS];
+  bool one_bit[NS];
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    fac[t] = jsm + p.steps[t].smem_off;
+    kmin[t] = (int)p.steps[t].dmin;
+    klen[t] = (uint32_t)p.steps[t].dlen;
+    one_bit[t] = p.steps[t].fbits == 1;
+  }
+  const int64_t nquads = (p.nrows + 3) / 4;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t full = p.nrows / 4;
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t m = bits_rows_mask<NS>(p, q, full);
+  int4 k[NS];
+  if (m) bits_load<NS>(p, q, full, m, k);
+  while (q < nquads) {
+    const int64_t qn = q + nth;
+    const uint32_t mn = bits_rows_mask<NS>(p, qn, full);
+    int4 kn[NS];
+    if (mn) bits_load<NS>(p, qn, full, mn, kn);
+    if (m) {
+      acc[0] += __popc(m);
+      unsigned long long run[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) run[j] = (m >> j) & 1u;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        const int kv[4] = {k[t].x, k[t].y, k[t].z, k[t].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t i = (uint32_t)kv[j] - (uint32_t)kmin[t];  // wraps below min: out of span
+          uint32_t f = 0;
+          if (run[j] != 0 && i < klen[t])
+            f = one_bit[t] ? (reinterpret_cast<const uint32_t*>(fac[t])[i >> 5] >> (i & 31)) & 1u : fac[t][i];
+          run[j] *= f;
+        }
+        acc[t + 1] += run[0] + run[1] + run[2] + run[3];
+        if (t + 1 < NS && !__any_sync(__activemask(), (run[0] | run[1] | run[2] | run[3]) != 0)) break;
+      }
+    }
+    q = qn;
+    m = mn;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) k[t] = kn[t];
+  }
+  __shared__ unsigned long long red[kJoinThreads / 32][ESC_MAX_STEPS + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int st = 0; st <= ESC_MAX_STEPS; ++st) {
+    unsigned long long v = acc[st];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+    if (lane == 0) red[warp][st] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x <= p.n_stages) {
+    unsigned long long v = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) v += red[w2][threadIdx.x];
+    if (v) atomicAdd(p.out + threadIdx.x, v);
+  }
+}
+
 template <int NS>
 __global__ void __launch_bounds__(kJoinThreads, 1) join_quad_kernel(const __grid_constant__ JoinParams p) {
   extern __shared__ __align__(16) uint8_t jsm[];
@@ -804,15 +887,29 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
       nullptr, esc::join_quad_kernel<1>, esc::join_quad_kernel<2>, esc::join_quad_kernel<3>,
       esc::join_quad_kernel<4>, esc::join_quad_kernel<5>, esc::join_quad_kernel<6>, esc::join_quad_kernel<7>,
       esc::join_quad_kernel<8>};
+  static void (*const small_kernels[ESC_MAX_STEPS + 1])(const esc::JoinParams) = {
+      nullptr, esc::join_small_kernel<1>, esc::join_small_kernel<2>, esc::join_small_kernel<3>,
+      esc::join_small_kernel<4>, esc::join_small_kernel<5>, esc::join_small_kernel<6>, esc::join_small_kernel<7>,
+      esc::join_small_kernel<8>};
   if (p.n_steps == 0) p.bits = 0;
-  // semi-join bitmaps -> join_bits_kernel; any other star -> join_quad_kernel; snowflake
-  // (stage-dependent weights) -> join_count_kernel
+  // semi-join bitmaps -> join_bits_kernel; 1/8-bit factors over int32 keys -> join_small_kernel;
+  // any other star -> join_quad_kernel; snowflake (stage-dependent weights) -> join_count_kernel
   bool quad = !p.bits && p.star && p.n_steps > 0;  // (hash steps: the one-row kernel measured faster)
   for (int t = 0; t < p.n_steps; ++t)
     if (p.steps[t].mode != ESC_JOIN_DENSE) quad = false;
-  auto kern = p.bits ? bits_kernels[p.n_steps] : quad ? quad_kernels[p.n_steps] : esc::join_count_kernel;
-  static thread_local uint32_t configured[2 * ESC_MAX_STEPS + 2] = {};
-  const int ci = p.bits ? p.n_steps : quad ? ESC_MAX_STEPS + 1 + p.n_steps : 0;
+  bool small = quad;
+  for (int t = 0; t < p.n_steps && small; ++t) {
+    const esc::JoinStepK& k = p.steps[t];
+    small = (k.fbits == 1 || k.fbits == 8) && k.dtype == ESC_I32 && k.nulls == nullptr &&
+            reinterpret_cast<uintptr_t>(k.keys) % 16 == 0 && k.smem_off != esc::kNoSmem && k.dmin >= INT32_MIN &&
+            k.dmin <= INT32_MAX && k.dlen <= INT32_MAX;
+  }
+  auto kern = p.bits ? bits_kernels[p.n_steps]
+              : small ? small_kernels[p.n_steps]
+              : quad  ? quad_kernels[p.n_steps]
+                      : esc::join_count_kernel;
+  static thread_local uint32_t configured[3 * ESC_MAX_STEPS + 3] = {};
+  const int ci = p.bits ? p.n_steps : small ? 2 * (ESC_MAX_STEPS + 1) + p.n_steps : quad ? ESC_MAX_STEPS + 1 + p.n_steps : 0;
   if (smem > 48 * 1024 && smem > configured[ci]) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

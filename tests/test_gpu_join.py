@@ -91,18 +91,19 @@ class TestHashIndex:
             assert idx.lookup(k).cpu().tolist() == [i for i, x in enumerate(keys) if x == k]
 
 
-@pytest.mark.parametrize("mode", ["bits", "dense", "hash"])
+@pytest.mark.parametrize("mode", ["bits", "small", "dense", "hash"])
 def test_star_count_large_probe(cuda, mode):
     """A 3M-row probe table (a ragged tail of 1 row past a multiple of 4, a probe predicate, NULL
-    keys) through four builds — the semi-join bitmap kernel (primary-key dimensions), dense
-    factors with a duplicate-key u8 dimension, and the hash path for a sparse key range — equals
-    the oracle's stage counts."""
+    keys) through four builds — the semi-join bitmap kernel (primary-key dimensions), the
+    small-factor kernel (a duplicate-key u8 dimension, int32 keys without NULLs), generic dense
+    factors (NULL probe keys) and the hash path for a sparse key range — equals the oracle's stage
+    counts."""
     dense = mode != "hash"
     from oracle import esc_oracle as O
     from paper_1901_01488_b200 import expr as ex, join
     from paper_1901_01488_b200.storage import KIND_INT32, KIND_INT64, Column, ColumnTable
 
-    g = np.random.default_rng({"bits": 2, "dense": 3, "hash": 4}[mode])
+    g = np.random.default_rng({"bits": 2, "small": 5, "dense": 3, "hash": 4}[mode])
     n = 3_000_017
     mult = 1 if dense else 1_000_003  # spread keys so the key range is too sparse for a direct array
     dims, otabs, steps_o, steps_d, fk = {}, {}, [], [], {}
@@ -125,7 +126,7 @@ def test_star_count_large_probe(cuda, mode):
         steps_d.append(join.BuildStep(f"d{s}", join.build_hash(dtab, "k", serde.from_json(res_j, f"d{s}")),
                                       ex.ColumnRef("f", f"k{s}")))
         v = (g.integers(0, nd + 2, n) * mult).astype(np.int64)
-        nulls = g.random(n) < (0.0 if mode == "bits" else 0.01)
+        nulls = g.random(n) < (0.0 if mode in ("bits", "small") else 0.01)
         probe_cols_o[f"k{s}"] = O.OColumn(np.where(nulls, 0, v), nulls)
         kind, arr = (KIND_INT32, np.where(nulls, 0, v).astype(np.int32)) if dense else (KIND_INT64, np.where(nulls, 0, v))
         probe_cols_d.append(Column(f"k{s}", kind, arr, nulls, device=cuda))
