@@ -327,6 +327,11 @@ int esc_hash_build_temp_bytes(int64_t n, size_t* bytes);
  * store the group's size there (esc_join_step_t.factor / factor_bits). */
 int esc_factor_array(const int64_t* unique_keys, const int64_t* counts, int64_t u, int64_t lo, int64_t span,
                      int32_t bits, void* out, size_t out_bytes, void* stream);
+/* A star step's (key, factor) pair table for sparse key ranges: pairs = int64[2 * capacity]
+ * (16-byte aligned), capacity a power of two > u; factor 0 marks an empty slot; splitmix64 +
+ * linear probing as esc_hash_insert.  Probed by esc_join_count in ESC_JOIN_PAIRS mode. */
+int esc_pairs_build(const int64_t* unique_keys, const int64_t* counts, int64_t u, int64_t* pairs, int64_t capacity,
+                    void* stream);
 int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int64_t n, int64_t* out_group_rows,
                    int64_t* out_unique_keys, int64_t* out_group_counts, int64_t* out_group_start, int64_t* out_stats,
                    void* d_temp, size_t temp_bytes, void* stream);
@@ -346,14 +351,14 @@ int esc_hash_probe(const int64_t* slots, int64_t capacity, const int64_t* unique
 int esc_expand(const int64_t* groups, const int64_t* offsets, int64_t n, const int64_t* group_start,
                const int64_t* group_rows, int64_t* out_tuple, int64_t* out_row, void* stream);
 
-enum { ESC_JOIN_DENSE = 0, ESC_JOIN_HASH = 1 };
+enum { ESC_JOIN_DENSE = 0, ESC_JOIN_HASH = 1, ESC_JOIN_PAIRS = 2 };
 
 /* One probe-keyed build step of a COUNT pipeline. */
 typedef struct {
   const void* key_data;     /* the probe table's key column (device, native integer width)   */
   const uint8_t* key_nulls; /* its bool NULL mask or NULL                                     */
   int32_t key_dtype;
-  int32_t mode;             /* ESC_JOIN_DENSE or ESC_JOIN_HASH                                */
+  int32_t mode;             /* ESC_JOIN_DENSE, ESC_JOIN_HASH or ESC_JOIN_PAIRS               */
   /* DENSE (star joins): factor(k) = factor[k - dense_min] for 0 <= k - dense_min < dense_len,
    * else 0; factor_bits = 1 (bitmap of 32-bit words), 8, 16, 32 or 64; 16-byte aligned       */
   int64_t dense_min;
@@ -361,7 +366,9 @@ typedef struct {
   const void* factor;
   int32_t factor_bits;
   int32_t pad;
-  /* HASH: g = the key's group (esc_hash_probe's table); weight[s][g] = its factor at stage s  */
+  /* HASH: g = the key's group (esc_hash_probe's table); weight[s][g] = its factor at stage s.
+   * PAIRS (star joins): slots = an esc_pairs_build table of capacity (key, factor) pairs: one
+   * dependent load per probed key instead of three (slot, key, weight)                        */
   const int64_t* slots;
   int64_t capacity;
   const int64_t* unique_keys;

@@ -90,7 +90,7 @@ class EscSelection(C.Structure):
 
 
 MAX_STEPS = 8
-JOIN_DENSE, JOIN_HASH = 0, 1
+JOIN_DENSE, JOIN_HASH, JOIN_PAIRS = 0, 1, 2
 
 
 class EscJoinStep(C.Structure):
@@ -147,6 +147,7 @@ _SIGNATURES = {
     "esc_hash_insert": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
     "esc_factor_array": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
                                    C.c_size_t, C.c_void_p]),
+    "esc_pairs_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
     "esc_hash_build_temp_bytes": (C.c_int, [C.c_int64, C.POINTER(C.c_size_t)]),
     "esc_hash_build": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),

@@ -284,6 +284,7 @@ def _count_pipeline(probe: ColumnTable, probe_alias: str, probe_pred, steps: lis
     if S > N.MAX_STEPS:
         raise ExecutionError(f"a probe pipeline supports at most {N.MAX_STEPS} build steps")
     keep = []
+    lib = N.load_library()
     j = N.EscJoin()
     j.n_stages = S
     j.nrows = probe.row_count
@@ -313,6 +314,19 @@ def _count_pipeline(probe: ColumnTable, probe_alias: str, probe_pred, steps: lis
             d.mode = N.JOIN_DENSE
             d.dense_min, d.dense_len, d.factor, d.factor_bits = lo, span, arr.data_ptr(), bits
             continue
+        if star:  # sparse key range: a (key, factor) pair table at load <= 1/4, one load per probe
+            cap = 16
+            while cap < 4 * max(idx.distinct_keys, 1):
+                cap *= 2
+            pairs = torch.empty(2 * cap, dtype=torch.int64, device=probe.device)
+            keep.append(pairs)
+            N.check(lib.esc_pairs_build(C.c_void_p(idx.unique_keys.data_ptr()) if idx.distinct_keys else None,
+                                        C.c_void_p(idx.group_counts.data_ptr()) if idx.distinct_keys else None,
+                                        idx.distinct_keys, C.c_void_p(pairs.data_ptr()), cap,
+                                        C.c_void_p(_stream(probe.device).cuda_stream)), "esc_pairs_build")
+            d.mode = N.JOIN_PAIRS
+            d.slots, d.capacity = pairs.data_ptr(), cap
+            continue
         d.mode = N.JOIN_HASH
         d.slots, d.capacity = idx.slots.data_ptr(), idx.capacity
         uk = idx.unique_keys if idx.unique_keys.numel() else idx.slots
@@ -325,7 +339,6 @@ def _count_pipeline(probe: ColumnTable, probe_alias: str, probe_pred, steps: lis
             d.weight[s] = w.data_ptr()
     j.n_steps = len(probe_keyed)
     out = torch.empty(S + 1, dtype=torch.int64, device=probe.device)
-    lib = N.load_library()
     stream = _stream(probe.device)
     ev0 = executor._ev_start(stream)
     N.check(lib.esc_join_count(C.byref(j), C.c_void_p(out.data_ptr()), C.c_void_p(stream.cuda_stream)),

@@ -141,4 +141,7 @@ def test_join_csv_plan_entry_points_validate_arguments(native_lib):
     err(native_lib.esc_hash_build(None, 2, None, 10, None, None, None, None, None, None, 0, None), "null hash build")
     err(native_lib.esc_factor_array(None, None, 1, 0, 8, 3, None, 0, None), "bad factor array")
     err(native_lib.esc_factor_array(None, None, 1, 0, 64, 8, None, 16, None), "too small")
+    err(native_lib.esc_pairs_build(None, None, 4, None, 12, None), "power of two")
+    err(native_lib.esc_pairs_build(None, None, 16, None, 16, None), "exceed")
+    err(native_lib.esc_pairs_build(None, None, 3, None, 16, None), "null pair table")
     assert native_lib.esc_csv_workspace_bytes(1 << 30) > native_lib.esc_csv_workspace_bytes(1 << 10)
