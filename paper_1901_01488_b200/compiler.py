@@ -59,6 +59,7 @@ class CompiledPredicate:
     may_fail: bool                # some UDF is evaluated densely (can raise)
     col_array: object = field(default=None, repr=False)
     c_plans: dict = field(default_factory=dict, repr=False)  # prepared one-pass launches (executor)
+    shapes: dict = field(default_factory=dict, repr=False)   # one-pass output templates (executor)
 
     @property
     def ncols(self) -> int:

@@ -628,7 +628,7 @@ def _take_outputs(ps: PendingStep, ws, k: int) -> list[Column]:
     are handed over as views (their plan is not cached again), others trimmed by one copy."""
     plan = ps.plan
     if ps.kind == "onepass" and plan.nbytes <= SMALL_OUTPUT_BYTES:
-        return [Column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
+        return [Column.device_column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
                 for c, v, m in zip(ps.proj, plan.out_values, plan.out_nulls)]
     if plan.trim_cache is None:
         plan.trim_cache = {}
@@ -735,29 +735,41 @@ def _onepass_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacit
     plan = ws.scratch.setdefault("plans", {}).pop(key, None)  # checked out until finished
     if plan is not None:
         return plan
-    extra, slots = [], []
-    for col in proj:
-        if col.name in cp.slot_of:
-            slots.append(cp.slot_of[col.name])
-        else:
-            slots.append(cp.ncols + len(extra))
-            extra.append(col)
-    if cp.ncols + len(extra) > N.MAX_COLS or len(proj) > N.MAX_PROJ:
-        raise ExecutionError("too many columns for one compaction")
-    outs = N.EscOutputs()
-    outs.n_proj = len(proj)
-    outs.capacity = capacity
-    values, nulls = [], []
+    # the shape-only parts (slots, column array, outputs template) are kept with the compiled
+    # predicate: a small table's outputs become its temp, so each step needs new buffers only
+    shape = cp.shapes.get(key[3:])
+    if shape is None:
+        extra, slots = [], []
+        for col in proj:
+            if col.name in cp.slot_of:
+                slots.append(cp.slot_of[col.name])
+            else:
+                slots.append(cp.ncols + len(extra))
+                extra.append(col)
+        if cp.ncols + len(extra) > N.MAX_COLS or len(proj) > N.MAX_PROJ:
+            raise ExecutionError("too many columns for one compaction")
+        tmpl = N.EscOutputs()
+        tmpl.n_proj = len(proj)
+        tmpl.capacity = capacity
+        for k in range(len(proj)):
+            tmpl.slot[k] = slots[k]
+        shape = cp.shapes[key[3:]] = (tmpl, cp.column_array(extra), cp.ncols + len(extra))
+    tmpl, mat_cols, mat_ncols = shape
+    outs = N.EscOutputs.from_buffer_copy(tmpl)
+    n_alloc = max(capacity, 1)
+    dev = table.device
+    values, nulls, nbytes = [], [], 0
     for k, col in enumerate(proj):
-        v = torch.empty(max(capacity, 1), dtype=col.values.dtype, device=table.device)
-        m = torch.empty(max(capacity, 1), dtype=torch.bool, device=table.device) if col.nulls is not None else None
+        v = torch.empty(n_alloc, dtype=col.values.dtype, device=dev)
+        m = torch.empty(n_alloc, dtype=torch.bool, device=dev) if col.nulls is not None else None
         values.append(v)
         nulls.append(m)
-        outs.slot[k] = slots[k]
-        outs.out_values[k] = v.data_ptr() if capacity else None
-        outs.out_nulls[k] = m.data_ptr() if m is not None and capacity else None
-    plan = _StepPlan(key, cp, None, outs, values, nulls, cp.column_array(extra), cp.ncols + len(extra))
-    plan.nbytes = sum(b.numel() * b.element_size() for b in [*values, *[m for m in nulls if m is not None]])
+        nbytes += n_alloc * (v.element_size() + (1 if m is not None else 0))
+        if capacity:
+            outs.out_values[k] = v.data_ptr()
+            outs.out_nulls[k] = m.data_ptr() if m is not None else None
+    plan = _StepPlan(key, cp, None, outs, values, nulls, mat_cols, mat_ncols)
+    plan.nbytes = nbytes
     return plan
 
 
