@@ -240,16 +240,23 @@ def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=N
     if err != (1 << 64) - 1:
         _raise_cell_error(data, field_end, field_kind, first_field, ncols, schema, name,
                           2 if has_header else 1, err >> 4, err & 15)
+    # which columns hold a NULL at all: one read for every column (a column without NULLs keeps
+    # no mask, as the Column constructor would decide with one wait per column)
+    has_null = torch.stack([o[1].any() for o in out]).tolist() if out and nrows else [False] * len(out)
     cols = []
-    for (cname, kind), (vals, nulls, _) in zip(schema, out):
+    for (cname, kind), (vals, nulls, _), hn in zip(schema, out, has_null):
+        mask = nulls if hn else None
         if kind.is_text:
             codes, dictionary = _encode_text(data, d_bytes, field_end, field_kind, first_field, nrows, ncols,
                                              schema.index((cname, kind)), vals, nulls, sp, name)
-            cols.append(Column(cname, kind, codes, nulls, dictionary))
+            cols.append(Column.device_column(cname, kind, codes, mask, dictionary) if mask is None
+                        else Column(cname, kind, codes, mask, dictionary))
         elif kind.name == DATE:
-            cols.append(Column(cname, kind, vals.to(torch.int32), nulls))
+            v = vals.to(torch.int32)
+            cols.append(Column.device_column(cname, kind, v, None, None) if mask is None else Column(cname, kind, v, mask))
         else:
-            cols.append(Column(cname, kind, vals, nulls))
+            cols.append(Column.device_column(cname, kind, vals, None, None) if mask is None
+                        else Column(cname, kind, vals, mask))
     return ColumnTable(name, cols)
 
 
