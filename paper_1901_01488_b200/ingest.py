@@ -147,6 +147,34 @@ def _cell_text(data: bytes, start: int, end: int) -> tuple[str, bool]:
     return raw.decode("utf-8", "replace"), b'"' not in raw
 
 
+_STAGE_BYTES = 8 << 20
+_staging: dict = {}
+
+
+def _upload(host: torch.Tensor, dev: torch.device, stream) -> torch.Tensor:
+    """The CSV bytes to HBM through two reused pinned staging buffers: the host copy of chunk
+    i + 1 overlaps the DMA of chunk i (pinning the whole text first, then copying it, serialised
+    the two)."""
+    n = int(host.numel())
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    if n <= _STAGE_BYTES:
+        out.copy_(host.pin_memory(), non_blocking=True)
+        return out
+    bufs = _staging.get(dev)
+    if bufs is None:
+        bufs = _staging[dev] = [(torch.empty(_STAGE_BYTES, dtype=torch.uint8).pin_memory(),
+                                 torch.cuda.Event()) for _ in range(2)]
+    for i, off in enumerate(range(0, n, _STAGE_BYTES)):
+        ln = min(_STAGE_BYTES, n - off)
+        buf, ev = bufs[i % 2]
+        ev.synchronize()  # the DMA that last read this buffer is done
+        buf[:ln].copy_(host[off:off + ln])
+        with torch.cuda.stream(stream):
+            out[off:off + ln].copy_(buf[:ln], non_blocking=True)
+            ev.record(stream)
+    return out
+
+
 def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=None) -> ColumnTable:
     """Build a device table from RFC-4180 CSV text (``\\N`` = NULL, ISO dates) — reference
     ``storage.load_csv``; errors are the reference's ``CsvError`` / ``OverflowError`` text."""
@@ -167,7 +195,7 @@ def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=N
         with warnings.catch_warnings():  # read-only view of the caller's bytes; only copied from
             warnings.simplefilter("ignore", UserWarning)
             host = torch.frombuffer(data, dtype=torch.uint8)
-        d_bytes = host.pin_memory().to(dev, non_blocking=True)
+        d_bytes = _upload(host, dev, stream)
     else:
         d_bytes = torch.zeros(1, dtype=torch.uint8, device=dev)
     ws_bytes = int(lib.esc_csv_workspace_bytes(n))
