@@ -144,4 +144,12 @@ def test_join_csv_plan_entry_points_validate_arguments(native_lib):
     err(native_lib.esc_pairs_build(None, None, 4, None, 12, None), "power of two")
     err(native_lib.esc_pairs_build(None, None, 16, None, 16, None), "exceed")
     err(native_lib.esc_pairs_build(None, None, 3, None, 16, None), "null pair table")
+    jp = N.EscJoin()
+    jp.n_steps, jp.n_stages, jp.nrows, jp.star = 1, 1, 10, 0
+    jp.stage_of[0] = 1
+    jp.steps[0].key_data, jp.steps[0].key_dtype, jp.steps[0].mode = 1, 2, N.JOIN_PAIRS
+    err(native_lib.esc_join_count(C.byref(jp), out, None), "star")
+    jp.star = 1
+    jp.steps[0].slots, jp.steps[0].capacity = 16, 12
+    err(native_lib.esc_join_count(C.byref(jp), out, None), "bad pair table")
     assert native_lib.esc_csv_workspace_bytes(1 << 30) > native_lib.esc_csv_workspace_bytes(1 << 10)
