@@ -956,7 +956,52 @@ struct StepPlanImpl {
   ScanLaunch scan;
   MatLaunch mat;
   bool onepass = false;  // one launch of the look-back kernel (no selection, no queued compaction)
+  // queued plans: the launches of parts 1, 2 and 3 captured once into CUDA graphs (their
+  // parameters never change), so a re-issue is one graph launch instead of up to five kernel
+  // launches with kilobytes of parameters each
+  cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
+  int graph_kernels[4] = {0, 0, 0, 0};
+  bool graph_failed[4] = {false, false, false, false};
+  ~StepPlanImpl() {
+    for (auto& g : graph)
+      if (g != nullptr) cudaGraphExecDestroy(g);
+  }
 };
+
+std::atomic<int> g_graphs{[] {
+  const char* e = getenv("ESC_GRAPHS");  // 0 turns the step-plan graphs off (experiments)
+  return e ? atoi(e) : 1;
+}()};
+
+// issue a queued plan's parts on `st` directly
+int issue_parts(StepPlanImpl* p, int parts, cudaStream_t st) {
+  int rc = (parts & 1) ? issue_scan(p->scan, p->kp, st) : ESC_OK;
+  return (rc != ESC_OK || !(parts & 2)) ? rc : issue_mat(p->mat, st);
+}
+
+// capture a queued plan's parts into an executable graph (on a private stream, thread-local
+// capture mode); false leaves the plan on direct launches
+bool capture_parts(StepPlanImpl* p, int parts) {
+  cudaStream_t cs = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return false;
+  const long long before = g_launches.load();
+  bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  const int rc = ok ? issue_parts(p, parts, cs) : ESC_ERR_CUDA;
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = ok ? cudaStreamEndCapture(cs, &g) : cudaErrorUnknown;
+  ok = ok && rc == ESC_OK && e == cudaSuccess && g != nullptr;
+  cudaGraphExec_t x = nullptr;
+  if (ok) ok = cudaGraphInstantiate(&x, g, 0) == cudaSuccess;
+  if (g != nullptr) cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  cudaGetLastError();  // a failed capture must not leave a sticky launch error behind
+  const long long issued = g_launches.load() - before;
+  g_launches -= issued;  // captured, not launched: counted per graph launch instead
+  if (!ok) return false;
+  p->graph[parts] = x;
+  p->graph_kernels[parts] = (int)issued;
+  return true;
+}
 
 // next look-back epoch of a workspace (status words carry it, so they need no clearing per launch)
 int next_epoch(KParams& kp, int64_t nrows, void* d_ws, cudaStream_t stream) {
@@ -1028,8 +1073,17 @@ int esc_step_plan_launch(void* plan, int32_t parts, void* stream) {
     const int rc = next_epoch(p->kp, p->kp.nrows, p->kp.hdr, st);
     return rc != ESC_OK ? rc : issue_scan(p->scan, p->kp, st);
   }
-  int rc = (parts & 1) ? issue_scan(p->scan, p->kp, st) : ESC_OK;
-  return (rc != ESC_OK || !(parts & 2)) ? rc : issue_mat(p->mat, st);
+  if (g_graphs.load() && g_trace == nullptr && !p->graph_failed[parts]) {
+    if (p->graph[parts] == nullptr && !capture_parts(p, parts)) {
+      p->graph_failed[parts] = true;
+      return issue_parts(p, parts, st);
+    }
+    const cudaError_t e = cudaGraphLaunch(p->graph[parts], st);
+    if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("step graph launch: ") + cudaGetErrorString(e));
+    g_launches += p->graph_kernels[parts];
+    return ESC_OK;
+  }
+  return issue_parts(p, parts, st);
 }
 
 int esc_step_plan_rebind(void* plan, const esc_outputs_t* outs) {
