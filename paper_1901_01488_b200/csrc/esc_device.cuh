@@ -1817,6 +1817,8 @@ __global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_ker
   extern __shared__ __align__(1024) uint8_t smem[];
   pdl_wait();
   pdl_trigger();
+  const uint32_t nd = *p.n_dense;
+  if (blockIdx.x >= nd) return;  // a CTA without a dense tile to stream leaves at once
   const int S = p.stages;
   uint8_t* ring = smem;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
@@ -1832,7 +1834,6 @@ __global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_ker
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint32_t nd = *p.n_dense;
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t policy = evict_first_policy();
