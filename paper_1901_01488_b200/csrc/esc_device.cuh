@@ -1617,6 +1617,15 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
       const unsigned long long soff_l = off_l;
       const int CPS = W / 4;
       const int cps_log = __ffs(CPS) - 1;
+      // the next round's bitmap chunk is loaded one round ahead (its latency hides behind this
+      // round's ranking and gathers)
+      auto load_round = [&](int b) {
+        const int sl = (b * 32 + lane) >> cps_log;
+        const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
+        return work ? __ldg(reinterpret_cast<const uint4*>(p.bitmap + (seg0 + sl) * W + ((b * 32 + lane) & (CPS - 1)) * 4))
+                    : make_uint4(0u, 0u, 0u, 0u);
+      };
+      uint4 w4n = load_round(0);
       for (int b = 0; b < CPS; ++b) {
         const int c = b * 32 + lane;
         const int sl = c >> cps_log;  // lane owning the chunk's segment
@@ -1625,8 +1634,8 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
         const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, soff_l, sl);
         const bool scap = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, sl) != 0;
         const int64_t seg = seg0 + sl;
-        uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
-        if (work) w4 = __ldg(reinterpret_cast<const uint4*>(p.bitmap + seg * W + sub * 4));
+        const uint4 w4 = w4n;
+        if (b + 1 < CPS) w4n = load_round(b + 1);
         const uint32_t pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
         uint32_t incl = pc;
         for (int d = 1; d < CPS; d <<= 1) {
