@@ -1,3 +1,5 @@
+"""Host cost of a kernel launch on this box (not part of the product): a tiny esc_gather and a torch
+fill_, 2000 each, timed on the host."""
 import ctypes as C, sys, time, os
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
 import torch
