@@ -70,7 +70,9 @@ __device__ __forceinline__ void csv_load_lane(const uint8_t* b, int64_t n, int64
 // SWAR classification of a lane's 16 bytes into 16-bit masks (bit k = byte k)
 __device__ __forceinline__ uint32_t eq_mask4(uint32_t w, uint32_t pat) {
   const uint32_t e = __vcmpeq4(w, pat);  // 0xFF in every byte equal to the pattern byte
-  return ((e >> 7) & 1u) | ((e >> 14) & 2u) | ((e >> 21) & 4u) | ((e >> 28) & 8u);
+  // the four byte-high bits (7, 15, 23, 31) gathered into bits 28..31 by one multiply: each of
+  // them meets exactly one of the shifts 21, 14, 7, 0 that lands it there, without carries
+  return ((e & 0x80808080u) * 0x00204081u) >> 28;
 }
 
 struct CsvMasks {
@@ -121,21 +123,18 @@ __device__ CsvSum csv_slice_sum(const uint8_t* b, int64_t n, int64_t s0, int64_t
     const CsvMasks m = csv_masks(L);
     const unsigned odd = __ballot_sync(0xFFFFFFFFu, __popc(m.quote) & 1);
     const uint32_t inside = quote_state(m.quote) ^ (((acc.flip ^ __popc(odd & lt)) & 1u) ? 0xFFFFu : 0u);
-    unsigned fe = __popc(m.sep & ~inside), fo = __popc(m.sep & inside);
-    unsigned re = __popc(m.rec & ~inside), ro = __popc(m.rec & inside);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      fe += __shfl_xor_sync(0xFFFFFFFFu, fe, d);
-      fo += __shfl_xor_sync(0xFFFFFFFFu, fo, d);
-      re += __shfl_xor_sync(0xFFFFFFFFu, re, d);
-      ro += __shfl_xor_sync(0xFFFFFFFFu, ro, d);
-    }
-    acc.f_e += fe;  // counts relative to the slice start state (the combine step's form)
-    acc.f_o += fo;
-    acc.r_e += re;
-    acc.r_o += ro;
+    // per-lane counts relative to the slice start state (the combine step's form), reduced
+    // over the warp once per slice
+    acc.f_e += __popc(m.sep & ~inside);
+    acc.f_o += __popc(m.sep & inside);
+    acc.r_e += __popc(m.rec & ~inside);
+    acc.r_o += __popc(m.rec & inside);
     acc.flip ^= __popc(odd) & 1u;
   }
+  acc.f_e = __reduce_add_sync(0xFFFFFFFFu, (unsigned)acc.f_e);
+  acc.f_o = __reduce_add_sync(0xFFFFFFFFu, (unsigned)acc.f_o);
+  acc.r_e = __reduce_add_sync(0xFFFFFFFFu, (unsigned)acc.r_e);
+  acc.r_o = __reduce_add_sync(0xFFFFFFFFu, (unsigned)acc.r_o);
   return acc;
 }
 
