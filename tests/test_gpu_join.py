@@ -217,3 +217,38 @@ def test_batched_esc_keeps_the_reference_error_sequence(cuda):
     assert [(d.table, d.exact_count, d.pushed_down) for d in ok.decisions] == [("a", 200, True), ("c", 400, True)]
     assert sum(d.subquery_ms for d in ok.decisions) > 0
     cat.temps.sweep()
+
+
+def test_build_indexes_batch_equals_single_builds(cuda):
+    """build_indexes (one host read for every build's statistics) equals build_hash one by one,
+    for keys of every integer width, with NULLs, duplicates, a residual and an empty build."""
+    import torch
+
+    from paper_1901_01488_b200 import expr as ex, join
+    from paper_1901_01488_b200.storage import Column, ColumnTable, parse_kind
+
+    g = np.random.default_rng(41)
+    specs = []
+    for i, (kind, dt, lo, hi) in enumerate((("INT8", np.int8, -100, 100), ("INT16", np.int16, -3000, 3000),
+                                            ("INT32", np.int32, -10**6, 10**6), ("INT64", np.int64, -10**12, 10**12))):
+        n = 5000 + 17 * i
+        k = g.integers(lo, hi, n).astype(dt)
+        k[::7] = k[::5][: len(k[::7])]  # duplicates
+        nulls = g.random(n) < 0.05
+        a = g.integers(0, 10, n).astype(np.int64)
+        t = ColumnTable(f"t{i}", [Column("k", parse_kind(kind), k, nulls, device=cuda),
+                                  Column("a", parse_kind("INT64"), a, device=cuda)])
+        res = ex.Comparison(ex.ColumnRef(f"t{i}", "a"), "<", 7) if i % 2 else None
+        specs.append((t, "k", res))
+    empty = ColumnTable("e", [Column("k", parse_kind("INT32"), np.zeros(0, np.int32), device=cuda)])
+    specs.append((empty, "k", None))
+    batch = join.build_indexes(specs)
+    for (t, key, res), b in zip(specs, batch):
+        s = join.build_hash(t, key, res)
+        assert b.n_entries == s.n_entries and b.distinct_keys == s.distinct_keys and b.capacity == s.capacity
+        for name in ("unique_keys", "group_counts", "group_start", "group_rows"):
+            assert torch.equal(getattr(b, name), getattr(s, name)), (t.name, name)
+        if s.distinct_keys:
+            uk = s.unique_keys.cpu().numpy()
+            assert np.all(np.diff(uk) > 0)  # ascending, distinct
+            assert b.key_range == (int(uk[0]), int(uk[-1]), int(s.group_counts.max()))
