@@ -565,6 +565,25 @@ __global__ void build_gather_kernel(const uint8_t* __restrict__ keys, int dtype,
   }
 }
 
+// keys of <= 4 bytes sort as 32-bit unsigned values biased by 2^31 (signed types): the radix sort
+// then runs 4 digit passes instead of 8
+__global__ void build_gather32_kernel(const uint8_t* __restrict__ keys, int dtype, int width,
+                                      const int64_t* __restrict__ rows, int64_t n, uint32_t bias,
+                                      uint32_t* __restrict__ out_keys, int64_t* __restrict__ out_rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows ? rows[i] : i;
+    out_keys[i] = (uint32_t)ld_int(keys + (size_t)r * width, dtype) + bias;
+    out_rows[i] = r;
+  }
+}
+
+__global__ void build_unbias_kernel(const uint32_t* __restrict__ uk32, const long long* __restrict__ num_runs,
+                                    uint32_t bias, long long* __restrict__ uk) {
+  const long long u = *num_runs;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < u; g += (long long)gridDim.x * blockDim.x)
+    uk[g] = bias ? (long long)(int32_t)(uk32[g] - bias) : (long long)uk32[g];
+}
+
 __global__ void build_stats_kernel(const long long* __restrict__ unique_keys, const long long* __restrict__ num_runs,
                                    const long long* __restrict__ max_count, int64_t* __restrict__ stats) {
   const long long u = *num_runs;
@@ -637,14 +656,19 @@ inline int build_temp_layout(int64_t n, BuildTemp* T) {
 inline int build_temp_layout_q(int64_t n, BuildTemp* T) {
   size_t a = 0, b = 0, c = 0, d = 0;
   const int nn = (int)n;
+  size_t a32 = 0, b32 = 0;
   if (cub::DeviceRadixSort::SortPairs(nullptr, a, (const long long*)nullptr, (long long*)nullptr,
                                       (const int64_t*)nullptr, (int64_t*)nullptr, nn) != cudaSuccess ||
+      cub::DeviceRadixSort::SortPairs(nullptr, a32, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                      (const int64_t*)nullptr, (int64_t*)nullptr, nn) != cudaSuccess ||
       cub::DeviceRunLengthEncode::Encode(nullptr, b, (const long long*)nullptr, (long long*)nullptr,
+                                         (long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess ||
+      cub::DeviceRunLengthEncode::Encode(nullptr, b32, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                          (long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess ||
       cub::DeviceScan::ExclusiveSum(nullptr, c, (const long long*)nullptr, (long long*)nullptr, nn + 1) != cudaSuccess ||
       cub::DeviceReduce::Max(nullptr, d, (const long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess)
     return fail(ESC_ERR_CUDA, "CUB temp-size query failed");
-  T->cub_bytes = std::max(std::max(a, b), std::max(c, d));
+  T->cub_bytes = std::max(std::max(std::max(a, a32), std::max(b, b32)), std::max(c, d));
   size_t off = 0;
   T->keys_in = off;     off += align256((size_t)n * 8);
   T->rows_in = off;     off += align256((size_t)n * 8);
@@ -751,19 +775,43 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
-  ++g_launches;
-  esc::build_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(keys), key_dtype,
-                                                             dtype_width(key_dtype), rows, n, keys_in, rows_in);
-  // stable (LSD radix) sort by key: equal keys keep ascending build-row order, as the
-  // reference's stable argsort; then runs = groups in ascending key order
   const int nn = (int)n;
-  g_launches += 4;
-  e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys_in, keys_sorted, rows_in, out_group_rows, nn, 0,
-                                      64, st);
-  if (e == cudaSuccess)
-    e = cub::DeviceRunLengthEncode::Encode(cub_tmp, cub_bytes, keys_sorted,
-                                           reinterpret_cast<long long*>(out_unique_keys),
-                                           reinterpret_cast<long long*>(out_group_counts), num_runs, nn, st);
+  const int w = dtype_width(key_dtype);
+  if (w <= 4) {
+    // stable (LSD radix) sort of 32-bit biased keys: equal keys keep ascending build-row order
+    const bool sgn = key_dtype == ESC_I8 || key_dtype == ESC_I16 || key_dtype == ESC_I32;
+    const uint32_t bias = sgn ? 0x80000000u : 0u;
+    uint32_t* k32_in = reinterpret_cast<uint32_t*>(keys_in);
+    uint32_t* k32_sorted = reinterpret_cast<uint32_t*>(keys_sorted);
+    uint32_t* uk32 = reinterpret_cast<uint32_t*>(keys_in);  // the input keys are dead after the sort
+    ++g_launches;
+    esc::build_gather32_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(keys), key_dtype, w,
+                                                                 rows, n, bias, k32_in, rows_in);
+    g_launches += 5;
+    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k32_in, k32_sorted, rows_in, out_group_rows, nn, 0, 32,
+                                        st);
+    if (e == cudaSuccess)
+      e = cub::DeviceRunLengthEncode::Encode(cub_tmp, cub_bytes, k32_sorted, uk32,
+                                             reinterpret_cast<long long*>(out_group_counts), num_runs, nn, st);
+    if (e == cudaSuccess) {
+      esc::build_unbias_kernel<<<(unsigned)blocks, 256, 0, st>>>(uk32, num_runs, bias,
+                                                                 reinterpret_cast<long long*>(out_unique_keys));
+      e = cudaGetLastError();
+    }
+  } else {
+    ++g_launches;
+    esc::build_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(keys), key_dtype, w, rows,
+                                                               n, keys_in, rows_in);
+    // stable (LSD radix) sort by key: equal keys keep ascending build-row order, as the
+    // reference's stable argsort; then runs = groups in ascending key order
+    g_launches += 4;
+    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys_in, keys_sorted, rows_in, out_group_rows, nn, 0,
+                                        64, st);
+    if (e == cudaSuccess)
+      e = cub::DeviceRunLengthEncode::Encode(cub_tmp, cub_bytes, keys_sorted,
+                                             reinterpret_cast<long long*>(out_unique_keys),
+                                             reinterpret_cast<long long*>(out_group_counts), num_runs, nn, st);
+  }
   if (e == cudaSuccess)
     e = cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, reinterpret_cast<const long long*>(out_group_counts),
                                       reinterpret_cast<long long*>(out_group_start), nn + 1, st);
