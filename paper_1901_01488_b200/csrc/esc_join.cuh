@@ -584,6 +584,91 @@ __global__ void build_unbias_kernel(const uint32_t* __restrict__ uk32, const lon
     uk[g] = bias ? (long long)(int32_t)(uk32[g] - bias) : (long long)uk32[g];
 }
 
+// The whole grouping of a small build (<= 1024 * ITEMS rows, keys of <= 4 bytes) in ONE block:
+// a stable block radix sort of the biased 32-bit keys with their rows, group starts by comparing
+// neighbours, a block scan for the group ids, then offsets, sizes, unique keys and statistics —
+// one launch where the device-wide path costs about a dozen.
+constexpr int kBuildSmallThreads = 1024;
+template <int ITEMS>
+struct BuildSmall {
+  using Sort = cub::BlockRadixSort<uint32_t, kBuildSmallThreads, ITEMS, int64_t>;
+  using Scan = cub::BlockScan<int, kBuildSmallThreads>;
+  using Reduce = cub::BlockReduce<long long, kBuildSmallThreads>;
+  union Temp {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+    typename Reduce::TempStorage reduce;
+  };
+  static constexpr size_t kSmem = sizeof(Temp) + sizeof(uint32_t) * kBuildSmallThreads;
+};
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kBuildSmallThreads, 1)
+build_small_kernel(const uint8_t* __restrict__ keys, int dtype, int width, const int64_t* __restrict__ rows,
+                   int64_t n, uint32_t bias, int64_t* __restrict__ group_rows, long long* __restrict__ uk,
+                   long long* __restrict__ counts, long long* __restrict__ start, int64_t* __restrict__ stats) {
+  using B = BuildSmall<ITEMS>;
+  extern __shared__ __align__(16) uint8_t bsm[];
+  typename B::Temp& tmp = *reinterpret_cast<typename B::Temp*>(bsm);
+  uint32_t* last_key = reinterpret_cast<uint32_t*>(bsm + sizeof(typename B::Temp));  // per thread
+  const int t = threadIdx.x;
+  uint32_t k[ITEMS];
+  int64_t v[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = (int64_t)t * ITEMS + i;
+    if (idx < n) {
+      const int64_t r = rows ? rows[idx] : idx;
+      k[i] = (uint32_t)ld_int(keys + (size_t)r * width, dtype) + bias;
+      v[i] = r;
+    } else {
+      k[i] = 0xFFFFFFFFu;  // padding: stable, so it stays behind every real row with the same key
+      v[i] = -1;
+    }
+  }
+  typename B::Sort(tmp.sort).Sort(k, v);  // blocked arrangement, ascending, stable
+  last_key[t] = k[ITEMS - 1];
+  __syncthreads();
+  int flag[ITEMS];
+  int nf = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t p = (int64_t)t * ITEMS + i;
+    const uint32_t prev = i > 0 ? k[i - 1] : (t > 0 ? last_key[t - 1] : 0u);
+    flag[i] = (p < n && (p == 0 || k[i] != prev)) ? 1 : 0;
+    nf += flag[i];
+  }
+  int g0, total;
+  typename B::Scan(tmp.scan).ExclusiveSum(nf, g0, total);
+  int g = g0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t p = (int64_t)t * ITEMS + i;
+    if (p < n) group_rows[p] = v[i];
+    if (flag[i]) {
+      uk[g] = bias ? (long long)(int32_t)(k[i] - bias) : (long long)k[i];
+      start[g] = p;
+      ++g;
+    }
+  }
+  if (t == 0) start[total] = n;
+  __syncthreads();  // every group start is written (global, same block)
+  long long most = 0;
+  for (int gg = t; gg < total; gg += kBuildSmallThreads) {
+    const long long c = __ldcg(start + gg + 1) - __ldcg(start + gg);
+    counts[gg] = c;
+    most = c > most ? c : most;
+  }
+  __syncthreads();
+  most = typename B::Reduce(tmp.reduce).Reduce(most, cub::Max());
+  if (t == 0) {
+    stats[0] = total;
+    stats[1] = total > 0 ? __ldcg(uk) : 0;
+    stats[2] = total > 0 ? __ldcg(uk + total - 1) : 0;
+    stats[3] = most;
+  }
+}
+
 __global__ void build_stats_kernel(const long long* __restrict__ unique_keys, const long long* __restrict__ num_runs,
                                    const long long* __restrict__ max_count, int64_t* __restrict__ stats) {
   const long long u = *num_runs;
@@ -758,8 +843,11 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
   if (n > 0 && temp_bytes < T.total) return fail(ESC_ERR_WORKSPACE, "hash build temp too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* t = static_cast<uint8_t*>(d_temp);
-  // counts are zeroed first: the scan and the max read past the u runs the encoder writes
-  cudaError_t e = cudaMemsetAsync(out_group_counts, 0, (size_t)(n + 1) * sizeof(int64_t), st);
+  // counts are zeroed first: the scan and the max read past the u runs the encoder writes (the
+  // one-block path below writes exactly the u counts it has)
+  const bool small_path = dtype_width(key_dtype) <= 4 && n > 0 && n <= (int64_t)esc::kBuildSmallThreads * 16;
+  cudaError_t e = small_path ? cudaSuccess
+                             : cudaMemsetAsync(out_group_counts, 0, (size_t)(n + 1) * sizeof(int64_t), st);
   if (e == cudaSuccess && n == 0) e = cudaMemsetAsync(out_stats, 0, 4 * sizeof(int64_t), st);
   if (e == cudaSuccess && n == 0) e = cudaMemsetAsync(out_group_start, 0, sizeof(int64_t), st);
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash build init: ") + cudaGetErrorString(e));
@@ -777,9 +865,26 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
   if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
   const int nn = (int)n;
   const int w = dtype_width(key_dtype);
+  const bool sgn = key_dtype == ESC_I8 || key_dtype == ESC_I16 || key_dtype == ESC_I32;
+  if (small_path) {  // one block does it all
+    const uint32_t bias = sgn ? 0x80000000u : 0u;
+    auto run = [&](auto kern, size_t smem) -> cudaError_t {
+      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e2 != cudaSuccess) return e2;
+      ++g_launches;
+      kern<<<1, esc::kBuildSmallThreads, smem, st>>>(static_cast<const uint8_t*>(keys), key_dtype, w, rows, n, bias,
+                                                     out_group_rows, reinterpret_cast<long long*>(out_unique_keys),
+                                                     reinterpret_cast<long long*>(out_group_counts),
+                                                     reinterpret_cast<long long*>(out_group_start), out_stats);
+      return cudaGetLastError();
+    };
+    e = n <= (int64_t)esc::kBuildSmallThreads * 8 ? run(esc::build_small_kernel<8>, esc::BuildSmall<8>::kSmem)
+                                                   : run(esc::build_small_kernel<16>, esc::BuildSmall<16>::kSmem);
+    if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("small hash build: ") + cudaGetErrorString(e));
+    return ESC_OK;
+  }
   if (w <= 4) {
     // stable (LSD radix) sort of 32-bit biased keys: equal keys keep ascending build-row order
-    const bool sgn = key_dtype == ESC_I8 || key_dtype == ESC_I16 || key_dtype == ESC_I32;
     const uint32_t bias = sgn ? 0x80000000u : 0u;
     uint32_t* k32_in = reinterpret_cast<uint32_t*>(keys_in);
     uint32_t* k32_sorted = reinterpret_cast<uint32_t*>(keys_sorted);

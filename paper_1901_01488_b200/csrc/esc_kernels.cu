@@ -25,6 +25,9 @@
 // Tiles that are not staged (tail tile, row-id selections, unaligned columns) run a separate,
 // cold, bounds-checked evaluator.
 #include <cuda_runtime.h>
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_run_length_encode.cuh>

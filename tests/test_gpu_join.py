@@ -229,9 +229,11 @@ def test_build_indexes_batch_equals_single_builds(cuda):
 
     g = np.random.default_rng(41)
     specs = []
-    for i, (kind, dt, lo, hi) in enumerate((("INT8", np.int8, -100, 100), ("INT16", np.int16, -3000, 3000),
-                                            ("INT32", np.int32, -10**6, 10**6), ("INT64", np.int64, -10**12, 10**12))):
-        n = 5000 + 17 * i
+    # sizes on both sides of the one-block path (<= 16384 rows with keys of <= 4 bytes)
+    for i, (kind, dt, lo, hi, n) in enumerate((("INT8", np.int8, -100, 100, 5000), ("INT16", np.int16, -3000, 3000, 9000),
+                                               ("INT32", np.int32, -10**6, 10**6, 16384),
+                                               ("INT32", np.int32, -2**31, 2**31 - 1, 50_021),
+                                               ("INT64", np.int64, -10**12, 10**12, 7000))):
         k = g.integers(lo, hi, n).astype(dt)
         k[::7] = k[::5][: len(k[::7])]  # duplicates
         nulls = g.random(n) < 0.05
