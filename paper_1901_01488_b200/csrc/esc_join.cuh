@@ -868,9 +868,13 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
   const bool sgn = key_dtype == ESC_I8 || key_dtype == ESC_I16 || key_dtype == ESC_I32;
   if (small_path) {  // one block does it all
     const uint32_t bias = sgn ? 0x80000000u : 0u;
-    auto run = [&](auto kern, size_t smem) -> cudaError_t {
-      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e2 != cudaSuccess) return e2;
+    static std::atomic<int> configured{0};  // bit per instantiation: the attribute is set once
+    auto run = [&](auto kern, size_t smem, int bit) -> cudaError_t {
+      if (!(configured.load() & bit)) {
+        const cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e2 != cudaSuccess) return e2;
+        configured.fetch_or(bit);
+      }
       ++g_launches;
       kern<<<1, esc::kBuildSmallThreads, smem, st>>>(static_cast<const uint8_t*>(keys), key_dtype, w, rows, n, bias,
                                                      out_group_rows, reinterpret_cast<long long*>(out_unique_keys),
@@ -878,8 +882,8 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
                                                      reinterpret_cast<long long*>(out_group_start), out_stats);
       return cudaGetLastError();
     };
-    e = n <= (int64_t)esc::kBuildSmallThreads * 8 ? run(esc::build_small_kernel<8>, esc::BuildSmall<8>::kSmem)
-                                                   : run(esc::build_small_kernel<16>, esc::BuildSmall<16>::kSmem);
+    e = n <= (int64_t)esc::kBuildSmallThreads * 8 ? run(esc::build_small_kernel<8>, esc::BuildSmall<8>::kSmem, 1)
+                                                   : run(esc::build_small_kernel<16>, esc::BuildSmall<16>::kSmem, 2);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("small hash build: ") + cudaGetErrorString(e));
     return ESC_OK;
   }

@@ -58,3 +58,14 @@ pr = cProfile.Profile(); pr.enable()
 for _ in range(50): eng.run(q)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+
+# build phase split
+import paper_1901_01488_b200.join as J
+acc.clear()
+timed(J, "HashTableIndex", "  HashTableIndex (ctor)")
+timed(J.HashTableIndex, "_finish", "  _finish")
+from paper_1901_01488_b200 import executor
+timed(executor, "eval_predicate", "  eval_predicate")
+timed(J, "build_indexes", "build_indexes")
+for _ in range(20): eng.run(q)
+for k, v in acc.items(): print(f"  {k:28s} {v / 20 * 1e3:8.3f} ms")
