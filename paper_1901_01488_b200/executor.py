@@ -454,6 +454,15 @@ def eval_predicate(table: ColumnTable, pred: ex.Expr | None,
         selection = RowSelection(table)
     if pred is None:
         return selection
+    n = table.row_count
+    if selection.indices is None and 0 < n <= ONEPASS_MAX_ROWS:
+        # small tables: ONE launch of the look-back kernel writes the row ids (select + the
+        # compaction chain would be five launches and two waits)
+        cp = compile_predicate(table, pred)
+        count, fails, _, _, rows = launch_compact(cp, table, None, n, [], n, want_row_ids=True)
+        if cp.unbound or cp.may_fail:
+            raise_udf_errors(table, cp, fails, None, n)
+        return RowSelection(table, rows[:count])
     sel = select(table, pred, selection)
     _, _, rows = launch_materialize_selection(sel, [], sel.count, want_row_ids=True)
     return RowSelection(table, rows)
