@@ -1319,8 +1319,16 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* 
   pdl_trigger();
   if (skip_materialize(rule)) return;
   if (threadIdx.x < 32) {  // one warp sums the earlier blocks' partials (independent loads in flight)
-    unsigned long long c = 0;
-    for (unsigned b = threadIdx.x; b < blockIdx.x; b += 32) c += partial[b];
+    unsigned long long c = 0, c1 = 0, c2 = 0, c3 = 0;  // four independent loads in flight per lane
+    unsigned b = threadIdx.x;
+    for (; b + 96 < blockIdx.x; b += 128) {
+      c += __ldcg(partial + b);
+      c1 += __ldcg(partial + b + 32);
+      c2 += __ldcg(partial + b + 64);
+      c3 += __ldcg(partial + b + 96);
+    }
+    for (; b < blockIdx.x; b += 32) c += __ldcg(partial + b);
+    c += c1 + c2 + c3;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
     if (threadIdx.x == 0) carry = c;
