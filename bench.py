@@ -31,6 +31,10 @@ sys.path.insert(0, ROOT)
 
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only when MEASURED_PEAKS.json is absent
 L2_BYTES = 126 * 2**20
+# ONE metric string for both arms (the driver divides the arms' values only when metric, unit and
+# direction agree); "fused" vs "reference" is in each line's `impl` / `config`
+METRIC = "rows/s (ESC sub-query: scan+count+compaction)"
+PARITY_CHUNK = 2_500_000  # rows per reference-port task (np.frompyfunc object arrays stay ~200 MB)
 
 
 def parse_args():
@@ -45,6 +49,7 @@ def parse_args():
     p.add_argument("--no-extras", action="store_true")
     p.add_argument("--sweep", default="", help="write the config-5 selectivity sweep JSON here")
     p.add_argument("--cpu-sample-rows", type=int, default=0)
+    p.add_argument("--no-parity", action="store_true", help="skip the full-shard parity check")
     return p.parse_args()
 
 
@@ -147,24 +152,41 @@ def _cpu_chunk(bounds):
     return count, [mat[c].values for c in st["project"]]
 
 
-def cpu_reference_run(cols: dict, pred, project, udfs, rows: int, procs: int, reps: int = 1):
-    """Time the reference algorithm (count sub-query + materialization) over ``rows`` rows split
-    into ``procs`` contiguous chunks run in parallel processes; returns (seconds per rep, count)."""
+def cpu_reference_run(cols: dict, pred, project, udfs, rows: int, procs: int, reps: int = 1,
+                      row_begin: int = 0, chunk: int = 0):
+    """Run the reference algorithm (count sub-query + materialization; the numpy port of
+    executor.count_star + optimizer.materialize_pushdown) over rows [row_begin, row_begin+rows)
+    in a pool of ``procs`` processes.  The range is cut into ``procs`` contiguous chunks, or into
+    ``chunk``-row tasks when given (the reference's own row-range concept, executor.py:485-504:
+    counts add up, chunk results concatenate in row order).  Returns (seconds per rep, count);
+    ``cpu_reference_run.last_columns`` holds the materialised columns of the last rep."""
     import multiprocessing as mp
 
-    _CPU_STATE.update(cols={k: v[:rows] for k, v in cols.items()}, pred=pred, project=project, udfs=udfs)
-    bounds = [((i * rows) // procs, ((i + 1) * rows) // procs) for i in range(procs)]
+    _CPU_STATE.update(cols=cols, pred=pred, project=project, udfs=udfs)
+    hi = row_begin + rows
+    if chunk:
+        bounds = [(lo, min(lo + chunk, hi)) for lo in range(row_begin, hi, chunk)]
+    else:
+        bounds = [(row_begin + (i * rows) // procs, row_begin + ((i + 1) * rows) // procs) for i in range(procs)]
     ctx = mp.get_context("fork")
     times, count = [], 0
     with ctx.Pool(procs) as pool:
         for _ in range(reps):
             t0 = time.perf_counter()
-            res = pool.map(_cpu_chunk, bounds)
+            res = pool.map(_cpu_chunk, bounds, chunksize=1)
             times.append(time.perf_counter() - t0)
             count = sum(r[0] for r in res)
-    # the materialised columns of the sample, chunks concatenated in row order (parity digest)
+    # the materialised columns, chunks concatenated in row order (parity digest)
     cpu_reference_run.last_columns = [np.concatenate([r[1][k] for r in res]) for k in range(len(project))]
     return times, count
+
+
+def full_parity_reference(cols: dict, pred, project, udfs, rows: int, procs: int):
+    """The reference port over EVERY row of this rank's shard (2.5M-row tasks in ``procs``
+    processes, outside any timed region): (count, digest of the materialised columns, seconds)."""
+    t0 = time.perf_counter()
+    _, count = cpu_reference_run(cols, pred, project, udfs, rows, procs, reps=1, chunk=PARITY_CHUNK)
+    return count, columns_digest(cpu_reference_run.last_columns), time.perf_counter() - t0
 
 
 def columns_digest(arrays) -> str:
@@ -183,17 +205,41 @@ def default_cpu_rows(procs: int) -> int:
 
 
 # ------------------------------------------------------------------------------------------------
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # `bench.py --gpus N` on its own: re-launch as N ranks, one process per GPU (what the
+        # driver's torchrun launch does), each rank reading RANK/LOCAL_RANK/WORLD_SIZE
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU"}),
+              flush=True)
+        return 2
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, max(world, args.gpus))
     return run_ours(args, rank, world, local_rank)
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the reference's CPU algorithm for this path (the numpy port in oracle/,
+    pinned to the reference's own outputs) on the host cores, on our arm's workload, metric and
+    unit.  Each step = the count sub-query + materialization over a bounded sample of config 4's
+    rows in every host core (contiguous row ranges, one process each); the single-core figure
+    (the reference as it ships: single-threaded numpy) is timed beside it."""
     if rank != 0:
         return 0
     from paper_1901_01488_b200 import datagen
@@ -206,21 +252,30 @@ def run_reference(args, rank, world):
     timed = times[args.warmup:]
     per_step = sum(timed) / len(timed)
     value = rows / per_step
+    one_rows = rows // procs
+    t1, _ = cpu_reference_run(cols, w.pred, w.project, w.udfs, one_rows, 1, reps=2)
+    single = {"value": one_rows / min(t1), "unit": "rows/s", "cores": 1, "kind": "port",
+              "sample": f"first {one_rows} rows of config 4 in ONE process (the reference ships single-threaded)"}
     line = {
-        "impl": "reference", "metric": "rows/s (ESC sub-query: scan+count+compaction)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "rows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "i32+f32+f64", "data": "synthetic (block-seeded Appendix B config-4 recipe)",
-        "config": {"workload": "config4 (BASELINE configs[3]) bounded sample", "rows_total": args.rows,
-                   "sample_rows": rows, "sample_count": count},
+        "config": {"workload": CONFIG4_WORKLOAD, "rows_total": args.rows, "sample_rows": rows,
+                   "sample_count": count},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": "port",
                          "sample": f"first {rows} rows of config 4, {procs} processes x contiguous row ranges; "
                                    "numpy port of executor.count_star + optimizer.materialize_pushdown "
-                                   "(Python UDF via np.frompyfunc)"},
+                                   "(Python UDF via np.frompyfunc)",
+                         "single_core": single},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+CONFIG4_WORKLOAD = ("config4: 600M-row table, A=x AND C BETWEEN -0.5 AND 1.0 AND (D=17 OR D>900) AND udf(B,D)>3; "
+                    "count + compaction of (A,C,D)")
 
 
 def run_ours(args, rank, world, local_rank):
@@ -241,18 +296,25 @@ def run_ours(args, rank, world, local_rank):
     w = datagen.config4_blocked(n, lo, hi, out={k: v.numpy() for k, v in pinned.items()}, threads=threads)
     gen_s = time.perf_counter() - t0
 
-    # CPU baseline BEFORE any CUDA context exists (the pool forks)
+    # CPU work BEFORE any CUDA context exists (the pools fork): the baseline on a bounded sample
+    # (rank 0, N = 1) and the parity reference over EVERY row of this rank's shard
     cpu_baseline, cpu_parity = None, None
+    cols = {k: v[1] for k, v in w.columns.items()}
+    procs = max(1, (os.cpu_count() or 1) // world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        procs = os.cpu_count() or 1
         rows = min(m, args.cpu_sample_rows or default_cpu_rows(procs))
-        cols = {k: v[1] for k, v in w.columns.items()}
-        times, cpu_count = cpu_reference_run(cols, w.pred, w.project, w.udfs, rows, procs, reps=2)
+        times, _ = cpu_reference_run(cols, w.pred, w.project, w.udfs, rows, procs, reps=2)
         per = min(times[1:]) if len(times) > 1 else times[0]
+        one_rows = rows // procs
+        t1, _ = cpu_reference_run(cols, w.pred, w.project, w.udfs, one_rows, 1, reps=2)
         cpu_baseline = {"value": rows / per, "unit": "rows/s", "cores": procs, "kind": "port",
                         "sample": f"first {rows} rows of this config-4 shard; numpy port of the reference "
-                                  f"(count sub-query + materialization) in {procs} processes"}
-        cpu_parity = (rows, cpu_count, columns_digest(cpu_reference_run.last_columns))
+                                  f"(count sub-query + materialization) in {procs} processes",
+                        "single_core": {"value": one_rows / min(t1), "unit": "rows/s", "cores": 1, "kind": "port",
+                                        "sample": f"first {one_rows} rows in ONE process (the reference ships "
+                                                  "single-threaded)"}}
+    if not args.no_parity:
+        cpu_parity = full_parity_reference(cols, w.pred, w.project, w.udfs, m, procs)
 
     import torch.distributed as dist
 
@@ -267,33 +329,6 @@ def run_ours(args, rank, world, local_rank):
     pred = serde.from_json(w.pred, "t", w.udfs)
     cfg = optimizer.EscConfig()
 
-    def make_table():
-        return ColumnTable("t", [Column(k, parse_kind(w.columns[k][0]), pinned[k].to(dev, non_blocking=True))
-                                 for k in "ABCD"])
-
-    table = make_table()
-    torch.cuda.synchronize()
-    cat = Catalog()
-    cat.register(table)
-    st = multigpu.ShardedTable("t", table, n, lo, rank, world)
-
-    parity = None
-    if cpu_parity is not None:  # the device path on the same sample: count and row-order digest
-        srows, scount, sdigest = cpu_parity
-        sample = ColumnTable("t", [Column(c.name, c.kind, c.values[:srows]) for c in table.columns])
-        dcount, dcols = executor.count_and_materialize(sample, pred, list(w.project), srows)
-        ddigest = columns_digest([c.values.cpu().numpy() for c in dcols])
-        parity = {"sample_rows": srows, "count_reference_port": scount, "count_device": dcount,
-                  "rows_digest_equal": ddigest == sdigest, "bit_exact": dcount == scount and ddigest == sdigest}
-
-    def step():
-        if world > 1:
-            d = multigpu.sharded_esc_subquery(st, pred, w.project, cfg)
-            return d.exact_count, d.local_count
-        d = optimizer.esc_subquery(cat, "t", pred, w.project, cfg)
-        cat.temps.sweep()
-        return d.exact_count, d.exact_count
-
     def barrier():
         if world > 1:
             dist.barrier()
@@ -305,6 +340,41 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def make_table():
+        return ColumnTable("t", [Column(k, parse_kind(w.columns[k][0]), pinned[k].to(dev, non_blocking=True))
+                                 for k in "ABCD"])
+
+    table = make_table()
+    torch.cuda.synchronize()
+    cat = Catalog()
+    cat.register(table)
+    st = multigpu.ShardedTable("t", table, n, lo, rank, world)
+
+    def step(keep: bool = False):
+        if world > 1:
+            d = multigpu.sharded_esc_subquery(st, pred, w.project, cfg)
+            return d.exact_count, d.local_count, d.columns
+        d = optimizer.esc_subquery(cat, "t", pred, w.project, cfg)
+        cols_ = cat.resolve_temp(d.temp).columns if keep and d.temp is not None else None
+        cat.temps.sweep()
+        return d.exact_count, d.exact_count, cols_
+
+    parity = None
+    if cpu_parity is not None:
+        # the device step over the WHOLE shard vs the reference port over the whole shard: the
+        # count and the digest of the materialised (A, C, D) slice; counts are additive and the
+        # ranks' slices concatenate in rank order, so per-rank equality is global equality
+        scount, sdigest, ssec = cpu_parity
+        _, dcount, dcols = step(keep=True)
+        ddigest = columns_digest([c.values.cpu().numpy() for c in dcols]) if dcols is not None else None
+        ok = dcount == scount and ddigest == sdigest
+        all_ok = ok if world == 1 else bool(max_over_ranks(0.0 if ok else 1.0) == 0.0)
+        parity = {"sample_rows": m, "rows": m, "count_reference_port": scount, "count_device": dcount,
+                  "rows_digest_equal": ddigest == sdigest, "bit_exact": ok, "all_ranks_bit_exact": all_ok,
+                  "reference_s": round(ssec, 1), "reference_procs": procs,
+                  "note": "every row of this rank's shard through the reference port (2.5M-row tasks), "
+                          "outside the timed region"}
 
     for _ in range(args.warmup):
         step()
@@ -318,7 +388,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        total, local = step()
+        total, local, _ = step()
     e1.record(stream)
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
@@ -394,12 +464,11 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0:
         line = {
-            "metric": "rows/s (ESC sub-query: fused scan+count+compaction)",
+            "metric": METRIC,
             "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "i32+f32+f64", "data": "synthetic (block-seeded Appendix B config-4 recipe)",
-            "config": {"workload": "config4: 600M-row table, A=x AND C BETWEEN -0.5 AND 1.0 AND (D=17 OR D>900) "
-                                   "AND udf(B,D)>3; count + compaction of (A,C,D)",
+            "config": {"workload": CONFIG4_WORKLOAD, "impl_note": "fused device scan+count+compaction",
                        "rows": n, "rows_per_gpu": m, "count": total, "selectivity": total / n,
                        "l2": f"inputs {m * 16 / 1e9:.1f} GB per GPU >> L2 (126 MB): no flush needed",
                        "parallelism": f"row-partitioned x{world}, NCCL all_gather of counts",
@@ -635,6 +704,24 @@ def _star_cpu_baseline(eng, plan_, res, sample_rows: int = 6_000_000):
                       f"executor.probe_joins, numpy); sample COUNT {stage[-1]}"}
 
 
+def _port_count_threads(cols: dict, pred) -> int:
+    """The reference port's count_star over every row, 2.5M-row chunks on the host threads
+    (numpy releases the GIL in the comparisons): the full-size parity pin of a sweep point."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import esc_oracle as O
+
+    n = len(next(iter(cols.values())))
+
+    def one(lo):
+        hi = min(lo + PARITY_CHUNK, n)
+        t = O.OTable("t", {k: O.OColumn(v[lo:hi], np.zeros(hi - lo, bool)) for k, v in cols.items()})
+        return O.count_star(t, pred, {})
+
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        return sum(ex.map(one, range(0, n, PARITY_CHUNK)))
+
+
 def run_sweep(args, dev, peak):
     """Config 5: single-range and 4-column conjunctive predicates at six selectivities, count-only
     vs fused count+compaction of (c0, c1, c4, c5); HBM GB/s vs selectivity."""
@@ -647,6 +734,7 @@ def run_sweep(args, dev, peak):
     n = args.rows
     w = datagen.config5_blocked(n, 0.01)
     t = ColumnTable("t", [Column(k, parse_kind(v[0]), v[1], device=dev) for k, v in w.columns.items()])
+    host = {k: v[1] for k, v in w.columns.items() if int(k[1]) < 4}  # the predicate columns (parity)
     del w
     res = []
     for conj4 in (False, True):
@@ -674,7 +762,9 @@ def run_sweep(args, dev, peak):
             pw = [t.column(c).values.element_size() for c in wl.project]
             lines = sum(n * w * (1.0 - (1.0 - se) ** (128 // w)) for w in pw)
             floor = bc + n / 4 + lines + k * sum(pw)
+            ref_k = _port_count_threads(host, wl.pred)
             res.append({"pred": "conj4" if conj4 else "single", "s": s, "count": k, "count_ms": cms,
+                        "count_reference_port": ref_k, "bit_exact": ref_k == k,
                         "count_GBps": bc / cms / 1e6, "count_frac": bc / cms / 1e6 / peak,
                         "compact_ms": mms, "compact_GBps": bm / mms / 1e6, "compact_frac": bm / mms / 1e6 / peak,
                         "line_floor_ms": floor / peak / 1e6, "line_floor_frac": floor / peak / 1e6 / mms})

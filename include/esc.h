@@ -255,6 +255,10 @@ typedef struct {
   uint8_t* cap_nulls[ESC_MAX_PROJ]; /* in: null bytes per capture, or NULL                */
   uint64_t* d_count;                /* in: optional device word; the scan stores the exact count
                                        there when it completes (ESC_OUT_SKIP_OVER_CAPACITY) */
+  const uint64_t* d_gate;           /* in: optional device word the materialisation's
+                                       ESC_OUT_SKIP_OVER_CAPACITY test reads INSTEAD of d_count —
+                                       written between the scan and the compaction by
+                                       esc_count_gate (multi-GPU: the GLOBAL count decides) */
 } esc_selection_t;
 
 /* Upper bounds of the selection buffers for `nrows` rows: bitmap words, segments (seg_counts
@@ -293,6 +297,20 @@ int esc_step_plan_launch(void* plan, int32_t parts, void* stream); /* parts: 1 s
 int esc_step_plan_rebind(void* plan, const esc_outputs_t* outs); /* one-pass plans; same n_proj,
                                                                      slots, capacity, null outputs */
 int esc_step_plan_destroy(void* plan);
+
+/* ---- multi-GPU row partitioner (K3) ------------------------------------------
+ * Rank r of G holds rows [floor(r*N/G), floor((r+1)*N/G)) of a table (the reference's np.linspace
+ * row-range split, executor.py:485-489).  After an all_gather of the ranks' device counts (int64
+ * each, rank order; NCCL on the same stream), ONE thread folds them on the device:
+ *   out[0] = global count  (sum)                 -> the push-down decision (optimizer.py:171-177)
+ *   out[1] = exclusive offset of rank `rank`     -> where this rank's compacted slice starts in the
+ *                                                   global, order-preserving temp (executor.py:500-504)
+ *   out[2] = gate: 0 when the global count <= capacity, else 2^62 (> any capacity) — pointed to
+ *            by esc_selection_t.d_gate, it makes the queued compaction of a table that does not
+ *            qualify GLOBALLY a no-op on every rank.
+ * No host round trip between the scan, the exchange and the compaction. */
+int esc_count_gate(const int64_t* counts, int32_t world, int32_t rank, int64_t capacity, int64_t* out,
+                   void* stream);
 
 /* out[i] = col[idx[i]] (values and, when present, nulls).  replaces Column.take
  * (storage.py:176-184). */

@@ -86,7 +86,7 @@ class EscSelection(C.Structure):
     _fields_ = [("bitmap", C.c_void_p), ("seg_counts", C.c_void_p), ("seg_rows", C.c_int32),
                 ("cap_per_seg", C.c_int32), ("n_cap", C.c_int32), ("cap_stride", C.c_int32),
                 ("cap_slot", C.c_int32 * MAX_PROJ), ("cap_values", C.c_void_p * MAX_PROJ),
-                ("cap_nulls", C.c_void_p * MAX_PROJ), ("d_count", C.c_void_p)]
+                ("cap_nulls", C.c_void_p * MAX_PROJ), ("d_count", C.c_void_p), ("d_gate", C.c_void_p)]
 
 
 MAX_STEPS = 8
@@ -132,6 +132,7 @@ _SIGNATURES = {
                                             C.c_void_p]),
     "esc_gather": (C.c_int, [C.POINTER(EscColumn), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                              C.c_void_p]),
+    "esc_count_gate": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p]),
     "esc_last_error": (C.c_char_p, []),
     "esc_launch_count": (C.c_int64, []),
     "esc_abi_version": (C.c_int, []),

@@ -72,8 +72,8 @@ class Catalog:
         return sorted(self._tables)
 
     # -- temp tables ----------------------------------------------------------------------------
-    def materialize_temp(self, columns: list[Column]) -> TempTableHandle:
-        return self.temps.materialize(columns)
+    def materialize_temp(self, columns: list[Column], shard=None) -> TempTableHandle:
+        return self.temps.materialize(columns, shard)
 
     def resolve_temp(self, handle: TempTableHandle) -> ColumnTable:
         return self.temps.resolve(handle)

@@ -1957,6 +1957,28 @@ __global__ void __launch_bounds__(256) copy_regions_kernel(const __grid_constant
   }
 }
 
+// ---- multi-GPU count gate (esc_count_gate): one warp folds the all-gathered per-rank counts ----
+__global__ void __launch_bounds__(32) count_gate_kernel(const int64_t* __restrict__ counts, int world, int rank,
+                                                        long long capacity, int64_t* __restrict__ out) {
+  const int lane = threadIdx.x;
+  unsigned long long total = 0, before = 0;
+  for (int r = lane; r < world; r += 32) {
+    const unsigned long long c = (unsigned long long)counts[r];
+    total += c;
+    if (r < rank) before += c;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    total += __shfl_xor_sync(0xFFFFFFFFu, total, d);
+    before += __shfl_xor_sync(0xFFFFFFFFu, before, d);
+  }
+  if (lane == 0) {
+    out[0] = (int64_t)total;
+    out[1] = (int64_t)before;
+    out[2] = total <= (unsigned long long)capacity ? 0 : (int64_t)(1ull << 62);
+  }
+}
+
 // gather: out[i] = col[idx[i]]
 template <typename T>
 __global__ void gather_kernel(const T* __restrict__ src, const uint8_t* __restrict__ nulls,

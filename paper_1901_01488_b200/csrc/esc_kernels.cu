@@ -108,19 +108,30 @@ int sm_count_cached() {
   return n;
 }
 
-// per-workspace epoch for the look-back status words (host side; guarded)
+// per-workspace epoch for the look-back status words (host side; guarded), and the most status
+// words any one-pass launch on that workspace has used (all of them end at the workspace's end)
 std::mutex g_epoch_mu;
-std::unordered_map<const void*, uint32_t> g_epochs;
+struct EpochState {
+  uint32_t epoch = 0;
+  size_t max_words = 0;
+};
+std::unordered_map<const void*, EpochState> g_epochs;
 
 size_t status_words(int64_t nrows) {
   const int64_t t = (int64_t)kConsumerWarps * kChunkRows;  // smallest tile
   return (size_t)((nrows + t - 1) / t) + 1;
 }
 
-// Workspace layout: [header][tile status (one-pass K2)][segment offsets u64][scan partials u64]
-//                   [segment counts u32][selection bitmap u32][dense-tile counter + list u32]
+// Workspace layout: [header][segment offsets u64][scan partials u64][segment counts u32]
+//                   [selection bitmap u32][dense-tile counter + list u32] ... [tile status u64]
+// The one-pass kernel's tile status words sit at the END of the workspace, whatever its size
+// (status_base): every other region is a prefix whose extent grows with nrows, the status words a
+// suffix that does too, and esc_workspace_bytes(n) covers both, so for any two launches of
+// n_a, n_b <= the workspace's capacity the prefix regions of one never overlap the status words of
+// the other — a smaller table's offsets/bitmap can never leave words that a later look-back
+// might take for a published status (they carry a 16-bit epoch tag, see next_epoch).
 struct WsLayout {
-  size_t status, offsets, partials, counts, bitmap, dense, total;
+  size_t offsets, partials, counts, bitmap, dense, total;
   int64_t max_tiles, bitmap_words;
 };
 WsLayout ws_layout(int64_t nrows) {
@@ -132,14 +143,18 @@ WsLayout ws_layout(int64_t nrows) {
   L.bitmap_words = ((nrows + t_max - 1) / t_max + 1) * (t_max / 32);  // covers every C's last tile
   const int64_t segs = L.max_tiles / kScanSeg + 2;
   auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  L.status = sizeof(WsHeader);
-  L.offsets = up(L.status + status_words(nrows) * 8);
+  L.offsets = up(sizeof(WsHeader));
   L.partials = up(L.offsets + (size_t)L.max_tiles * 8);
   L.counts = up(L.partials + (size_t)segs * 8);
   L.bitmap = up(L.counts + (size_t)L.max_tiles * 4);
   L.dense = up(L.bitmap + (size_t)L.bitmap_words * 4);
-  L.total = up(L.dense + 256 + (size_t)L.max_tiles * 4);
+  L.total = up(L.dense + 256 + (size_t)L.max_tiles * 4) + up(status_words(nrows) * 8);
   return L;
+}
+
+unsigned long long* status_base(void* d_ws, size_t ws_bytes, int64_t nrows) {
+  uint8_t* end = static_cast<uint8_t*>(d_ws) + (ws_bytes & ~(size_t)7);
+  return reinterpret_cast<unsigned long long*>(end - status_words(nrows) * 8);
 }
 
 int validate_program(const esc_program_t* prog, int32_t ncols) {
@@ -543,7 +558,7 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
   std::memcpy(kp.udf_ops, prog->udf_ops, sizeof(kp.udf_ops));
   kp.lut = prog->lut;
   kp.hdr = static_cast<WsHeader*>(d_ws);
-  kp.status = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(d_ws) + sizeof(WsHeader));
+  kp.status = status_base(d_ws, ws_bytes, nrows);
   kp.result = result;
   kp.trace = g_trace;
   return ESC_OK;
@@ -805,8 +820,10 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   sp.rule.skip_count = nullptr;
   sp.rule.skip_capacity = outs->capacity;
   if (outs->flags & ESC_OUT_SKIP_OVER_CAPACITY) {
-    if (sel->d_count == nullptr) return fail(ESC_ERR_INVALID, "ESC_OUT_SKIP_OVER_CAPACITY needs sel->d_count");
-    sp.rule.skip_count = reinterpret_cast<const unsigned long long*>(sel->d_count);
+    if (sel->d_count == nullptr && sel->d_gate == nullptr)
+      return fail(ESC_ERR_INVALID, "ESC_OUT_SKIP_OVER_CAPACITY needs sel->d_count or sel->d_gate");
+    sp.rule.skip_count = reinterpret_cast<const unsigned long long*>(sel->d_gate != nullptr ? sel->d_gate
+                                                                                             : sel->d_count);
   }
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
@@ -916,7 +933,7 @@ int esc_workspace_init(void* d_ws, size_t ws_bytes, void* stream) {
                         sizeof(unsigned long long) * ESC_MAX_UDFS, st);
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("workspace init: ") + cudaGetErrorString(e));
   std::lock_guard<std::mutex> g(g_epoch_mu);
-  g_epochs[d_ws] = 0;
+  g_epochs[d_ws] = EpochState();
   return ESC_OK;
 }
 
@@ -1009,15 +1026,19 @@ bool capture_parts(StepPlanImpl* p, int parts) {
 // next look-back epoch of a workspace (status words carry it, so they need no clearing per launch)
 int next_epoch(KParams& kp, int64_t nrows, void* d_ws, cudaStream_t stream) {
   std::lock_guard<std::mutex> g(g_epoch_mu);
-  uint32_t& ep = g_epochs[d_ws];
-  ep = (ep + 1) & 0xFFFFu;
-  if (ep == 0) {
-    // epoch wrapped: stale status words could alias, clear them
-    cudaError_t e = cudaMemsetAsync(kp.status, 0, status_words(nrows) * sizeof(unsigned long long), stream);
+  EpochState& es = g_epochs[d_ws];
+  const size_t words = status_words(nrows);
+  if (words > es.max_words) es.max_words = words;
+  es.epoch = (es.epoch + 1) & 0xFFFFu;
+  if (es.epoch == 0) {
+    // epoch wrapped: a word left by ANY earlier one-pass launch on this workspace (of any table
+    // size: they all end at the workspace's end) could alias the new epoch — clear all of them
+    unsigned long long* end = kp.status + words;
+    cudaError_t e = cudaMemsetAsync(end - es.max_words, 0, es.max_words * sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("status clear: ") + cudaGetErrorString(e));
-    ep = 1;
+    es.epoch = 1;
   }
-  kp.epoch = ep;
+  kp.epoch = es.epoch;
   return ESC_OK;
 }
 }  // namespace
@@ -1220,6 +1241,18 @@ int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const 
   copy_regions_kernel<<<dim3((unsigned)bx, (unsigned)n), 256, 0, static_cast<cudaStream_t>(stream)>>>(cr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("copy launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
+int esc_count_gate(const int64_t* counts, int32_t world, int32_t rank, int64_t capacity, int64_t* out,
+                   void* stream) {
+  if (counts == nullptr || out == nullptr) return fail(ESC_ERR_INVALID, "null count gate buffer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ESC_ERR_INVALID, "bad world / rank");
+  if (capacity < 0) return fail(ESC_ERR_INVALID, "negative capacity");
+  ++g_launches;
+  count_gate_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(counts, world, rank, capacity, out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("count gate launch: ") + cudaGetErrorString(e));
   return ESC_OK;
 }
 

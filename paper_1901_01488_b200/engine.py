@@ -1,5 +1,9 @@
 """Engine facade: one query at a time, temps never outlive the query.
 
+Multi-GPU: each rank runs its own Engine over its shards of the same tables (one process per GPU)
+and the same queries in the same order; :meth:`Engine.run` then plans on global counts and
+executes with :func:`.multigpu.execute_plan_sharded`.
+
 The reference ``Engine.run`` (``pkg/src/escdb/engine.py:56-77``) plans, executes, and sweeps every
 planner temp table in a ``finally``; its ESC overhead is ``sum(subquery_ms + materialize_ms)``.
 :meth:`Engine.run` does the same on the device (ESC sub-queries, then the hash-join pipeline of
@@ -67,12 +71,22 @@ class Engine:
         t0 = time.perf_counter()
         try:
             p = optimizer.plan(ra, self.catalog, self.config)
-            rows, count, stats = join.execute_plan(p, self.catalog, workers=self.workers)
+            if self._sharded(p):
+                from .multigpu import execute_plan_sharded
+
+                rows, count, stats = execute_plan_sharded(p, self.catalog, workers=self.workers)
+            else:
+                rows, count, stats = join.execute_plan(p, self.catalog, workers=self.workers)
             elapsed = (time.perf_counter() - t0) * 1000.0
         finally:
             self.catalog.temps.sweep()
         return QueryResult(count=count, rows=rows, plan=p, stats=stats, time_ms=elapsed,
                            overhead_ms=optimizer.esc_overhead_ms(p))
+
+    def _sharded(self, p) -> bool:
+        """Does the plan touch a row-partitioned table (multi-GPU: one Engine per rank, every
+        rank running the same query)?"""
+        return any(self.catalog.table(src).shard is not None for src in p.graph.source.values())
 
     def optimize(self, ra, keep_temps: bool = False) -> OptimizeResult:
         t0 = time.perf_counter()

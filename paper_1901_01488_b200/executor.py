@@ -528,10 +528,15 @@ class PendingStep:
 
 
 def launch_step(table: ColumnTable, pred: ex.Expr, needed, capacity: int, materialize: bool = True,
-                slot: int = 1) -> PendingStep:
+                slot: int = 1, between=None) -> PendingStep:
     """Queue one table's ESC step on the stream without waiting: K1 count (``materialize``
     False), the one-pass compaction (small tables) or K1 select + the queued compaction; the
-    kernels' result block is the workspace's pinned ``slot`` (1 .. N.RESULT_SLOTS)."""
+    kernels' result block is the workspace's pinned ``slot`` (1 .. N.RESULT_SLOTS).
+
+    ``between(plan, stream)`` (multi-GPU): on the queued path it is called after the scan and
+    before the compaction — it queues the count exchange and the device gate
+    (``plan.gate_buf``, :func:`gate_buffers`) that the compaction then reads instead of the local
+    count.  ``PendingStep.kind`` tells the caller whether it ran (``"queued"``)."""
     cp = compile_predicate(table, pred)
     n = table.row_count
     lib = N.load_library()
@@ -573,18 +578,33 @@ def launch_step(table: ColumnTable, pred: ex.Expr, needed, capacity: int, materi
             return PendingStep(table, None, proj, cap, "done", result=(sel.count, None))
         return PendingStep(table, None, proj, cap, "done", result=(sel.count, materialize_selection(sel, needed)))
     plan = _step_plan(cp, table, proj, cap, ws)
-    ckey = (slot, ws_ptr, N.TUNING[0])
+    gated = between is not None
+    ckey = (slot, ws_ptr, N.TUNING[0], gated)
     handle = plan.c_plans.get(ckey) if plan.c_plans is not None else None
     if handle is None:  # prepare the scan + compaction launches once (lowering, geometry, JIT lookup)
         h = C.c_void_p()
-        N.check(lib.esc_step_plan_create(C.byref(cp.program), cp.column_array(), cp.ncols, n, C.byref(plan.sel.desc),
-                                         plan.mat_cols, plan.mat_ncols, C.byref(plan.outs), res, C.c_void_p(ws_ptr),
-                                         C.c_size_t(ws_bytes), C.byref(h)), "esc_step_plan_create")
+        if gated:  # the compaction's skip test reads the gate word the exchange step writes
+            world = table.shard.world if table.shard is not None else None
+            plan.sel.desc.d_gate = gate_buffers(plan, table.device, world)[0][-1:].data_ptr()
+        try:
+            N.check(lib.esc_step_plan_create(C.byref(cp.program), cp.column_array(), cp.ncols, n,
+                                             C.byref(plan.sel.desc), plan.mat_cols, plan.mat_ncols, C.byref(plan.outs),
+                                             res, C.c_void_p(ws_ptr), C.c_size_t(ws_bytes), C.byref(h)),
+                    "esc_step_plan_create")
+        finally:
+            plan.sel.desc.d_gate = None
         handle = _CPlan(h.value, lib)
         if plan.c_plans is None:
             plan.c_plans = {}
         plan.c_plans[ckey] = handle
-    if KERNEL_EVENTS is None:
+    if gated:
+        for part, kind in ((1, "select"), (2, "materialize")):
+            ev0 = _ev_start(stream)
+            N.check(lib.esc_step_plan_launch(C.c_void_p(handle.ptr), part, sp), "esc_step_plan_launch")
+            _ev_end(stream, ev0, kind)
+            if part == 1:
+                between(plan, stream)
+    elif KERNEL_EVENTS is None:
         N.check(lib.esc_step_plan_launch(C.c_void_p(handle.ptr), 3, sp), "esc_step_plan_launch")
     else:  # profiling: events between the scan and the compaction
         for part, kind in ((1, "select"), (2, "materialize")):
@@ -661,8 +681,24 @@ class _StepPlan:
     mat_cols: object
     mat_ncols: int
     nbytes: int = 0
-    c_plans: dict | None = None   # (result slot, workspace) -> prepared esc_step_plan
+    c_plans: dict | None = None   # (result slot, workspace, tuning, gated) -> prepared esc_step_plan
     trim_cache: dict | None = None  # _trim's ctypes arguments (sources are the fixed outputs)
+    gate: tuple | None = None     # multi-GPU: (device int64[world + 3], pinned host copy)
+
+
+def gate_buffers(plan: _StepPlan, device: torch.device, world: int | None = None) -> tuple:
+    """The multi-GPU exchange buffers of a queued step plan: a device int64 vector
+    ``[counts of every rank (world) | global count, this rank's offset, gate]`` (esc_count_gate's
+    layout; the gate word is the last) and its pinned host copy.  The device buffer's address is
+    captured by the gated C plan, so it lives as long as the plan."""
+    if plan.gate is None:
+        if world is None:
+            import torch.distributed as dist
+
+            world = dist.get_world_size() if dist.is_initialized() else 1
+        dbuf = torch.zeros(world + 3, dtype=torch.int64, device=device)
+        plan.gate = (dbuf, torch.zeros(world + 3, dtype=torch.int64, pin_memory=True))
+    return plan.gate
 
 
 def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: int, ws) -> _StepPlan:

@@ -277,10 +277,35 @@ class Column:
         return vals, mask
 
 
-class ColumnTable:
-    """Immutable named relation of equal-length device columns (reference ``storage.py:206-244``)."""
+@dataclass(frozen=True)
+class ShardInfo:
+    """Where a row-partitioned table's local rows sit in the global table.
 
-    def __init__(self, name: str, columns: Sequence[Column], is_temporary: bool = False):
+    Rank ``rank`` of ``world`` holds global rows ``[offset, offset + counts[rank])``; ``counts``
+    lists every rank's rows in rank order, so the ranks' slices concatenated in rank order are the
+    global table in row order — the reference's chunk-order concatenation
+    (``executor.py:500-504``).  ``group`` is the ``torch.distributed`` process group the ranks
+    exchange counts over (None: the default group)."""
+
+    rank: int
+    world: int
+    offset: int
+    counts: tuple
+    group: object = field(default=None, compare=False)
+
+    @property
+    def global_rows(self) -> int:
+        return sum(self.counts)
+
+
+class ColumnTable:
+    """Immutable named relation of equal-length device columns (reference ``storage.py:206-244``).
+
+    ``shard`` (multi-GPU extension): this object holds ONE rank's contiguous row range of a
+    row-partitioned table; ``row_count`` is the local rows, :attr:`global_row_count` the table's."""
+
+    def __init__(self, name: str, columns: Sequence[Column], is_temporary: bool = False,
+                 shard: "ShardInfo | None" = None):
         columns = list(columns)
         if not columns:
             raise EmptySchema(f"table {name!r} must have at least one column")
@@ -299,6 +324,15 @@ class ColumnTable:
         self.row_count = sizes.pop()
         self.is_temporary = is_temporary
         self._by_name = {c.name: c for c in columns}
+        if shard is not None and shard.counts[shard.rank] != self.row_count:
+            raise LengthMismatch(f"table {name!r}: shard of rank {shard.rank} holds {self.row_count} rows, "
+                                 f"its ShardInfo says {shard.counts[shard.rank]}")
+        self.shard = shard
+
+    @property
+    def global_row_count(self) -> int:
+        """Rows of the whole table (all ranks' shards); ``row_count`` when not sharded."""
+        return self.shard.global_rows if self.shard is not None else self.row_count
 
     @classmethod
     def empty(cls, name: str, schema, device=None) -> "ColumnTable":
@@ -346,7 +380,10 @@ class ColumnTable:
 
 @dataclass(frozen=True)
 class TempTableHandle:
-    """Opaque handle of an optimizer temp table (reference ``storage.py:325-334``)."""
+    """Opaque handle of an optimizer temp table (reference ``storage.py:325-334``).
+
+    For a sharded temp (multi-GPU) ``row_count`` is the GLOBAL row count — what the planner
+    orders builds by — and every rank's handle has the same id (ranks plan in lockstep)."""
 
     id: int
     schema: tuple = field(compare=False)
@@ -364,12 +401,15 @@ class TempTableStore:
         self._next = 1
         self._tables: dict[int, ColumnTable] = {}
 
-    def materialize(self, columns: Sequence[Column]) -> TempTableHandle:
+    def materialize(self, columns: Sequence[Column], shard: ShardInfo | None = None) -> TempTableHandle:
+        """Register compacted columns as a temp.  ``shard``: they are this rank's slice of a
+        row-partitioned temp (the slices of all ranks, in rank order, are the temp); the handle
+        then carries the global row count."""
         tid = self._next
         self._next += 1
-        table = ColumnTable(f"$temp{tid}", columns, is_temporary=True)
+        table = ColumnTable(f"$temp{tid}", columns, is_temporary=True, shard=shard)
         self._tables[tid] = table
-        return TempTableHandle(tid, tuple((c.name, c.kind) for c in table.columns), table.row_count)
+        return TempTableHandle(tid, tuple((c.name, c.kind) for c in table.columns), table.global_row_count)
 
     def resolve(self, handle: TempTableHandle) -> ColumnTable:
         try:
