@@ -62,13 +62,16 @@ def peak_hbm():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def recorded_traffic(kind: str):
-    """dram bytes per launch from the committed ncu capture (profiles/traffic.json), or None."""
+def recorded_traffic(kind: str, rows: int, profiled_rows: int = 600_000_000):
+    """DRAM bytes per launch from the committed ncu capture (profiles/traffic.json, one launch
+    over ``profiled_rows`` rows), scaled to a launch over ``rows`` rows (a rank's shard); None
+    when absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(kind)
+            v = json.load(fh).get(kind)
     except (OSError, ValueError):
         return None
+    return None if v is None else v * rows / profiled_rows
 
 
 # ------------------------------------------------------------------------------------------------
@@ -322,10 +325,19 @@ def run_ours(args, rank, world, local_rank):
     from paper_1901_01488_b200.catalog import Catalog
     from paper_1901_01488_b200.storage import Column, ColumnTable, parse_kind
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # ESC_BENCH_BACKEND=gloo (plumbing checks on a one-GPU box only): every rank on cuda:0,
+    # counts exchanged through host memory — never a measurement configuration
+    backend = os.environ.get("ESC_BENCH_BACKEND", "nccl")
+    gpu = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    # ESC_BENCH_SHARDED=1 runs the multi-GPU step (device count exchange + gated compaction) even
+    # at N = 1 (a one-rank group): its fixed per-step cost against the single-GPU step
+    sharded = world > 1 or os.environ.get("ESC_BENCH_SHARDED") == "1"
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None, rank=rank, world_size=world)
     pred = serde.from_json(w.pred, "t", w.udfs)
     cfg = optimizer.EscConfig()
 
@@ -352,7 +364,7 @@ def run_ours(args, rank, world, local_rank):
     st = multigpu.ShardedTable("t", table, n, lo, rank, world)
 
     def step(keep: bool = False):
-        if world > 1:
+        if sharded:
             d = multigpu.sharded_esc_subquery(st, pred, w.project, cfg)
             return d.exact_count, d.local_count, d.columns
         d = optimizer.esc_subquery(cat, "t", pred, w.project, cfg)
@@ -384,7 +396,7 @@ def run_ours(args, rank, world, local_rank):
 
     launches0 = _native.load_library().esc_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local_rank).__enter__()  # sampled across every timed region below
+    clocks = ClockSampler(gpu).__enter__()  # sampled across every timed region below
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
@@ -422,7 +434,7 @@ def run_ours(args, rank, world, local_rank):
             t = make_table()                                    # H2D of this rank's shard
             c2 = Catalog()
             c2.register(t)
-            if world > 1:
+            if sharded:
                 d = multigpu.sharded_esc_subquery(multigpu.ShardedTable("t", t, n, lo, rank, world), pred,
                                                   w.project, cfg)
                 outs = d.columns or []
@@ -451,7 +463,7 @@ def run_ours(args, rank, world, local_rank):
 
     clocks.__exit__(None, None, None)
     if not clocks.lines:  # the device-timed region is ~20 ms: take one reading right after it
-        clocks.lines = ClockSampler.snapshot(local_rank)
+        clocks.lines = ClockSampler.snapshot(gpu)
     extras = {}
     if not args.no_extras and world == 1:
         extras = run_extras(table, w, pred, cfg, dev, peak)
@@ -471,10 +483,11 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": CONFIG4_WORKLOAD, "impl_note": "fused device scan+count+compaction",
                        "rows": n, "rows_per_gpu": m, "count": total, "selectivity": total / n,
                        "l2": f"inputs {m * 16 / 1e9:.1f} GB per GPU >> L2 (126 MB): no flush needed",
-                       "parallelism": f"row-partitioned x{world}, NCCL all_gather of counts",
+                       "parallelism": (f"row-partitioned x{world}, {backend.upper()} all_gather of counts" if sharded
+                                       else "1 GPU"),
                        "host_gen_s": round(gen_s, 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": recorded_traffic("select_config4"),
+                         "frac": achieved / peak, "traffic": recorded_traffic("select_config4", m),
                          "peak_source": peak_src,
                          "kernel": "esc_scan_kernel<C, false, JitPred> (K1: predicate + count + selection bitmap)",
                          "kernel_ms": kern_avg, "algorithmic_bytes": algo_bytes,
@@ -493,7 +506,7 @@ def run_ours(args, rank, world, local_rank):
             "extras": extras,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 
@@ -523,6 +536,31 @@ def _time_kernels(fn, reps, dev, flush=False):
     return [(a.elapsed_time(b), k) for a, b, k in ev]
 
 
+def _device_step_ms(launch, finish, reps, dev, flush=True) -> float:
+    """Median device time of ``launch()`` (kernels queued, no host wait inside): L2 flushed, then
+    a ~1 ms sleep kernel holds the stream while the host enqueues the events and the launches, so
+    the events bracket device work only; ``finish(result)`` after each rep."""
+    import torch
+
+    for _ in range(3):
+        r = launch()
+        torch.cuda.synchronize()
+        finish(r)
+    ts = []
+    for _ in range(reps):
+        if flush:
+            _flush_l2(dev)
+        torch.cuda._sleep(2_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = launch()
+        e1.record()
+        torch.cuda.synchronize()
+        finish(r)
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
 def run_extras(table, w, pred, cfg, dev, peak):
     """Secondary numbers: count-only K1 on config 4, config 2 (L2 flushed), config 3 ESC overhead."""
     import torch
@@ -549,13 +587,14 @@ def run_extras(table, w, pred, cfg, dev, peak):
     p2 = serde.from_json(w2.pred, "lineitem")
     d = optimizer.esc_subquery(c2, "lineitem", p2, w2.project, cfg)
     c2.temps.sweep()
-    tt = _time_kernels(lambda: (optimizer.esc_subquery(c2, "lineitem", p2, w2.project, cfg), c2.temps.sweep()),
-                       10, dev, flush=True)
-    kms = sum(x for x, k in tt if k in ("select", "materialize")) / 10
+    cap2 = (d.row_count * 1) // 5  # floor(0.2 * rows): the queued step's capacity
+    kms = _device_step_ms(lambda: executor.launch_step(t2, p2, w2.project, cap2), executor.finish_step, 15, dev)
     b2 = w2.algorithmic_bytes(d.exact_count)
     out["config2_fused"] = {"count": d.exact_count, "kernel_ms": kms, "rows_per_s": w2.nrows / (kms * 1e-3),
                             "GBps": b2 / (kms * 1e-3) / 1e9, "frac": b2 / (kms * 1e-3) / 1e9 / peak,
-                            "note": "L2 flushed before every rep"}
+                            "note": "device time of the queued step (K1 select + one-kernel mid-size compaction), "
+                                    "L2 flushed before every rep; a sleep kernel holds the stream while the step "
+                                    "is enqueued, so no host launch latency is inside the events"}
 
     # config 3: the 4-dimension star query — ESC overhead (reference definition, engine.py:69) and
     # the query executed end to end (Engine.run: ESC + hash builds over the temps + the fused

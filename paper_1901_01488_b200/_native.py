@@ -143,6 +143,7 @@ _SIGNATURES = {
     "esc_jit_stats": (C.c_int, [C.POINTER(C.c_int64)]),
     "esc_jit_selftest": (C.c_int, []),
     "esc_set_stream_div": (C.c_int, [C.c_int]),
+    "esc_set_mid_max_rows": (C.c_int64, [C.c_int64]),
     "esc_debug_trace": (C.c_int, [C.c_void_p]),
     "esc_copy_regions": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "esc_hash_insert": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
@@ -213,6 +214,13 @@ def set_jit(mode: int, min_rows: int = -1):
     """0 = interpreter only, 1 = JIT scans of >= min_rows rows, 2 = always JIT."""
     check(load_library().esc_set_jit(int(mode), int(min_rows)), "esc_set_jit")
     TUNING[0] += 1
+
+
+def set_mid_max_rows(rows: int) -> int:
+    """Largest selection (rows) compacted by the one-launch mid-size kernel (0: never); returns
+    the previous setting."""
+    TUNING[0] += 1
+    return int(load_library().esc_set_mid_max_rows(int(rows)))
 
 
 def set_stream_div(div: int) -> int:

@@ -40,7 +40,9 @@ struct WsHeader {
   unsigned long long done;    // CTAs finished (last-CTA detection)
   unsigned long long pad0;
   unsigned long long fail[ESC_MAX_UDFS];  // first failing row per UDF (packed), ~0 = none
-  unsigned long long pad1[4];
+  unsigned long long mid_ticket;  // sel_mid_kernel block tickets   (reset by its last block)
+  unsigned long long mid_done;    // sel_mid_kernel blocks past their prefix read (reset likewise)
+  unsigned long long pad1[2];
 };
 static_assert(sizeof(WsHeader) == 128, "header is one 128-byte line");
 
@@ -107,6 +109,9 @@ struct KParams {
   uint32_t rows_off;     // stage offset of the u16 row-index scratch (row-id outputs)
   unsigned long long* trace;  // diagnostics (esc_debug_trace): per-CTA %globaltimer stamps, or nullptr
   int32_t ticket_tiles;       // K1: consecutive tiles per ticket (>= ~128 KB of staged data per ticket)
+  int32_t prefetch_l2;        // K1 over a table whose staged bytes fit in L2: every CTA first asks L2 to
+                              // prefetch its static share of the full tiles (bulk prefetch), so DRAM
+                              // has the whole scan queued from the start instead of ramping with the ring
 };
 
 // Programmatic dependent launch: the compaction chain's kernels are launched with
@@ -157,6 +162,13 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
           smem_u32(smem_dst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+// L2 prefetch of [g, g + bytes) (16-byte aligned and sized), 64 KB per instruction
+__device__ __forceinline__ void bulk_prefetch_l2(const uint8_t* g, unsigned long long bytes) {
+  for (unsigned long long o = 0; o < bytes; o += 65536ull) {
+    const uint32_t n = (uint32_t)((bytes - o) < 65536ull ? (bytes - o) : 65536ull);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g + o), "r"(n) : "memory");
+  }
 }
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
@@ -887,6 +899,23 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
     // ===================== producer =====================
     if (lane == 0) {
       const uint64_t policy = evict_first_policy();
+      if (!COMPACT && p.prefetch_l2 && p.n_full_tiles > 0) {
+        // this CTA's static share of the full tiles' staged bytes, every column (16-byte units)
+        const int64_t rows = p.n_full_tiles * (int64_t)p.tile_rows;
+        const int64_t r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+        for (int i = 0; i < p.ncols; ++i) {
+          const KCol& col = p.cols[i];
+          if (col.staged) {
+            const unsigned long long a = ((unsigned long long)r0 * col.width) & ~15ull;
+            const unsigned long long b = ((unsigned long long)r1 * col.width) & ~15ull;
+            if (b > a) bulk_prefetch_l2(col.data + a, b - a);
+          }
+          if (col.nulls_staged) {
+            const unsigned long long a = (unsigned long long)r0 & ~15ull, b = (unsigned long long)r1 & ~15ull;
+            if (b > a) bulk_prefetch_l2(col.nulls + a, b - a);
+          }
+        }
+      }
       // K2: static round-robin schedule: round r of every CTA covers tiles [r*G, (r+1)*G), so a
       // tile's look-back predecessors are evaluated concurrently in the same round (K2 is a
       // cooperative launch: every CTA is resident, no look-back waits on an unscheduled CTA).
@@ -1737,6 +1766,267 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
     if (!work || pc == 0) continue;
     sparse_chunk(p, seg, sub, w4, p.seg_offsets[seg] + incl - pc, scap);
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// ONE-kernel selection compaction for mid-size tables (sel_mid_kernel): replaces the offsets scan
+// (tile_scan_partials + tile_scan_apply), the streamed and the gathered compaction, i.e. four
+// dependent launches, each a few us of launch + ramp at a few million rows.
+//
+// Block b (an atomic ticket, so it only ever waits on blocks that are already running) owns
+// segments [b*SPB, (b+1)*SPB):
+//   1. loads its segments' counts and publishes their sum at once (agg[b] = sum + 1, release);
+//   2. expands its hits into a shared-memory list (row, capture slot) in row order and issues the
+//      loads of every projected value of its first batch of entries (captured values from the
+//      scan's capture slots, the rest gathered from HBM) — none of that needs the output base;
+//   3. only then reads its base, the sum of agg[0..b): by now every predecessor has published
+//      (each does so after one load round trip), so it is a flat parallel read, not a look-back
+//      chain, and its latency hides behind the gathers in flight; the last block to have read
+//      clears agg[] and the counters (no host reset: prepared graphs re-issue it as is);
+//   4. writes entry e of the block to output position base + e (coalesced stores).
+// ------------------------------------------------------------------------------------------
+constexpr int kMidThreads = 256;
+constexpr int kMidMaxBlocks = 4096;  // block-sum words reserved in the workspace
+constexpr int kMidList = 2048;       // hit-list entries per batch (>= one whole segment: seg_rows <= 1024)
+
+struct MidParams {
+  int32_t segs_per_block;
+  int32_t pad;
+  int64_t n_blocks;
+  unsigned long long* agg;       // [n_blocks] published block sums + 1 (0 = not yet), cleared by the last block
+  unsigned long long* ticket;    // block tickets (cleared by the last block)
+  unsigned long long* done;      // blocks past their prefix read (cleared by the last block)
+  unsigned long long* trace;     // diagnostics (esc_debug_trace): 8 %globaltimer stamps per block, or nullptr
+};
+
+// one thread's share of a batch round: entries e0 + j*256 (j < kMidJ), projections k0 .. k0+3
+constexpr int kMidJ = 2;  // entries per thread and round (x 4 projections: 8 loads in flight, no spills)
+struct MidRound {
+  int64_t prow[kMidJ];
+  uint32_t slot[kMidJ];
+  bool ok[kMidJ];
+  unsigned long long v[4][kMidJ];
+  uint8_t nb[4][kMidJ];
+};
+
+__device__ __forceinline__ void mid_rows(const SelParams& p, const uint32_t* l_row, const uint32_t* l_slot,
+                                         int64_t row0, int nb, int e0, MidRound& r) {
+#pragma unroll
+  for (int j = 0; j < kMidJ; ++j) {
+    const int e = e0 + j * kMidThreads;
+    r.ok[j] = e < nb;
+    const int64_t row = row0 + (r.ok[j] ? l_row[e] : 0u);
+    r.slot[j] = r.ok[j] ? l_slot[e] : 0xFFFFFFFFu;
+    r.prow[j] = (r.ok[j] && p.row_ids) ? __ldg(p.row_ids + row) : row;
+  }
+}
+
+__device__ __forceinline__ void mid_load(const SelParams& p, int k0, MidRound& r) {
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+    for (int j = 0; j < kMidJ; ++j) {
+      r.v[kk][j] = 0;
+      r.nb[kk][j] = 0;
+    }
+    const int k = k0 + kk;
+    if (k >= p.n_proj) continue;
+    const KCol& col = p.cols[k];
+    const int ci = p.cap_index[k];
+#pragma unroll
+    for (int j = 0; j < kMidJ; ++j) {
+      if (!r.ok[j]) continue;
+      if (ci >= 0 && r.slot[j] != 0xFFFFFFFFu) {
+        r.v[kk][j] = ld_w(col.width, p.cap_values[ci], r.slot[j]);
+        if (p.cap_nulls[ci] != nullptr) r.nb[kk][j] = p.cap_nulls[ci][r.slot[j]];
+      } else {
+        switch (col.width) {
+          case 1: r.v[kk][j] = __ldcg(col.data + r.prow[j]); break;
+          case 2: r.v[kk][j] = __ldcg(reinterpret_cast<const uint16_t*>(col.data) + r.prow[j]); break;
+          case 4: r.v[kk][j] = __ldcg(reinterpret_cast<const uint32_t*>(col.data) + r.prow[j]); break;
+          default: r.v[kk][j] = __ldcg(reinterpret_cast<const unsigned long long*>(col.data) + r.prow[j]); break;
+        }
+        if (col.nulls != nullptr) r.nb[kk][j] = __ldg(col.nulls + r.prow[j]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void mid_store(const SelParams& p, int k0, const MidRound& r, unsigned long long pos0,
+                                          int e0, long long cap) {
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const int k = k0 + kk;
+    if (k >= p.n_proj) continue;
+    const int width = p.cols[k].width;
+#pragma unroll
+    for (int j = 0; j < kMidJ; ++j) {
+      const unsigned long long pos = pos0 + (unsigned long long)(e0 + j * kMidThreads);
+      if (!r.ok[j] || (long long)pos >= cap) continue;
+      st_bits(width, p.outs.out_values[k], pos, r.v[kk][j]);
+      if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = r.nb[kk][j];
+    }
+  }
+  if (k0 == 0 && p.outs.out_row_ids != nullptr) {
+#pragma unroll
+    for (int j = 0; j < kMidJ; ++j) {
+      const unsigned long long pos = pos0 + (unsigned long long)(e0 + j * kMidThreads);
+      if (r.ok[j] && (long long)pos < cap) p.outs.out_row_ids[pos] = r.prow[j];
+    }
+  }
+}
+
+// block-wide sum of one value per thread (s_red: >= kMidThreads/32 words)
+__device__ __forceinline__ unsigned long long mid_block_sum(unsigned long long v, unsigned long long* s_red) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+#pragma unroll
+  for (int w = 0; w < kMidThreads / 32; ++w) t += s_red[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_constant__ SelParams p,
+                                                                 const __grid_constant__ MidParams m) {
+  __shared__ uint32_t l_row[kMidList];
+  __shared__ uint32_t l_slot[kMidList];
+  __shared__ unsigned long long s_red[kMidThreads / 32];
+  __shared__ unsigned long long s_scan[33];
+  __shared__ long long s_block;
+  extern __shared__ uint32_t s_cnt[];  // [segs_per_block]: counts, then exclusive offsets in the block
+  const unsigned long long t_start = m.trace != nullptr ? gtimer() : 0ull;
+  pdl_wait();
+  pdl_trigger();
+  if (skip_materialize(p.rule)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_block = (long long)atomicAdd(m.ticket, 1ull);
+  __syncthreads();
+  const int64_t b = s_block;
+  unsigned long long* tr = (m.trace != nullptr && threadIdx.x == 0) ? m.trace + 8 * 1024 + b * 8 : nullptr;
+  if (tr) { tr[0] = t_start; tr[1] = gtimer(); }
+  const int SPB = m.segs_per_block;
+  const int64_t seg0 = b * SPB;
+  const int nseg = (int)((seg0 + SPB <= p.n_segs) ? SPB : (p.n_segs > seg0 ? p.n_segs - seg0 : 0));
+  const int W = p.seg_rows / 32;
+  // the bitmap words of this warp's first four segments are loaded with the counts (the
+  // expansion of the first batch then needs no further round trip)
+  uint32_t wpre[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int si = warp + q * (kMidThreads / 32);
+    wpre[q] = (si < nseg && lane < W) ? __ldcg(p.bitmap + (seg0 + si) * W + lane) : 0u;
+  }
+  // 1. this block's segment counts; their sum is published at once
+  unsigned long long mine = 0;
+  for (int i = threadIdx.x; i < nseg; i += kMidThreads) {
+    const uint32_t c = __ldcg(p.seg_counts + seg0 + i);
+    s_cnt[i] = c;
+    mine += c & ~ESC_SEG_CAPTURED;
+  }
+  const unsigned long long block_sum = mid_block_sum(mine, s_red);
+  if (threadIdx.x == 0) {
+    st_release(m.agg + b, block_sum + 1);
+    if (tr) tr[2] = gtimer();
+  }
+  // exclusive offsets of the block's segments (in place; chunks of 256 with a running carry;
+  // < 2^31: a block's hits <= its rows, bounded on the host)
+  unsigned long long carry = 0;
+  for (int c0 = 0; c0 < nseg; c0 += kMidThreads) {
+    const int i = c0 + threadIdx.x;
+    const unsigned long long v = i < nseg ? (s_cnt[i] & ~ESC_SEG_CAPTURED) : 0u;
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan(v, s_scan, &tot);
+    if (i < nseg) s_cnt[i] = (uint32_t)(carry + ex) | (s_cnt[i] & ESC_SEG_CAPTURED);
+    carry += tot;
+  }
+  __syncthreads();
+  const long long cap = p.outs.capacity;
+  const int64_t row0 = seg0 * (int64_t)p.seg_rows;
+  const uint32_t block_hits = (uint32_t)carry;
+  if (tr) tr[3] = gtimer();
+  auto off_of = [&](int i) -> uint32_t { return i < nseg ? (s_cnt[i] & ~ESC_SEG_CAPTURED) : block_hits; };
+  unsigned long long base = 0;
+  bool have_base = false;
+  // 2-4. hit lists, batch by batch of whole segments (a segment's <= 1024 hits always fit)
+  for (int sb = 0; sb < nseg || !have_base;) {
+    int se = sb;
+    uint32_t first = 0, upto = 0;
+    if (sb < nseg) {
+      first = off_of(sb);
+      se = sb + 1;
+      while (se < nseg && off_of(se + 1) - first <= (uint32_t)kMidList) ++se;
+      upto = off_of(se);
+      // expand: warp per segment, lane per bitmap word, hits in row order (the first batch's
+      // first four segments per warp use the words loaded at the start)
+      for (int si = sb + warp, q = 0; si < se; si += kMidThreads / 32, ++q) {
+        const uint32_t o = off_of(si);
+        if (off_of(si + 1) == o) continue;  // empty segment
+        const bool captured = (s_cnt[si] & ESC_SEG_CAPTURED) != 0;
+        const int64_t seg = seg0 + si;
+        const bool pre = sb == 0 && q < 4;
+        const uint32_t word = pre ? (q == 0 ? wpre[0] : q == 1 ? wpre[1] : q == 2 ? wpre[2] : wpre[3])
+                                  : (lane < W ? __ldcg(p.bitmap + seg * W + lane) : 0u);
+        const uint32_t pc = __popc(word);
+        uint32_t incl = pc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+          if (lane >= d) incl += t;
+        }
+        uint32_t j = incl - pc;  // rank of this word's first hit in the segment
+        uint32_t wbits = word;
+        const uint32_t rbase = (uint32_t)si * (uint32_t)p.seg_rows + (uint32_t)lane * 32u;
+        while (wbits) {
+          const int bit = __ffs(wbits) - 1;
+          wbits &= wbits - 1;
+          const uint32_t e = o - first + j;
+          l_row[e] = rbase + (uint32_t)bit;
+          l_slot[e] = captured ? (uint32_t)((size_t)j * p.cap_stride + seg) : 0xFFFFFFFFu;
+          ++j;
+        }
+      }
+      __syncthreads();
+    }
+    if (tr && sb == 0) tr[4] = gtimer();
+    const int nb = (int)(upto - first);
+    // the first round's loads are issued BEFORE the base is read (they do not need it)
+    for (int e0 = threadIdx.x, round = 0; round == 0 || e0 < nb; e0 += kMidJ * kMidThreads, ++round) {
+      for (int k0 = 0; k0 < (p.n_proj > 0 ? p.n_proj : 1); k0 += 4) {
+        MidRound r;
+        mid_rows(p, l_row, l_slot, row0, nb, e0, r);
+        mid_load(p, k0, r);
+        if (!have_base) {  // block-uniform: every thread takes this branch together, once
+          unsigned long long pre = 0;
+          for (int64_t q = threadIdx.x; q < b; q += kMidThreads) {
+            unsigned long long v = ld_relaxed(m.agg + q);  // relaxed polls (acquire per poll is a fence each)
+            while (v == 0ull) v = ld_relaxed(m.agg + q);
+            pre += v - 1;
+          }
+          // no fence here: it would wait for the gathers in flight; the polls are complete
+          // (their values are consumed) before this block counts itself done below
+          base = mid_block_sum(pre, s_red);
+          have_base = true;
+          if (threadIdx.x == 0) {
+            if (tr) tr[5] = gtimer();
+            // the last block past its base read resets the table for the next launch
+            if (atomicAdd(m.done, 1ull) == (unsigned long long)m.n_blocks - 1) {
+              for (int64_t q = 0; q < m.n_blocks; ++q) __stcg(m.agg + q, 0ull);
+              __stcg(m.ticket, 0ull);
+              __stcg(m.done, 0ull);
+            }
+          }
+        }
+        mid_store(p, k0, r, base + first, e0, cap);
+      }
+    }
+    __syncthreads();
+    sb = se;
+    if (sb >= nseg) break;
+  }
+  if (tr) tr[6] = gtimer();
 }
 
 // ------------------------------------------------------------------------------------------

@@ -108,6 +108,13 @@ int sm_count_cached() {
   return n;
 }
 
+// K1 L2 prefetch of the whole scan when its staged bytes are at most this (ESC_PREFETCH_L2_BYTES;
+// 0 = off): the 126 MB L2 holds a mid-size table's predicate columns
+std::atomic<long long> g_prefetch_max_bytes{[] {
+  const char* e = getenv("ESC_PREFETCH_L2_BYTES");
+  return e ? atoll(e) : 0ll;  // measured slower on config 2 (43 -> 47 us): off by default
+}()};
+
 // per-workspace epoch for the look-back status words (host side; guarded), and the most status
 // words any one-pass launch on that workspace has used (all of them end at the workspace's end)
 std::mutex g_epoch_mu;
@@ -122,8 +129,9 @@ size_t status_words(int64_t nrows) {
   return (size_t)((nrows + t - 1) / t) + 1;
 }
 
-// Workspace layout: [header][segment offsets u64][scan partials u64][segment counts u32]
-//                   [selection bitmap u32][dense-tile counter + list u32] ... [tile status u64]
+// Workspace layout: [header][mid-kernel block sums u64 x kMidMaxBlocks][segment offsets u64]
+//                   [scan partials u64][segment counts u32][selection bitmap u32]
+//                   [dense-tile counter + list u32] ... [tile status u64]
 // The one-pass kernel's tile status words sit at the END of the workspace, whatever its size
 // (status_base): every other region is a prefix whose extent grows with nrows, the status words a
 // suffix that does too, and esc_workspace_bytes(n) covers both, so for any two launches of
@@ -131,7 +139,7 @@ size_t status_words(int64_t nrows) {
 // the other — a smaller table's offsets/bitmap can never leave words that a later look-back
 // might take for a published status (they carry a 16-bit epoch tag, see next_epoch).
 struct WsLayout {
-  size_t offsets, partials, counts, bitmap, dense, total;
+  size_t mid, offsets, partials, counts, bitmap, dense, total;
   int64_t max_tiles, bitmap_words;
 };
 WsLayout ws_layout(int64_t nrows) {
@@ -143,7 +151,9 @@ WsLayout ws_layout(int64_t nrows) {
   L.bitmap_words = ((nrows + t_max - 1) / t_max + 1) * (t_max / 32);  // covers every C's last tile
   const int64_t segs = L.max_tiles / kScanSeg + 2;
   auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  L.offsets = up(sizeof(WsHeader));
+  L.mid = sizeof(WsHeader);  // sel_mid_kernel block sums: a FIXED place (every launch size sees the same
+                             // words, which its last block leaves zero)
+  L.offsets = up(L.mid + kMidMaxBlocks * sizeof(unsigned long long));
   L.partials = up(L.offsets + (size_t)L.max_tiles * 8);
   L.counts = up(L.partials + (size_t)segs * 8);
   L.bitmap = up(L.counts + (size_t)L.max_tiles * 4);
@@ -536,6 +546,9 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
     const int64_t spread = kp.n_tiles / (2 * (int64_t)sms);  // small scans keep one tile per ticket
     if (kb > spread) kb = spread;
     kp.ticket_tiles = (int32_t)(kb < 1 ? 1 : (kb > 8 ? 8 : kb));
+    // tables whose staged bytes fit comfortably in L2: prefetch them all up front (DRAM ramp)
+    const long long staged = (long long)kp.n_full_tiles * g.tma_bytes;
+    kp.prefetch_l2 = (staged > 0 && staged <= g_prefetch_max_bytes.load()) ? 1 : 0;
   }
   rc = lower_program(prog, kp);
   if (rc != ESC_OK) return rc;
@@ -661,6 +674,14 @@ std::atomic<int> g_stream_div{[] {
   return e ? atoi(e) : 32;
 }()};
 
+// selections over at most this many rows compact with ONE sel_mid_kernel launch (ESC_MID_MAX_ROWS;
+// 0 turns it off): below it the chain's launch + ramp costs dominate, above it the streamed
+// (TMA) compaction of dense tiles reads less than per-hit gathers
+std::atomic<long long> g_mid_max_rows{[] {
+  const char* e = getenv("ESC_MID_MAX_ROWS");
+  return e ? atoll(e) : (32ll << 20);
+}()};
+
 uint32_t stream_dense_min(int tile_rows) {
   const int div = g_stream_div.load();
   if (div <= 0) return 0xFFFFFFFFu;  // streaming off
@@ -744,6 +765,9 @@ bool plan_stream(StreamParams& tp, const SelParams& sp, const esc_column_t* cols
 struct MatLaunch {
   SelParams sp;
   StreamParams tp;
+  MidParams mp;
+  bool mid = false;        // one sel_mid_kernel launch instead of the scan + compaction chain
+  size_t mid_smem = 0;
   bool streaming = false;
   bool empty = true;
   unsigned segs = 0;
@@ -767,6 +791,9 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
     return fail(ESC_ERR_INVALID, "bad outputs");
   const WsLayout L = ws_layout(nrows);
   if (d_ws == nullptr || ws_bytes < L.total) return fail(ESC_ERR_WORKSPACE, "workspace too small");
+  M->mid = false;  // M may be a reused (thread-local) launch: every route flag is re-decided here
+  M->streaming = false;
+  M->empty = true;
   std::memset(&sp, 0, sizeof(sp));
   sp.bitmap = sel->bitmap;
   sp.seg_counts = sel->seg_counts;
@@ -809,14 +836,9 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   M->partials = reinterpret_cast<unsigned long long*>(ws + L.partials);
   M->seg_counts = sel->seg_counts;
   sp.seg_offsets = M->offsets;
-  // dense stream tiles (no row-id chaining: the staged tile must be the physical rows)
-  StreamParams& tp = M->tp;
-  M->streaming = plan_stream(tp, sp, cols, outs, sel, nrows, d_row_ids);
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   sp.rule.dense_min = 0xFFFFFFFFu;
-  sp.rule.segs_per_tile = 8;
-  sp.rule.n_tiles = 0;
-  sp.rule.n_dense = reinterpret_cast<uint32_t*>(ws + L.dense);
-  sp.rule.dense_list = reinterpret_cast<uint32_t*>(ws + L.dense + 256);
   sp.rule.skip_count = nullptr;
   sp.rule.skip_capacity = outs->capacity;
   if (outs->flags & ESC_OUT_SKIP_OVER_CAPACITY) {
@@ -825,8 +847,40 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
     sp.rule.skip_count = reinterpret_cast<const unsigned long long*>(sel->d_gate != nullptr ? sel->d_gate
                                                                                              : sel->d_count);
   }
-  const int sms = sm_count_cached();
-  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  // mid-size selections: ONE kernel (sel_mid_kernel) — offsets and compaction without the chain
+  if (nrows <= g_mid_max_rows.load()) {
+    static const int mid_resident = [] {
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sel_mid_kernel, kMidThreads, 4096);
+      return b > 0 ? b : 4;
+    }();
+    const int64_t target = (int64_t)sms * mid_resident;
+    int64_t spb = (sp.n_segs + target - 1) / target;
+    if (spb < 1) spb = 1;
+    if ((sp.n_segs + spb - 1) / spb > kMidMaxBlocks) spb = (sp.n_segs + kMidMaxBlocks - 1) / kMidMaxBlocks;
+    if (spb * sel->seg_rows < (1ll << 31) && spb <= 4096) {
+      MidParams& mp = M->mp;
+      std::memset(&mp, 0, sizeof(mp));
+      mp.segs_per_block = (int32_t)spb;
+      mp.n_blocks = (sp.n_segs + spb - 1) / spb;
+      uint8_t* ws = static_cast<uint8_t*>(d_ws);
+      mp.agg = reinterpret_cast<unsigned long long*>(ws + L.mid);  // fixed place: zero between launches
+      mp.trace = g_trace;
+      WsHeader* hdr = static_cast<WsHeader*>(d_ws);
+      mp.ticket = &hdr->mid_ticket;
+      mp.done = &hdr->mid_done;
+      M->mid = true;
+      M->mid_smem = (size_t)spb * sizeof(uint32_t);
+      return ESC_OK;
+    }
+  }
+  // dense stream tiles (no row-id chaining: the staged tile must be the physical rows)
+  StreamParams& tp = M->tp;
+  M->streaming = plan_stream(tp, sp, cols, outs, sel, nrows, d_row_ids);
+  sp.rule.segs_per_tile = 8;
+  sp.rule.n_tiles = 0;
+  sp.rule.n_dense = reinterpret_cast<uint32_t*>(ws + L.dense);
+  sp.rule.dense_list = reinterpret_cast<uint32_t*>(ws + L.dense + 256);
   if (M->streaming) {
     sp.rule.dense_min = stream_dense_min(tp.tile_rows);
     sp.rule.segs_per_tile = tp.segs_per_tile;
@@ -893,6 +947,12 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, si
 int issue_mat(const MatLaunch& M, cudaStream_t st) {
   if (M.empty) return ESC_OK;
   const SelParams& sp = M.sp;
+  if (M.mid) {
+    cudaError_t e = launch_pdl(sel_mid_kernel, (unsigned)M.mp.n_blocks, kMidThreads, M.mid_smem, st, sp, M.mp);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("mid-size compaction launch: ") + cudaGetErrorString(e));
+    return ESC_OK;
+  }
   cudaError_t e = launch_pdl(tile_scan_partials, M.segs, kScanThreads, 0, st, M.seg_counts, sp.n_segs, M.partials,
                              sp.rule.n_dense, sp.rule.skip_count, sp.rule.skip_capacity);
   if (e == cudaSuccess)
@@ -1295,6 +1355,12 @@ int esc_debug_trace(void* d_stamps) {
 int esc_set_stream_div(int div) {
   const int prev = g_stream_div.load();
   g_stream_div = div;
+  return prev;
+}
+
+int64_t esc_set_mid_max_rows(int64_t max_rows) {
+  const long long prev = g_mid_max_rows.load();
+  if (max_rows >= 0) g_mid_max_rows = max_rows;
   return prev;
 }
 
