@@ -460,8 +460,10 @@ int esc_jit_stats(int64_t* out);
 int esc_set_stream_div(int div);
 /* Selections over at most max_rows rows are compacted by ONE launch (sel_mid_kernel: block sums
  * published and read flat, then each block's hits expanded and written) instead of the offsets
- * scan + streamed/gathered compaction chain; 0 turns it off, < 0 leaves it.  Default 32M rows
- * (env ESC_MID_MAX_ROWS).  Returns the previous setting. */
+ * scan + streamed/gathered compaction chain, when the output capacity is at most a quarter of the
+ * rows (denser results stream better through the chain); 0 turns it off, >= 2^40 forces it for
+ * every size and density, < 0 leaves it.  Default 32M rows (env ESC_MID_MAX_ROWS).  Returns the
+ * previous setting. */
 int64_t esc_set_mid_max_rows(int64_t max_rows);
 /* Diagnostics: when d_stamps (device, >= 8 x grid uint64) is non-null, every later scan launch
  * writes per-CTA %globaltimer stamps (start, first tile, consumers done, producer done, CTA

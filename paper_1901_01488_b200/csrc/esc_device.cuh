@@ -1976,6 +1976,22 @@ __global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_co
           const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
           if (lane >= d) incl += t;
         }
+        const uint32_t cnt = off_of(si + 1) - o;
+        if (cnt > 2u * (uint32_t)W) {
+          // dense segment: lane per row, word by word (W steps instead of up to 32 bit steps)
+          const uint32_t lt = (1u << lane) - 1u, excl = incl - pc;
+          for (int w = 0; w < W; ++w) {
+            const uint32_t ww = __shfl_sync(0xFFFFFFFFu, word, w);
+            const uint32_t wb = __shfl_sync(0xFFFFFFFFu, excl, w);
+            if ((ww >> lane) & 1u) {
+              const uint32_t jj = wb + __popc(ww & lt);
+              const uint32_t e = o - first + jj;
+              l_row[e] = (uint32_t)si * (uint32_t)p.seg_rows + (uint32_t)w * 32u + (uint32_t)lane;
+              l_slot[e] = captured ? (uint32_t)((size_t)jj * p.cap_stride + seg) : 0xFFFFFFFFu;
+            }
+          }
+          continue;
+        }
         uint32_t j = incl - pc;  // rank of this word's first hit in the segment
         uint32_t wbits = word;
         const uint32_t rbase = (uint32_t)si * (uint32_t)p.seg_rows + (uint32_t)lane * 32u;

@@ -847,8 +847,13 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
     sp.rule.skip_count = reinterpret_cast<const unsigned long long*>(sel->d_gate != nullptr ? sel->d_gate
                                                                                              : sel->d_count);
   }
-  // mid-size selections: ONE kernel (sel_mid_kernel) — offsets and compaction without the chain
-  if (nrows <= g_mid_max_rows.load()) {
+  // mid-size selections: ONE kernel (sel_mid_kernel) — offsets and compaction without the chain —
+  // when the output can hold at most a quarter of the rows (an ESC step's capacity is the push-down
+  // threshold, 20% by default; an exact materialisation's is its count): it gathers hit by hit,
+  // which beats the chain up to ~10-20% density and loses to the chain's TMA-streamed dense tiles
+  // beyond (tools/diag_mid_sweep.py: 4M-48M rows, s = 0.001 .. 0.5)
+  const long long mid_max = g_mid_max_rows.load();  // >= 2^40: forced for every size and density (tests)
+  if (nrows <= mid_max && (outs->capacity <= nrows / 4 || mid_max >= (1ll << 40))) {
     static const int mid_resident = [] {
       int b = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sel_mid_kernel, kMidThreads, 4096);
