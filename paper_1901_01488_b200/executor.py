@@ -820,9 +820,10 @@ def _onepass_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacit
 
 def _trim(proj: list, values: list, nulls: list, count: int, stream, cache: dict | None = None) -> list[Column]:
     """Exact-size temp columns: the first ``count`` rows of each capacity-sized output, copied
-    by ONE batched launch (esc_copy_regions).  ``cache`` (a plan's dict) keeps the ctypes
-    argument arrays — the sources are the plan's fixed buffers — so a step only fills in the
-    destinations and sizes."""
+    by ONE batched launch (esc_copy_regions) into one caching-allocator tensor per column (a
+    single allocation carved into views measured 7 us slower per step: each slice + view is a
+    torch op of its own).  ``cache`` (a plan's dict) keeps the ctypes argument arrays — the
+    sources are the plan's fixed buffers — so a step only fills in the destinations and sizes."""
     srcs = [t for v, m in zip(values, nulls) for t in ((v,) if m is None else (v, m))]
     k = len(srcs)
     if not k:

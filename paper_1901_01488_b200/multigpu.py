@@ -265,7 +265,7 @@ def _finish(item: _Launched):
     return count, counts, None
 
 
-def esc_batch(catalog, prepared: list, config) -> list:
+def esc_batch(catalog, prepared: list, config, register: bool = True) -> list:
     """ESC steps of several SHARDED tables (``prepared`` as optimizer.esc_subqueries builds it:
     (alias, table, predicate, needed, global rows, fused, global capacity)) — every step queued
     (scan, device count exchange, gated compaction), ONE host wait, then results in item order;
@@ -300,14 +300,16 @@ def esc_batch(catalog, prepared: list, config) -> list:
         if qualified and config.materialize:
             if cols is None:
                 raise ExecutionError(f"internal: qualified table {it.alias!r} overflowed its temp buffer")
-            t2 = time.perf_counter()
-            sh = it.table.shard
-            temp = catalog.materialize_temp(cols, ShardInfo(sh.rank, sh.world, exclusive_offsets(counts)[sh.rank],
-                                                            tuple(counts), sh.group))
-            mat_ms = (time.perf_counter() - t2) * 1000.0
+            if register:
+                t2 = time.perf_counter()
+                sh = it.table.shard
+                temp = catalog.materialize_temp(cols, ShardInfo(sh.rank, sh.world, exclusive_offsets(counts)[sh.rank],
+                                                                tuple(counts), sh.group))
+                mat_ms = (time.perf_counter() - t2) * 1000.0
         d = EscDecision(it.alias, it.predicate, total, it.rc, Fraction(total, it.rc) if it.rc else Fraction(0),
                         qualified, temp is not None, temp, sub_ms, mat_ms)
         d.local_count, d.counts = local, counts
+        d.columns = cols if qualified and config.materialize else None
         decisions.append(d)
     if launch_error is not None:
         raise launch_error[0] from launch_error[1]
@@ -362,7 +364,6 @@ class ShardedDecision:
 def sharded_esc_subquery(st: ShardedTable, predicate, needed, config, group=None) -> ShardedDecision:
     """The ESC step of one sharded table: the scan on every rank's shard, one device count
     exchange, the gated compaction, one host wait.  The slice is returned, not registered."""
-    from .catalog import Catalog
     from .optimizer import _ratio, _trivially_true
 
     if predicate is None or _trivially_true(predicate):
@@ -374,14 +375,9 @@ def sharded_esc_subquery(st: ShardedTable, predicate, needed, config, group=None
     fused = config.materialize and rc > 0 and rc >= config.min_table_size
     num, den = _ratio(config.max_selectivity)
     gcap = (num * rc) // den if fused else 0
-    scratch = Catalog()
-    (d,) = esc_batch(scratch, [(st.name, t, predicate, list(needed), rc, fused, gcap)], config)
-    cols = None
-    if d.temp is not None:
-        cols = scratch.resolve_temp(d.temp).columns
-        scratch.temps.sweep()
+    (d,) = esc_batch(None, [(st.name, t, predicate, list(needed), rc, fused, gcap)], config, register=False)
     return ShardedDecision(st.name, d.exact_count, rc, d.selectivity, d.qualified, d.local_count,
-                           exclusive_offsets(d.counts)[st.rank], d.counts, cols)
+                           exclusive_offsets(d.counts)[st.rank], d.counts, d.columns)
 
 
 # ------------------------------------------------------------------------------------------------
