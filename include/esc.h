@@ -323,6 +323,49 @@ int esc_gather(const esc_column_t* col, const int64_t* d_idx, int64_t n, void* o
 #define ESC_MAX_REGIONS 72
 int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const int64_t* bytes, void* stream);
 
+/* ---- device sort and grouping (esc_sort.cuh; no library kernels) --------------------------
+ * Used by the hash build's grouping (f1: np.unique + stable argsort, executor.py:275-303), the CSV
+ * loader's TEXT dictionary by first appearance (f3: Dictionary.encode order, storage.py:127-153,
+ * :247-275) and the histogram arm's value sort (f4: np.sort, catalog.py:178-223). */
+
+/* Temp bytes for esc_sort_pairs / esc_runs over n keys of key_bytes (4 | 8), with values or not. */
+size_t esc_sort_temp_bytes(int64_t n, int32_t key_bytes, int32_t with_values);
+
+/* Stable LSD radix sort of unsigned keys (key_bytes 4 | 8) by bits [begin_bit, end_bit), with
+ * optional 64-bit values carried along (vals_in NULL: keys only).  Equal keys keep their input
+ * order.  keys_in / vals_in are not modified; outputs must not alias inputs. */
+int esc_sort_pairs(const void* keys_in, const uint64_t* vals_in, void* keys_out, uint64_t* vals_out, int64_t n,
+                   int32_t key_bytes, int32_t begin_bit, int32_t end_bit, void* temp, size_t temp_bytes,
+                   void* stream);
+
+/* Runs of a SORTED key array: unique_keys[r] (decoded to int64: 0 raw, 1 u32, 2 int32 stored
+ * ^ 2^31, 3 int64 stored ^ 2^63), starts[0..runs] (starts[runs] = n), counts[r] (optional),
+ * run_of[i] (optional) and stats = {runs, first key, last key, largest run}.  Read stats after a
+ * stream sync. */
+int esc_runs(const void* sorted_keys, int32_t key_bytes, int32_t decode, int64_t n, int64_t* unique_keys,
+             int64_t* starts, int64_t* counts, int64_t* run_of, int64_t* stats, void* temp, size_t temp_bytes,
+             void* stream);
+
+/* Order-preserving unsigned sort keys of an integer column: 1-4 byte signed -> uint32 ^ 2^31,
+ * unsigned -> uint32, int64 -> uint64 ^ 2^63 (decode 2 / 1 / 3 in esc_runs). */
+int esc_order_keys(const void* values, int32_t dtype, int64_t n, void* out, void* stream);
+/* Values of a column given as runs (esc_runs output) at sorted positions ranks[0..k). */
+int esc_rank_values(const int64_t* unique_keys, const int64_t* starts, const int64_t* stats, const int64_t* ranks,
+                    int32_t k, int64_t* out, void* stream);
+/* Equi-depth histogram buckets over a column given as runs: bucket j = [lo_j, hi_j) with hi_j the
+ * end of the last run whose value <= bounds[j+1] (the last bucket ends at n), and its distinct
+ * values (reference catalog.py:178-223: searchsorted(right) + distinct counts). */
+int esc_hist_buckets(const int64_t* unique_keys, const int64_t* starts, const int64_t* stats, int64_t n,
+                     const int64_t* bounds, int32_t nb, int64_t* out_hi, int64_t* out_distinct, void* stream);
+/* First-appearance dictionary codes of n TEXT cells from their 64-bit content hashes (nulls:
+ * optional bool mask): out_codes[i] (0 for NULL), out_rep[i] = the first row holding the same
+ * content (-1 for NULL), out_first[c] = the first row of code c, *out_n_codes (device word) —
+ * the reference's Dictionary.encode order (storage.py:127-153).  Hash collisions are the
+ * caller's to detect (esc_csv_verify_text compares every cell with its representative). */
+size_t esc_dict_temp_bytes(int64_t n);
+int esc_dict_encode(const int64_t* hashes, const uint8_t* nulls, int64_t n, int32_t* out_codes, int64_t* out_rep,
+                    int64_t* out_first, int64_t* out_n_codes, void* temp, size_t temp_bytes, void* stream);
+
 /* ---- hash joins over the device-resident temps ------------------------ */
 #define ESC_MAX_STEPS 8  /* build steps of one probe pipeline */
 

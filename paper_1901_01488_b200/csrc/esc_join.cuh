@@ -555,12 +555,13 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_quad_kernel(const __grid
 }
 
 // ---- hash build grouping (esc_hash_build) ----------------------------------------------------
+// 64-bit keys sort as unsigned values with the sign bit flipped (order-preserving)
 __global__ void build_gather_kernel(const uint8_t* __restrict__ keys, int dtype, int width,
-                                    const int64_t* __restrict__ rows, int64_t n, long long* __restrict__ out_keys,
-                                    int64_t* __restrict__ out_rows) {
+                                    const int64_t* __restrict__ rows, int64_t n,
+                                    unsigned long long* __restrict__ out_keys, int64_t* __restrict__ out_rows) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = rows ? rows[i] : i;
-    out_keys[i] = ld_int(keys + (size_t)r * width, dtype);
+    out_keys[i] = (unsigned long long)ld_int(keys + (size_t)r * width, dtype) ^ (1ull << 63);
     out_rows[i] = r;
   }
 }
@@ -575,13 +576,6 @@ __global__ void build_gather32_kernel(const uint8_t* __restrict__ keys, int dtyp
     out_keys[i] = (uint32_t)ld_int(keys + (size_t)r * width, dtype) + bias;
     out_rows[i] = r;
   }
-}
-
-__global__ void build_unbias_kernel(const uint32_t* __restrict__ uk32, const long long* __restrict__ num_runs,
-                                    uint32_t bias, long long* __restrict__ uk) {
-  const long long u = *num_runs;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < u; g += (long long)gridDim.x * blockDim.x)
-    uk[g] = bias ? (long long)(int32_t)(uk32[g] - bias) : (long long)uk32[g];
 }
 
 // The whole grouping of a small build (<= 1024 * ITEMS rows, keys of <= 4 bytes) in ONE block:
@@ -669,15 +663,6 @@ build_small_kernel(const uint8_t* __restrict__ keys, int dtype, int width, const
   }
 }
 
-__global__ void build_stats_kernel(const long long* __restrict__ unique_keys, const long long* __restrict__ num_runs,
-                                   const long long* __restrict__ max_count, int64_t* __restrict__ stats) {
-  const long long u = *num_runs;
-  stats[0] = u;
-  stats[1] = u > 0 ? unique_keys[0] : 0;
-  stats[2] = u > 0 ? unique_keys[u - 1] : 0;
-  stats[3] = *max_count;
-}
-
 // dense factor array of a star step: bit / count of every key's group at key - lo
 __global__ void factor_array_kernel(const long long* __restrict__ unique_keys, const long long* __restrict__ counts,
                                     int64_t u, long long lo, int bits, uint8_t* __restrict__ out) {
@@ -706,61 +691,20 @@ __global__ void pairs_insert_kernel(const long long* __restrict__ uk, const long
   }
 }
 
-struct BuildTemp {  // esc_hash_build's scratch: intermediate arrays + the largest CUB temp need
-  size_t keys_in, rows_in, keys_sorted, num_runs, max_count, cub, total;
-  size_t cub_bytes;
+struct BuildTemp {  // esc_hash_build's scratch: gathered keys / rows, sorted keys, the sort's own temp
+  size_t keys_in, rows_in, keys_sorted, sort, total;
+  size_t sort_bytes;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-inline int build_temp_layout_q(int64_t n, BuildTemp* T);
-
-// CUB's temp-size queries cost host time per call: layouts are memoised per power-of-two size
-// class (the sizes grow with n, so the class's largest n covers every n in it)
 inline int build_temp_layout(int64_t n, BuildTemp* T) {
-  int64_t cls = 1024;
-  while (cls < n) cls <<= 1;
-  static std::mutex mu;
-  static std::unordered_map<int64_t, BuildTemp> memo;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    auto it = memo.find(cls);
-    if (it != memo.end()) {
-      *T = it->second;
-      return ESC_OK;
-    }
-  }
-  const int rc = build_temp_layout_q(cls, T);
-  if (rc == ESC_OK) {
-    std::lock_guard<std::mutex> g(mu);
-    memo[cls] = *T;
-  }
-  return rc;
-}
-
-inline int build_temp_layout_q(int64_t n, BuildTemp* T) {
-  size_t a = 0, b = 0, c = 0, d = 0;
-  const int nn = (int)n;
-  size_t a32 = 0, b32 = 0;
-  if (cub::DeviceRadixSort::SortPairs(nullptr, a, (const long long*)nullptr, (long long*)nullptr,
-                                      (const int64_t*)nullptr, (int64_t*)nullptr, nn) != cudaSuccess ||
-      cub::DeviceRadixSort::SortPairs(nullptr, a32, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                      (const int64_t*)nullptr, (int64_t*)nullptr, nn) != cudaSuccess ||
-      cub::DeviceRunLengthEncode::Encode(nullptr, b, (const long long*)nullptr, (long long*)nullptr,
-                                         (long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess ||
-      cub::DeviceRunLengthEncode::Encode(nullptr, b32, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                         (long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess ||
-      cub::DeviceScan::ExclusiveSum(nullptr, c, (const long long*)nullptr, (long long*)nullptr, nn + 1) != cudaSuccess ||
-      cub::DeviceReduce::Max(nullptr, d, (const long long*)nullptr, (long long*)nullptr, nn) != cudaSuccess)
-    return fail(ESC_ERR_CUDA, "CUB temp-size query failed");
-  T->cub_bytes = std::max(std::max(std::max(a, a32), std::max(b, b32)), std::max(c, d));
+  T->sort_bytes = esc_sort_temp_bytes(n, 8, 1);  // the 64-bit layout also covers 32-bit keys
   size_t off = 0;
   T->keys_in = off;     off += align256((size_t)n * 8);
   T->rows_in = off;     off += align256((size_t)n * 8);
   T->keys_sorted = off; off += align256((size_t)n * 8);
-  T->num_runs = off;    off += 256;
-  T->max_count = off;   off += 256;
-  T->cub = off;         off += align256(T->cub_bytes);
+  T->sort = off;        off += align256(T->sort_bytes);
   T->total = off;
   return ESC_OK;
 }
@@ -843,27 +787,16 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
   if (n > 0 && temp_bytes < T.total) return fail(ESC_ERR_WORKSPACE, "hash build temp too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* t = static_cast<uint8_t*>(d_temp);
-  // counts are zeroed first: the scan and the max read past the u runs the encoder writes (the
-  // one-block path below writes exactly the u counts it has)
   const bool small_path = dtype_width(key_dtype) <= 4 && n > 0 && n <= (int64_t)esc::kBuildSmallThreads * 16;
-  cudaError_t e = small_path ? cudaSuccess
-                             : cudaMemsetAsync(out_group_counts, 0, (size_t)(n + 1) * sizeof(int64_t), st);
-  if (e == cudaSuccess && n == 0) e = cudaMemsetAsync(out_stats, 0, 4 * sizeof(int64_t), st);
+  cudaError_t e = cudaSuccess;
+  if (n == 0) e = cudaMemsetAsync(out_stats, 0, 4 * sizeof(int64_t), st);
   if (e == cudaSuccess && n == 0) e = cudaMemsetAsync(out_group_start, 0, sizeof(int64_t), st);
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash build init: ") + cudaGetErrorString(e));
   if (n == 0) return ESC_OK;
-  long long* keys_in = reinterpret_cast<long long*>(t + T.keys_in);
-  int64_t* rows_in = reinterpret_cast<int64_t*>(t + T.rows_in);
-  long long* keys_sorted = reinterpret_cast<long long*>(t + T.keys_sorted);
-  long long* num_runs = reinterpret_cast<long long*>(t + T.num_runs);
-  long long* max_count = reinterpret_cast<long long*>(t + T.max_count);
-  void* cub_tmp = t + T.cub;
-  size_t cub_bytes = T.cub_bytes;
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
-  const int nn = (int)n;
   const int w = dtype_width(key_dtype);
   const bool sgn = key_dtype == ESC_I8 || key_dtype == ESC_I16 || key_dtype == ESC_I32;
   if (small_path) {  // one block does it all
@@ -887,53 +820,33 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("small hash build: ") + cudaGetErrorString(e));
     return ESC_OK;
   }
-  if (w <= 4) {
-    // stable (LSD radix) sort of 32-bit biased keys: equal keys keep ascending build-row order
+  // the framework's own stable LSD radix sort (esc_sort.cuh): equal keys keep ascending build-row
+  // order, as the reference's stable argsort; then the runs are the groups in ascending key order
+  uint8_t* ks = t + T.keys_sorted;
+  int64_t* rows_in = reinterpret_cast<int64_t*>(t + T.rows_in);
+  if (w <= 4) {  // 32-bit keys (biased by 2^31 when signed): 4 digit passes instead of 8
     const uint32_t bias = sgn ? 0x80000000u : 0u;
-    uint32_t* k32_in = reinterpret_cast<uint32_t*>(keys_in);
-    uint32_t* k32_sorted = reinterpret_cast<uint32_t*>(keys_sorted);
-    uint32_t* uk32 = reinterpret_cast<uint32_t*>(keys_in);  // the input keys are dead after the sort
+    uint32_t* k32_in = reinterpret_cast<uint32_t*>(t + T.keys_in);
     ++g_launches;
     esc::build_gather32_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(keys), key_dtype, w,
                                                                  rows, n, bias, k32_in, rows_in);
-    g_launches += 5;
-    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k32_in, k32_sorted, rows_in, out_group_rows, nn, 0, 32,
-                                        st);
-    if (e == cudaSuccess)
-      e = cub::DeviceRunLengthEncode::Encode(cub_tmp, cub_bytes, k32_sorted, uk32,
-                                             reinterpret_cast<long long*>(out_group_counts), num_runs, nn, st);
-    if (e == cudaSuccess) {
-      esc::build_unbias_kernel<<<(unsigned)blocks, 256, 0, st>>>(uk32, num_runs, bias,
-                                                                 reinterpret_cast<long long*>(out_unique_keys));
-      e = cudaGetLastError();
-    }
+    rc = esc_sort_pairs(k32_in, reinterpret_cast<const uint64_t*>(rows_in), ks,
+                        reinterpret_cast<uint64_t*>(out_group_rows), n, 4, 0, 32, t + T.sort, T.sort_bytes, st);
+    if (rc == ESC_OK)
+      rc = esc_runs(ks, 4, sgn ? esc::ESC_KEY_I32 : esc::ESC_KEY_RAW, n, out_unique_keys, out_group_start,
+                    out_group_counts, nullptr, out_stats, t + T.sort, T.sort_bytes, st);
   } else {
+    unsigned long long* k64_in = reinterpret_cast<unsigned long long*>(t + T.keys_in);
     ++g_launches;
     esc::build_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint8_t*>(keys), key_dtype, w, rows,
-                                                               n, keys_in, rows_in);
-    // stable (LSD radix) sort by key: equal keys keep ascending build-row order, as the
-    // reference's stable argsort; then runs = groups in ascending key order
-    g_launches += 4;
-    e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys_in, keys_sorted, rows_in, out_group_rows, nn, 0,
-                                        64, st);
-    if (e == cudaSuccess)
-      e = cub::DeviceRunLengthEncode::Encode(cub_tmp, cub_bytes, keys_sorted,
-                                             reinterpret_cast<long long*>(out_unique_keys),
-                                             reinterpret_cast<long long*>(out_group_counts), num_runs, nn, st);
+                                                               n, k64_in, rows_in);
+    rc = esc_sort_pairs(k64_in, reinterpret_cast<const uint64_t*>(rows_in), ks,
+                        reinterpret_cast<uint64_t*>(out_group_rows), n, 8, 0, 64, t + T.sort, T.sort_bytes, st);
+    if (rc == ESC_OK)
+      rc = esc_runs(ks, 8, esc::ESC_KEY_I64, n, out_unique_keys, out_group_start, out_group_counts, nullptr,
+                    out_stats, t + T.sort, T.sort_bytes, st);
   }
-  if (e == cudaSuccess)
-    e = cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, reinterpret_cast<const long long*>(out_group_counts),
-                                      reinterpret_cast<long long*>(out_group_start), nn + 1, st);
-  if (e == cudaSuccess)
-    e = cub::DeviceReduce::Max(cub_tmp, cub_bytes, reinterpret_cast<const long long*>(out_group_counts), max_count,
-                               nn, st);
-  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash build: ") + cudaGetErrorString(e));
-  ++g_launches;
-  esc::build_stats_kernel<<<1, 1, 0, st>>>(reinterpret_cast<const long long*>(out_unique_keys), num_runs, max_count,
-                                           out_stats);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("hash build stats: ") + cudaGetErrorString(e));
-  return ESC_OK;
+  return rc;
 }
 
 int esc_hash_insert(const int64_t* unique_keys, int64_t n_unique, int64_t* slots, int64_t capacity, void* stream) {

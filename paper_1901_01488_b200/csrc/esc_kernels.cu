@@ -28,10 +28,6 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_reduce.cuh>
-#include <cub/device/device_run_length_encode.cuh>
-#include <cub/device/device_scan.cuh>
 #include <dlfcn.h>
 #include <nvrtc.h>
 
@@ -1400,5 +1396,6 @@ int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t n
 
 }  // extern "C"
 
+#include "esc_sort.cuh"
 #include "esc_join.cuh"
 #include "esc_csv.cuh"

@@ -875,6 +875,23 @@ def take_column(col: Column, indices) -> Column:
     return Column(col.name, col.kind, out, nulls, col.dictionary)
 
 
+def gather_values(values: torch.Tensor, indices: torch.Tensor) -> torch.Tensor:
+    """values[indices] for a plain device tensor (esc_gather; no NULL mask)."""
+    lib = N.load_library()
+    dev = values.device
+    idx = indices.to(device=dev, dtype=torch.int64).contiguous()
+    n = int(idx.numel())
+    out = torch.empty(n, dtype=values.dtype, device=dev)
+    desc = N.EscColumn()
+    desc.data = values.data_ptr() if values.numel() else None
+    desc.nulls = None
+    desc.dtype = N.dtype_code(values)
+    N.check(lib.esc_gather(C.byref(desc), C.c_void_p(idx.data_ptr()) if n else None, n,
+                           C.c_void_p(out.data_ptr()) if n else None, None, C.c_void_p(_stream(dev).cuda_stream)),
+            "esc_gather")
+    return out
+
+
 def execute_count(ra, catalog) -> int:
     """Single-table COUNT tree: Aggregate over optional Select over optional Project over a
     Scan / TempScan (reference ``executor.py:232-250``)."""

@@ -26,6 +26,7 @@ import torch
 from . import _native as N
 from . import executor
 from . import expr as ex
+from . import sorting
 from .errors import Inestimable, UnsupportedColumnKind
 from .storage import ColumnTable
 
@@ -71,12 +72,15 @@ def build_histogram(table: ColumnTable, column: str, buckets: int) -> EquiDepthH
         z = np.zeros(0, dtype=np.int64)
         return EquiDepthHistogram(table.name, column, np.zeros(1, dtype=np.int64), z, z.copy(), null_count,
                                   table.row_count)
-    v = torch.sort(valid.to(torch.int64)).values
+    # the framework's own stable radix sort, then the sorted column as runs (value, start)
+    keys, _, dec = sorting.ordered_keys(valid)
+    skeys, _ = sorting.sort_pairs(keys)
+    uk, starts, _, _, stats = sorting.runs(skeys, dec, want_counts=False)
     k = min(buckets, n)
     # equi-depth split points at value boundaries; duplicates collapse buckets
     ranks = torch.tensor([0] + [min(n - 1, (i * n) // k - 1) for i in range(1, k + 1)], dtype=torch.int64,
-                         device=v.device)
-    at = v[ranks].cpu().tolist()
+                         device=valid.device)
+    at = sorting.rank_values(uk, starts, stats, ranks).cpu().tolist()
     edges = [int(at[0])]
     for e in at[1:]:
         if e > edges[-1]:
@@ -85,18 +89,11 @@ def build_histogram(table: ColumnTable, column: str, buckets: int) -> EquiDepthH
         edges.append(edges[0])
     boundaries = np.asarray(edges, dtype=np.int64)
     nb = len(boundaries) - 1
-    hi = torch.searchsorted(v, torch.as_tensor(boundaries[1:], device=v.device), right=True)
-    hi[-1] = n
-    # changes[i] = number of value changes in v[1..i]; distinct(lo, hi) = 1 + changes[hi-1] - changes[lo]
-    changes = torch.zeros(n, dtype=torch.int64, device=v.device)
-    if n > 1:
-        torch.cumsum((v[1:] != v[:-1]).to(torch.int64), 0, out=changes[1:])
+    hi, dist = sorting.hist_buckets(uk, starts, stats, n, torch.as_tensor(boundaries, device=valid.device))
     his = hi.cpu().numpy().astype(np.int64)
     los = np.concatenate(([0], his[:-1])).astype(np.int64)
-    ch_hi = changes[torch.as_tensor(np.maximum(his - 1, 0), device=v.device)].cpu().numpy()
-    ch_lo = changes[torch.as_tensor(np.minimum(los, n - 1), device=v.device)].cpu().numpy()
     counts = (his - los).astype(np.int64)
-    distincts = np.where(counts > 0, 1 + ch_hi - ch_lo, 0).astype(np.int64)
+    distincts = dist.cpu().numpy().astype(np.int64)
     return EquiDepthHistogram(table.name, column, boundaries, counts, distincts[:nb], null_count, table.row_count)
 
 

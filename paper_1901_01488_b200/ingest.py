@@ -32,6 +32,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from . import executor, sorting
 from .errors import CsvError, TypeMismatch
 from .storage import (DATE, INT64, Column, ColumnKind, ColumnTable, Dictionary, date_to_days, default_device,
                       format_decimal)
@@ -313,25 +314,11 @@ def _encode_text(data, d_bytes, field_end, field_kind, first_field, nrows, ncols
     dev = hashes.device
     if nrows == 0:
         return torch.empty(0, dtype=torch.int32, device=dev), Dictionary()
-    rows = torch.arange(nrows, device=dev)
-    valid = ~nulls
-    vrows = rows[valid]
-    codes = torch.zeros(nrows, dtype=torch.int32, device=dev)
-    rep = torch.full((nrows,), -1, dtype=torch.int64, device=dev)
+    # codes in first-appearance order by the framework's own device sort (esc_dict_encode: cells
+    # grouped by content hash with a stable radix sort, groups ordered by their first row)
+    codes, rep, first, u = sorting.dict_encode(hashes, nulls)
     words = []
-    if vrows.numel():
-        uniq, inverse = torch.unique(hashes[valid], return_inverse=True)
-        # first appearance = the first row of each group after a stable sort by group (an
-        # atomic-min scatter serialised on the few hot groups of a low-cardinality column:
-        # 549 us for 1M rows of 6 strings, ncu)
-        counts = torch.bincount(inverse, minlength=uniq.numel())
-        starts = torch.cumsum(counts, 0) - counts
-        first = vrows[torch.argsort(inverse, stable=True)[starts]]
-        order = torch.argsort(first)
-        code_of = torch.empty_like(order)
-        code_of[order] = torch.arange(order.numel(), device=dev)
-        codes[valid] = code_of[inverse].to(torch.int32)
-        rep[valid] = first[inverse]
+    if u:
         bad = torch.zeros(1, dtype=torch.int32, device=dev)
         N.check(N.load_library().esc_csv_verify_text(C.c_void_p(d_bytes.data_ptr()), C.c_void_p(field_end.data_ptr()),
                                                     C.c_void_p(field_kind.data_ptr()), first_field, nrows, ncols, col,
@@ -340,13 +327,14 @@ def _encode_text(data, d_bytes, field_end, field_kind, first_field, nrows, ncols
         if int(bad.item()):
             raise CsvError(f"{name}: TEXT content hash collision in column {col}; the device loader cannot "
                            "encode this file")
-        reps = first[order]
-        f = first_field + reps * ncols + col
-        fe = field_end[f].cpu().tolist()
-        prev = field_end[(f - 1).clamp(min=0)].cpu().tolist()
-        pk = field_kind[(f - 1).clamp(min=0)].cpu().tolist()
-        for fi, e, p_, k in zip(f.cpu().tolist(), fe, prev, pk):
-            s = 0 if fi == 0 else p_ + (2 if k == 3 else 1)
+        reps = first.cpu().numpy()
+        f = first_field + reps * ncols + col  # the representative cells' field numbers (host)
+        fi = torch.as_tensor(np.concatenate([f, np.maximum(f - 1, 0)]), device=dev)
+        ends = executor.gather_values(field_end, fi).cpu().numpy()  # esc_gather, one launch
+        fe, prev = ends[:u], ends[u:]
+        pk = executor.gather_values(field_kind, fi[u:]).cpu().numpy()
+        for fi_, e, p_, k in zip(f.tolist(), fe.tolist(), prev.tolist(), pk.tolist()):
+            s = 0 if fi_ == 0 else p_ + (2 if k == 3 else 1)
             words.append(_cell_text(data, s, e)[0])
     d = Dictionary()
     for w in words:
