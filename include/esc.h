@@ -472,6 +472,14 @@ int esc_csv_fields(const uint8_t* d_bytes, int64_t nbytes, int64_t* d_field_end,
 int esc_csv_parse(const uint8_t* d_bytes, const int64_t* d_field_end, const uint8_t* d_field_kind, int64_t first_field,
                   int64_t nrows, int32_t ncols, int32_t col, int32_t kind, int32_t scale, int64_t* d_values,
                   int64_t* d_lengths, uint8_t* d_nulls, uint64_t* d_first_error, void* stream);
+/* Record validation (the reference's csv.reader + per-record field count, storage.py:247-275):
+ * d_out[0] = min over malformed data records of (record << 32 | fields held; an empty line holds
+ * 0), ~0 when all hold ncols fields; d_out[1] = the first record-ending '\r' that is not the last
+ * byte (a lone CR inside a line, which Python's csv rejects), ~0 if none.  d_rec_end lists the
+ * data records' last fields (header skipped); first_field = the first data record's first field. */
+int esc_csv_check(const uint8_t* d_bytes, int64_t nbytes, const int64_t* d_field_end, const uint8_t* d_field_kind,
+                  int64_t nsep, const int64_t* d_rec_end, int64_t nrows, int64_t first_field, int32_t ncols,
+                  uint64_t* d_out, void* stream);
 /* TEXT dictionary check: d_bad |= 1 when a cell's content differs from its group representative's
  * (rep[row], -1 for NULL) — i.e. a 64-bit hash collision. */
 int esc_csv_verify_text(const uint8_t* d_bytes, const int64_t* d_field_end, const uint8_t* d_field_kind,

@@ -492,6 +492,41 @@ __global__ void csv_verify_kernel(const CsvVerify p) {
   }
 }
 
+// ---- record validation (the reference's csv.reader + field-count check, storage.py:247-275) ---
+// out[0] = min over bad records of (record << 32 | fields it holds) — a record holds ncols fields,
+//          an empty line holds 0 — or ~0 when every record is well formed;
+// out[1] = the first field-ending '\r' that is not the last byte (Python's csv rejects a lone CR
+//          inside a line), or ~0
+struct CsvCheck {
+  const uint8_t* b;
+  int64_t n;
+  const long long* field_end;
+  const uint8_t* field_kind;
+  int64_t nsep;
+  const long long* rec_end;  // the data records (the header's already skipped)
+  int64_t nrows;
+  long long first_field;
+  int32_t ncols;
+  unsigned long long* out;
+};
+
+__global__ void csv_check_kernel(const CsvCheck p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.nrows; i += stride) {
+    const long long e = p.rec_end[i];
+    const long long pv = i == 0 ? p.first_field - 1 : p.rec_end[i - 1];
+    const long long nf = e - pv;
+    const long long start = pv >= 0 ? p.field_end[pv] + (p.field_kind[pv] == 3 ? 2 : 1) : 0;
+    const long long got = (nf == 1 && p.field_end[e] == start) ? 0 : nf;
+    if (got != p.ncols) atomicMin(p.out, ((unsigned long long)i << 32) | (unsigned long long)(got & 0xFFFFFFFFll));
+  }
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < p.nsep; f += stride) {
+    if (p.field_kind[f] != 2) continue;
+    const long long pos = p.field_end[f];
+    if (pos < p.n - 1 && p.b[pos] == 13) atomicMin(p.out + 1, (unsigned long long)pos);
+  }
+}
+
 }  // namespace esc
 
 // ==========================================================================================
@@ -604,6 +639,39 @@ int esc_csv_verify_text(const uint8_t* d_bytes, const int64_t* d_field_end, cons
   esc::csv_verify_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("CSV verify launch: ") + cudaGetErrorString(e));
+  return ESC_OK;
+}
+
+int esc_csv_check(const uint8_t* d_bytes, int64_t nbytes, const int64_t* d_field_end, const uint8_t* d_field_kind,
+                  int64_t nsep, const int64_t* d_rec_end, int64_t nrows, int64_t first_field, int32_t ncols,
+                  uint64_t* d_out, void* stream) {
+  if (nbytes < 0 || nsep < 0 || nrows < 0 || ncols <= 0 || d_out == nullptr ||
+      (nsep > 0 && (d_field_end == nullptr || d_field_kind == nullptr)) || (nrows > 0 && d_rec_end == nullptr))
+    return fail(ESC_ERR_INVALID, "bad CSV check arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_out, 0xFF, 2 * sizeof(uint64_t), st);
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("CSV check init: ") + cudaGetErrorString(e));
+  const int64_t work = nrows > nsep ? nrows : nsep;
+  if (work == 0) return ESC_OK;
+  esc::CsvCheck p;
+  p.b = d_bytes;
+  p.n = nbytes;
+  p.field_end = reinterpret_cast<const long long*>(d_field_end);
+  p.field_kind = d_field_kind;
+  p.nsep = nsep;
+  p.rec_end = reinterpret_cast<const long long*>(d_rec_end);
+  p.nrows = nrows;
+  p.first_field = first_field;
+  p.ncols = ncols;
+  p.out = reinterpret_cast<unsigned long long*>(d_out);
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  int64_t blocks = (work + 255) / 256;
+  if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+  ++g_launches;
+  esc::csv_check_kernel<<<(unsigned)blocks, 256, 0, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("CSV check launch: ") + cudaGetErrorString(e));
   return ESC_OK;
 }
 

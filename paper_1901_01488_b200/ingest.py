@@ -221,33 +221,28 @@ def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=N
         nsep += 1
         nrec += 1
     field_end, field_kind, rec_end = field_end[:nsep], field_kind[:nsep], rec_end[:nrec]
-    # Python's csv (text without newline translation) rejects a lone '\r' that is followed by
-    # more data on its line; records of earlier lines are still checked first
-    lone_cr = -1
-    if nsep:
-        kinds2 = torch.nonzero(field_kind == 2).flatten()
-        pos = field_end[kinds2]
-        cr = pos[(d_bytes[pos.clamp(max=max(n - 1, 0))] == 13) & (pos < n - 1)]
-        if cr.numel():
-            lone_cr = int(cr.min())
     first_rec = 1 if has_header and nrec > 0 else 0
-    first_field = int(rec_end[0]) + 1 if first_rec else 0
     nrows = nrec - first_rec
-
-    # records must hold exactly ncols fields (an empty line is a record of 0 fields)
-    if nrows:
-        ends = rec_end[first_rec:]
-        prev = torch.cat([torch.tensor([first_field - 1], device=dev), ends[:-1]])
-        nfields = ends - prev
-        starts = torch.where(prev >= 0, field_end[prev.clamp(min=0)] + torch.where(
-            field_kind[prev.clamp(min=0)] == 3, 2, 1), torch.zeros_like(prev))
-        empty_line = (nfields == 1) & (field_end[ends] == starts)
-        got = torch.where(empty_line, torch.zeros_like(nfields), nfields)
-        bad = torch.nonzero(got != ncols)
-        if bad.numel():
-            r = int(bad[0, 0])
-            if lone_cr < 0 or int(field_end[ends[r]]) < data.rfind(b"\n", 0, lone_cr) + 1:
-                raise CsvError(f"{name}: row {first_rec + r + 1}: expected {ncols} fields, got {int(got[r])}")
+    # records must hold exactly ncols fields (an empty line is a record of 0 fields), and Python's
+    # csv (text without newline translation) rejects a lone '\r' that is followed by more data on
+    # its line; records of earlier lines are still checked first — one device pass (esc_csv_check)
+    first_field = 0
+    if first_rec:
+        first_field = int(rec_end[0].item()) + 1
+    chk = torch.empty(2, dtype=torch.int64, device=dev)
+    N.check(lib.esc_csv_check(C.c_void_p(d_bytes.data_ptr()), n, C.c_void_p(field_end.data_ptr()) if nsep else None,
+                              C.c_void_p(field_kind.data_ptr()) if nsep else None, nsep,
+                              C.c_void_p(rec_end.data_ptr() + 8 * first_rec) if nrows else None, nrows, first_field,
+                              ncols, C.c_void_p(chk.data_ptr()), sp), "esc_csv_check")
+    bad_word, cr_word = (int(x) & ((1 << 64) - 1) for x in chk.cpu().tolist())
+    lone_cr = -1 if cr_word == (1 << 64) - 1 else cr_word
+    if bad_word != (1 << 64) - 1:
+        r, got = bad_word >> 32, bad_word & 0xFFFFFFFF
+        if got >= 1 << 31:
+            got -= 1 << 32
+        last_field = int(rec_end[first_rec + r].item())
+        if lone_cr < 0 or int(field_end[last_field].item()) < data.rfind(b"\n", 0, lone_cr) + 1:
+            raise CsvError(f"{name}: row {first_rec + r + 1}: expected {ncols} fields, got {got}")
     if lone_cr >= 0:
         raise csv.Error("new-line character seen in unquoted field - do you need to open the file with newline=''?")
 
