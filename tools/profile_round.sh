@@ -24,7 +24,7 @@ $N -k regex:esc_scan_kernel --launch-skip 30 --launch-count 1 -o gpurun_out/prof
     > gpurun_out/prof/k1c2.log 2>&1
 $N -k regex:sel_compact --launch-skip 10 --launch-count 1 -o gpurun_out/prof/selc_config2 python tools/diag_config2.py \
     > gpurun_out/prof/selc2.log 2>&1
-$N -k regex:esc_scan_kernel --launch-skip 60 --launch-count 1 -o gpurun_out/prof/onepass_dim python tools/diag_onepass2.py \
+$N -k regex:esc_scan_kernel --launch-skip 60 --launch-count 1 -o gpurun_out/prof/onepass_dim python tools/diag_onepass.py \
     > gpurun_out/prof/op.log 2>&1
 fi
 ls -la gpurun_out/prof
