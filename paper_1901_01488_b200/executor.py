@@ -462,6 +462,8 @@ def eval_predicate(table: ColumnTable, pred: ex.Expr | None,
         count, fails, _, _, rows = launch_compact(cp, table, None, n, [], n, want_row_ids=True)
         if cp.unbound or cp.may_fail:
             raise_udf_errors(table, cp, fails, None, n)
+        if count * 4 < n:  # don't pin an n-row buffer for a small selection: exact-size copy
+            rows = _exact_copy(rows, count, _stream(table.device))
         return RowSelection(table, rows[:count])
     sel = select(table, pred, selection)
     _, _, rows = launch_materialize_selection(sel, [], sel.count, want_row_ids=True)
@@ -851,6 +853,17 @@ def _trim(proj: list, values: list, nulls: list, count: int, stream, cache: dict
             mm = outs[r]
             r += 1
         out.append(Column.device_column(c.name, c.kind, vv, mm, c.dictionary))
+    return out
+
+
+def _exact_copy(t: torch.Tensor, k: int, stream) -> torch.Tensor:
+    """The first ``k`` elements of a device tensor in a new exact-size tensor (esc_copy_regions)."""
+    out = torch.empty(k, dtype=t.dtype, device=t.device)
+    if k:
+        nbytes = k * t.element_size()
+        N.check(N.load_library().esc_copy_regions(1, (C.c_void_p * 1)(out.data_ptr()),
+                                                  (C.c_void_p * 1)(t.data_ptr()), (C.c_int64 * 1)(nbytes),
+                                                  C.c_void_p(stream.cuda_stream)), "esc_copy_regions")
     return out
 
 

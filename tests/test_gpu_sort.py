@@ -144,3 +144,31 @@ def test_large_hash_build_grouping(cuda, dtype):
         assert np.array_equal(idx.unique_keys.cpu().numpy(), oi.unique_keys)
         assert np.array_equal(idx.group_rows.cpu().numpy(), oi.group_rows)
         assert np.array_equal(idx.group_start.cpu().numpy()[: len(oi.group_start)], oi.group_start)
+
+
+@pytest.mark.parametrize("dtype", ["uint8", "uint16", "uint32", "int8", "int16", "int32"])
+def test_one_block_hash_build_matches_numpy(cuda, dtype):
+    """The one-block build (<= 16K rows, keys <= 4 bytes) against numpy's unique + stable argsort,
+    for unsigned keys (bias 0) and keys equal to the 32-bit padding sentinel (0xFFFFFFFF after
+    the bias: INT32_MAX, UINT32_MAX), with duplicates and a row subset."""
+    from paper_1901_01488_b200 import join
+    from paper_1901_01488_b200.storage import Column, ColumnKind, ColumnTable
+
+    np_dt = np.dtype(dtype)
+    info = np.iinfo(np_dt)
+    g = np.random.default_rng(5)
+    for n in (1, 100, 8192, 16_384):
+        keys = g.integers(int(info.min), int(info.max) + 1, n, dtype=np.int64).astype(np_dt)
+        keys[: min(n, 3)] = info.max  # the sentinel after biasing, and duplicates of it
+        if n > 10:
+            keys[5:9] = info.min
+        t = ColumnTable("b", [Column("k", ColumnKind("INT64"), keys, device=cuda)])
+        rows = np.sort(g.choice(n, max(n // 2, 1), replace=False)).astype(np.int64)
+        for sel in (None, rows):
+            idx = join.HashTableIndex(t, "k", torch.from_numpy(sel).to(cuda) if sel is not None else None)
+            sub = keys.astype(np.int64) if sel is None else keys.astype(np.int64)[sel]
+            base = np.arange(n) if sel is None else sel
+            u = np.unique(sub)
+            order = np.argsort(sub, kind="stable")
+            assert np.array_equal(idx.unique_keys.cpu().numpy(), u), (dtype, n)
+            assert np.array_equal(idx.group_rows.cpu().numpy(), base[order]), (dtype, n)
