@@ -511,13 +511,19 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
-def _flush_l2(dev):
+def _flush_l2(dev, clean: bool = False):
+    """Evict L2 with a buffer twice its size: written (``clean`` False — L2 is left full of DIRTY
+    lines, so the next kernel's first 126 MB of reads also pay their write-backs), or read
+    (``clean`` True — L2 left holding clean lines, what a scan meets after other reads)."""
     import torch
 
     buf = getattr(_flush_l2, "buf", None)
     if buf is None:
-        buf = _flush_l2.buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
-    buf.zero_()
+        buf = _flush_l2.buf = torch.zeros(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    if clean:
+        buf.view(torch.int64).max()
+    else:
+        buf.zero_()
 
 
 def _time_kernels(fn, reps, dev, flush=False):
@@ -536,7 +542,7 @@ def _time_kernels(fn, reps, dev, flush=False):
     return [(a.elapsed_time(b), k) for a, b, k in ev]
 
 
-def _device_step_ms(launch, finish, reps, dev, flush=True) -> float:
+def _device_step_ms(launch, finish, reps, dev, flush=True, clean=False) -> float:
     """Median device time of ``launch()`` (kernels queued, no host wait inside): L2 flushed, then
     a ~1 ms sleep kernel holds the stream while the host enqueues the events and the launches, so
     the events bracket device work only; ``finish(result)`` after each rep."""
@@ -549,7 +555,7 @@ def _device_step_ms(launch, finish, reps, dev, flush=True) -> float:
     ts = []
     for _ in range(reps):
         if flush:
-            _flush_l2(dev)
+            _flush_l2(dev, clean)
         torch.cuda._sleep(2_000_000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -589,12 +595,17 @@ def run_extras(table, w, pred, cfg, dev, peak):
     c2.temps.sweep()
     cap2 = (d.row_count * 1) // 5  # floor(0.2 * rows): the queued step's capacity
     kms = _device_step_ms(lambda: executor.launch_step(t2, p2, w2.project, cap2), executor.finish_step, 15, dev)
+    kms_clean = _device_step_ms(lambda: executor.launch_step(t2, p2, w2.project, cap2), executor.finish_step, 15,
+                                dev, clean=True)
     b2 = w2.algorithmic_bytes(d.exact_count)
     out["config2_fused"] = {"count": d.exact_count, "kernel_ms": kms, "rows_per_s": w2.nrows / (kms * 1e-3),
                             "GBps": b2 / (kms * 1e-3) / 1e9, "frac": b2 / (kms * 1e-3) / 1e9 / peak,
+                            "kernel_ms_clean_l2": kms_clean, "frac_clean_l2": b2 / (kms_clean * 1e-3) / 1e9 / peak,
                             "note": "device time of the queued step (K1 select + one-kernel mid-size compaction), "
-                                    "L2 flushed before every rep; a sleep kernel holds the stream while the step "
-                                    "is enqueued, so no host launch latency is inside the events"}
+                                    "L2 flushed before every rep by WRITING 252 MB (kernel_ms: the scan's first reads "
+                                    "also pay the flush's dirty write-backs) or by READING it (kernel_ms_clean_l2); "
+                                    "a sleep kernel holds the stream while the step is enqueued, so no host launch "
+                                    "latency is inside the events"}
 
     # config 3: the 4-dimension star query — ESC overhead (reference definition, engine.py:69) and
     # the query executed end to end (Engine.run: ESC + hash builds over the temps + the fused

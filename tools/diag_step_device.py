@@ -17,13 +17,13 @@ p2 = serde.from_json(w2.pred, "lineitem")
 cap = int(0.2 * t2.row_count)
 
 
-def measure(label, parts=None, reps=15):
+def measure(label, parts=None, reps=15, clean=False):
     for _ in range(3):
         ps = executor.launch_step(t2, p2, w2.project, cap)
         torch.cuda.synchronize(); executor.finish_step(ps)
     ts = []
     for _ in range(reps):
-        bench._flush_l2(dev)
+        bench._flush_l2(dev, clean)
         torch.cuda._sleep(2_000_000)  # ~1 ms: the host enqueues the step meanwhile
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -36,6 +36,7 @@ def measure(label, parts=None, reps=15):
 
 
 measure("default")
-N.set_mid_max_rows(0); measure("mid off"); N.set_mid_max_rows(32 << 20)
+measure("default, clean L2", clean=True)
+N.set_mid_max_rows(0); measure("mid off"); measure("mid off, clean L2", clean=True); N.set_mid_max_rows(32 << 20)
 for k, v in list(os.environ.items()):
     pass
