@@ -293,7 +293,9 @@ int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, in
                          esc_selection_t* sel, const esc_column_t* mat_cols, int32_t mat_ncols,
                          const esc_outputs_t* outs, esc_result_t* result, void* d_ws, size_t ws_bytes,
                          void** out_plan);
-int esc_step_plan_launch(void* plan, int32_t parts, void* stream); /* parts: 1 scan, 2 compaction, 3 both */
+#define ESC_PLAN_GRAPH 4 /* esc_step_plan_launch parts flag: issue a single part as a (cached) CUDA graph too */
+int esc_step_plan_launch(void* plan, int32_t parts, void* stream); /* parts: 1 scan, 2 compaction, 3 both
+                                                                      (| ESC_PLAN_GRAPH) */
 int esc_step_plan_rebind(void* plan, const esc_outputs_t* outs); /* one-pass plans; same n_proj,
                                                                      slots, capacity, null outputs */
 int esc_step_plan_destroy(void* plan);

@@ -108,6 +108,7 @@ class EscJoin(C.Structure):
 
 SEG_CAPTURED = 0x80000000
 OUT_SKIP_OVER_CAPACITY = 1
+PLAN_GRAPH = 4  # esc_step_plan_launch: a single part as a cached CUDA graph
 STRUCTS = [EscProgram, EscInstr, EscUdf, EscUdfOp, EscColumn, EscResult, EscOutputs, EscSelection, EscJoinStep,
            EscJoin]
 

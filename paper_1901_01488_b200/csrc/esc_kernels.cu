@@ -1150,6 +1150,8 @@ int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, in
 
 int esc_step_plan_launch(void* plan, int32_t parts, void* stream) {
   if (plan == nullptr) return fail(ESC_ERR_INVALID, "null plan");
+  const bool force_graph = (parts & ESC_PLAN_GRAPH) != 0;
+  parts &= ~ESC_PLAN_GRAPH;
   if (parts < 1 || parts > 3) return fail(ESC_ERR_INVALID, "parts must be 1 (scan), 2 (compaction) or 3");
   StepPlanImpl* p = static_cast<StepPlanImpl*>(plan);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1158,10 +1160,12 @@ int esc_step_plan_launch(void* plan, int32_t parts, void* stream) {
     const int rc = next_epoch(p->kp, p->kp.nrows, p->kp.hdr, st);
     return rc != ESC_OK ? rc : issue_scan(p->scan, p->kp, st);
   }
-  // graphs for whole steps only: the profiling split (parts 1 / 2 with events between) launches
-  // directly — as two graphs the split measured 30-40 us longer on a 6M-row table (the PDL
-  // overlap between the scan and the compaction chain does not cross graph boundaries)
-  if (parts == 3 && g_graphs.load() && g_trace == nullptr && !p->graph_failed[parts]) {
+  // graphs for whole steps, or for a part when asked (ESC_PLAN_GRAPH): the profiling split
+  // (parts 1 / 2 with events between) launches directly — as two graphs it measured 30-40 us
+  // longer on a 6M-row table, since the PDL overlap of the scan and the compaction chain does not
+  // cross graph boundaries; the multi-GPU step, whose count exchange sits between the parts
+  // anyway, asks for graphs (no kilobyte parameter blocks marshalled per launch)
+  if ((parts == 3 || force_graph) && g_graphs.load() && g_trace == nullptr && !p->graph_failed[parts]) {
     if (p->graph[parts] == nullptr && !capture_parts(p, parts)) {
       p->graph_failed[parts] = true;
       return issue_parts(p, parts, st);

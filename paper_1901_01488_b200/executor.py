@@ -602,7 +602,7 @@ def launch_step(table: ColumnTable, pred: ex.Expr, needed, capacity: int, materi
     if gated:
         for part, kind in ((1, "select"), (2, "materialize")):
             ev0 = _ev_start(stream)
-            N.check(lib.esc_step_plan_launch(C.c_void_p(handle.ptr), part, sp), "esc_step_plan_launch")
+            N.check(lib.esc_step_plan_launch(C.c_void_p(handle.ptr), part | N.PLAN_GRAPH, sp), "esc_step_plan_launch")
             _ev_end(stream, ev0, kind)
             if part == 1:
                 between(plan, stream)
