@@ -106,11 +106,21 @@ enum {
   ESC_UDF_MOD = 7,      /* CPython float_rem (floored), error on %0     */
   ESC_UDF_FLOORDIV = 8, /* CPython float_floor_div, error on //0        */
   ESC_UDF_NEG = 9, ESC_UDF_ABS = 10,
-  ESC_UDF_SQUARE = 11   /* x ** 2 (OverflowError when finite x overflows) */
+  ESC_UDF_SQUARE = 11,  /* x ** 2 (OverflowError when finite x overflows) */
+  /* comparisons: pop b, a; push 1.0 if (a op b) else 0.0 (IEEE: NaN compares false, != true) */
+  ESC_UDF_LT = 12, ESC_UDF_LE = 13, ESC_UDF_GT = 14, ESC_UDF_GE = 15, ESC_UDF_EQ = 16, ESC_UDF_NE = 17,
+  /* control flow of traced branches (if / else, conditional expressions, min / max): offsets in
+   * `arg`, relative to the next op, always forward */
+  ESC_UDF_JMPF = 18,    /* pop c; skip `arg` ops when c == 0.0 */
+  ESC_UDF_JMP = 19,     /* skip `arg` ops */
+  /* math.floor / math.ceil / int(): integral result (ValueError on NaN, OverflowError on inf) */
+  ESC_UDF_FLOOR = 20, ESC_UDF_CEIL = 21, ESC_UDF_TRUNC = 22,
+  ESC_UDF_SQRT = 23     /* math.sqrt (ValueError "math domain error" below zero) */
 };
 
 /* UDF failure codes (low 3 bits of esc_result_t.udf_fail[]) */
-enum { ESC_FAIL_DIV = 1, ESC_FAIL_MOD = 2, ESC_FAIL_FLOORDIV = 3, ESC_FAIL_POW = 4 };
+enum { ESC_FAIL_DIV = 1, ESC_FAIL_MOD = 2, ESC_FAIL_FLOORDIV = 3, ESC_FAIL_POW = 4, ESC_FAIL_NAN_INT = 5,
+       ESC_FAIL_INF_INT = 6, ESC_FAIL_DOMAIN = 7 };
 
 typedef union {
   int64_t i;

@@ -407,6 +407,23 @@ __device__ __noinline__ double udf_eval(const KParams& p, const esc_udf_t& u, co
         stk[sp - 1] = y;
         break;
       }
+      case ESC_UDF_JMPF:
+        if (stk[--sp] == 0.0) i += o.arg;
+        break;
+      case ESC_UDF_JMP: i += o.arg; break;
+      case ESC_UDF_FLOOR: case ESC_UDF_CEIL: case ESC_UDF_TRUNC: {
+        const double x = stk[sp - 1];
+        if (isnan(x)) { *fail = ESC_FAIL_NAN_INT; return 0.0; }
+        if (isinf(x)) { *fail = ESC_FAIL_INF_INT; return 0.0; }
+        stk[sp - 1] = o.op == ESC_UDF_FLOOR ? floor(x) : o.op == ESC_UDF_CEIL ? ceil(x) : trunc(x);
+        break;
+      }
+      case ESC_UDF_SQRT: {
+        const double x = stk[sp - 1];
+        if (x < 0.0) { *fail = ESC_FAIL_DOMAIN; return 0.0; }
+        stk[sp - 1] = __dsqrt_rn(x);
+        break;
+      }
       default: {
         const double b = stk[--sp];
         const double a = stk[sp - 1];
@@ -423,10 +440,16 @@ __device__ __noinline__ double udf_eval(const KParams& p, const esc_udf_t& u, co
             if (b == 0.0) { *fail = ESC_FAIL_MOD; return 0.0; }
             r = py_mod(a, b);
             break;
-          default:  // FLOORDIV
+          case ESC_UDF_FLOORDIV:
             if (b == 0.0) { *fail = ESC_FAIL_FLOORDIV; return 0.0; }
             r = py_floordiv(a, b);
             break;
+          case ESC_UDF_LT: r = a < b ? 1.0 : 0.0; break;
+          case ESC_UDF_LE: r = a <= b ? 1.0 : 0.0; break;
+          case ESC_UDF_GT: r = a > b ? 1.0 : 0.0; break;
+          case ESC_UDF_GE: r = a >= b ? 1.0 : 0.0; break;
+          case ESC_UDF_EQ: r = a == b ? 1.0 : 0.0; break;
+          default: r = a != b ? 1.0 : 0.0; break;  // ESC_UDF_NE
         }
         stk[sp - 1] = r;
       }

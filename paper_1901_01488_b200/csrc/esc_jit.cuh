@@ -168,6 +168,15 @@ constexpr double kExact = 9007199254740992.0;  // 2^53
 
 std::string as_double(const Val& v) { return v.is_int ? "(double)" + v.name : v.name; }
 
+// UDFs gen_udf_body turns into straight-line code: arithmetic only (no branches, comparisons
+// or math functions — those run through the interpreter's atom_udf)
+bool straight_line_udf(const KParams& kp, int ui) {
+  const esc_udf_t& u = kp.udfs[ui];
+  for (int i = 0; i < u.n_ops; ++i)
+    if (kp.udf_ops[u.first_op + i].op > ESC_UDF_SQUARE) return false;
+  return true;
+}
+
 // UDF `ui` of the program -> statements computing `double`/`long long` result; returns its Val
 Val gen_udf_body(const KParams& kp, int ui, std::ostringstream& o, const std::string& pfx) {
   const esc_udf_t& u = kp.udfs[ui];
@@ -431,6 +440,11 @@ bool gen_pred(const KParams& kp, int C, std::ostringstream& o) {
         const esc_udf_t& u = kp.udfs[K.aux];
         const std::string ce = K.combine == ESC_COMB_AND ? (care + " & " + acc)
                                : K.combine == ESC_COMB_OR ? (care + " & ~" + acc) : care;
+        if (!straight_line_udf(kp, K.aux)) {
+          // branches / math: the interpreter's atom (a jump-aware stack machine) on the staged tile
+          o << "      r = atom_udf(p, " << I << ", rr, " << ce << ", valid);\n";
+          break;
+        }
         o << "      r = 0u;\n      uint32_t todo = " << (u.dense ? std::string("valid") : "(" + ce + ") & valid")
           << ";\n      while (todo) {\n        const int bit = __ffs(todo) - 1;\n        todo &= todo - 1;\n"
           << "        const int lr = l0 + " << kChunkRows << " * (bit >> 2) + (bit & 3);\n"

@@ -193,25 +193,44 @@ int validate_program(const esc_program_t* prog, int32_t ncols) {
         return fail(ESC_ERR_INVALID, "UDF out of range");
       for (int a = 0; a < u.n_args; ++a)
         if (u.arg_col[a] >= ncols) return fail(ESC_ERR_INVALID, "UDF argument slot out of range");
-      int sp = 0;
+      // stack heights along every path (jumps only go forward, so one pass in op order visits each
+      // op after all of its predecessors): a branch merge must see one height, the end exactly 1
+      int height[ESC_MAX_UDF_OPS + 1];
+      for (int k = 0; k <= u.n_ops; ++k) height[k] = -1;
+      height[0] = 0;
       for (int k = 0; k < u.n_ops; ++k) {
         const esc_udf_op_t& o = prog->udf_ops[u.first_op + k];
+        int sp = height[k];
+        if (sp < 0) continue;  // unreachable
+        int jump = -1;  // extra successor
+        bool falls = true;
         if (o.op == ESC_UDF_ARG) {
           if (o.arg >= u.n_args) return fail(ESC_ERR_INVALID, "UDF ARG index out of range");
           ++sp;
         } else if (o.op == ESC_UDF_CONST) {
           ++sp;
-        } else if (o.op == ESC_UDF_NEG || o.op == ESC_UDF_ABS || o.op == ESC_UDF_SQUARE) {
+        } else if (o.op == ESC_UDF_NEG || o.op == ESC_UDF_ABS || o.op == ESC_UDF_SQUARE ||
+                   (o.op >= ESC_UDF_FLOOR && o.op <= ESC_UDF_SQRT)) {
           if (sp < 1) return fail(ESC_ERR_INVALID, "UDF stack underflow");
-        } else if (o.op >= ESC_UDF_ADD && o.op <= ESC_UDF_FLOORDIV) {
+        } else if ((o.op >= ESC_UDF_ADD && o.op <= ESC_UDF_FLOORDIV) || (o.op >= ESC_UDF_LT && o.op <= ESC_UDF_NE)) {
           if (sp < 2) return fail(ESC_ERR_INVALID, "UDF stack underflow");
           --sp;
+        } else if (o.op == ESC_UDF_JMPF || o.op == ESC_UDF_JMP) {
+          if (o.op == ESC_UDF_JMPF && sp-- < 1) return fail(ESC_ERR_INVALID, "UDF stack underflow");
+          jump = k + 1 + o.arg;
+          if (jump > u.n_ops) return fail(ESC_ERR_INVALID, "UDF jump out of range");
+          falls = o.op == ESC_UDF_JMPF;
         } else {
           return fail(ESC_ERR_INVALID, "bad UDF opcode");
         }
         if (sp > 16) return fail(ESC_ERR_INVALID, "UDF stack overflow");
+        for (int t : {falls ? k + 1 : -1, jump}) {
+          if (t < 0) continue;
+          if (height[t] >= 0 && height[t] != sp) return fail(ESC_ERR_INVALID, "UDF branches leave different stacks");
+          height[t] = sp;
+        }
       }
-      if (sp != 1) return fail(ESC_ERR_INVALID, "UDF program must leave one value");
+      if (height[u.n_ops] != 1) return fail(ESC_ERR_INVALID, "UDF program must leave one value");
     }
   }
   if (depth != 0) return fail(ESC_ERR_INVALID, "unbalanced PUSH/POP");

@@ -48,8 +48,7 @@ def test_may_fail_flags():
 
 
 @pytest.mark.parametrize("fn,msg", [
-    (lambda x: x if x > 0 else -x, "control flow"),
-    (lambda x: math.sqrt(x), "float()"),
+    (lambda x: math.exp(x), "float()"),
     (lambda x: x ** 3, "\\*\\* 3"),
     (lambda x: "s", "returns str"),
     (lambda x: round(x), "float()"),
@@ -66,3 +65,49 @@ def test_failure_messages_are_cpythons():
         1.0 % 0.0
     except ZeroDivisionError as e:
         assert FAIL_MESSAGES[N.FAIL_MOD] == str(e)
+
+
+BRANCHY = [
+    (lambda x, y: x if x > y else y * 0.5, 2),
+    (lambda x, y: min(x, y, 0.25) - max(x, -y), 2),
+    (lambda x, y: -1.0 if x < -1 else (1.0 if x > 1 else x), 2),
+    (lambda x, y: x / y if y != 0 else 0.0, 2),
+    (lambda x, y: math.floor(x / 10.0) % 7 + y, 2),
+    (lambda x, y: math.ceil(x) // 3, 2),
+    (lambda x, y: math.trunc(x) * 0.5 - math.fabs(y), 2),
+    (lambda x, y: math.sqrt(abs(x)) if x == x else y, 2),
+    (lambda x, y: 1.0 if (x > 0 and y > 0) or x < -5 else 2.0, 2),
+    (lambda x, y: 0.0 if math.isnan(x) or math.isinf(y) else x, 2),
+    (lambda x, y: x > y, 2),
+    (lambda x, y: (x > 0) * 3.0 + y, 2),
+]
+
+
+@pytest.mark.parametrize("fn,n", BRANCHY)
+def test_branchy_trace_equals_python(fn, n):
+    """Path-enumerated programs (jumps, comparisons, floor/ceil/trunc/sqrt/fabs/isnan/isinf)
+    reproduce CPython on every path, errors included."""
+    prog = trace(fn, n)
+    rng = random.Random(11)
+    special = [0.0, -0.0, 1.0, -1.0, 7.0, -9.0, 13.5, -2.25, 1e15, math.nan, math.inf, -math.inf]
+    for _ in range(1500):
+        args = [rng.choice(special + [rng.uniform(-50, 50)]) for _ in range(n)]
+        try:
+            want = ("ok", float(fn(*args)))
+        except (ArithmeticError, ValueError) as exc:
+            want = ("err", str(exc))
+        try:
+            got = ("ok", prog.evaluate(args))
+        except (ArithmeticError, ValueError) as exc:
+            got = ("err", str(exc))
+        if want[0] == got[0] == "ok" and math.isnan(want[1]):
+            assert math.isnan(got[1]), args
+        else:
+            assert want == got, args
+
+
+@pytest.mark.parametrize("fn", [lambda x: math.floor(x) + math.floor(x), lambda x: float(x), lambda x: math.exp(x),
+                                lambda x: math.floor(x) * 2, lambda x: x ** 3, lambda x: round(x)])
+def test_untraceable_branchy_refused(fn):
+    with pytest.raises(UnsupportedUdf):
+        trace(fn, 1)
