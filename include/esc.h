@@ -179,6 +179,9 @@ typedef struct {
   const uint8_t* nulls; /* device pointer to a bool mask (1 = NULL), or NULL if none  */
   int32_t dtype;        /* ESC_I8 ...                                                 */
   int32_t flags;        /* ESC_COL_* hints                                            */
+  const uint32_t* null_bits; /* optional: the same NULLs packed 1 bit per row (bit r%32 of word
+                                r/32; esc_pack_nulls); count / selection scans then stream N/8
+                                bytes of NULL state instead of N.  NULL = use the byte mask */
 } esc_column_t;
 
 /* esc_column_t.flags: stage this column through shared memory even when the program does not
@@ -323,6 +326,11 @@ int esc_step_plan_destroy(void* plan);
  * No host round trip between the scan, the exchange and the compaction. */
 int esc_count_gate(const int64_t* counts, int32_t world, int32_t rank, int64_t capacity, int64_t* out,
                    void* stream);
+
+/* Packed NULL bitmap of a bool mask: bit (r & 31) of out[r >> 5] = nulls[r] != 0; out holds
+ * esc_null_bits_words(n) words (the last ones zero-padded to a 16-byte multiple). */
+int64_t esc_null_bits_words(int64_t n);
+int esc_pack_nulls(const uint8_t* nulls, int64_t n, uint32_t* out, void* stream);
 
 /* out[i] = col[idx[i]] (values and, when present, nulls).  replaces Column.take
  * (storage.py:176-184). */

@@ -70,7 +70,8 @@ class EscProgram(C.Structure):
 
 
 class EscColumn(C.Structure):
-    _fields_ = [("data", C.c_void_p), ("nulls", C.c_void_p), ("dtype", C.c_int32), ("flags", C.c_int32)]
+    _fields_ = [("data", C.c_void_p), ("nulls", C.c_void_p), ("dtype", C.c_int32), ("flags", C.c_int32),
+                ("null_bits", C.c_void_p)]
 
 
 class EscResult(C.Structure):
@@ -135,6 +136,8 @@ _SIGNATURES = {
     "esc_gather": (C.c_int, [C.POINTER(EscColumn), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                              C.c_void_p]),
     "esc_count_gate": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p]),
+    "esc_null_bits_words": (C.c_int64, [C.c_int64]),
+    "esc_pack_nulls": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "esc_last_error": (C.c_char_p, []),
     "esc_launch_count": (C.c_int64, []),
     "esc_abi_version": (C.c_int, []),

@@ -21,6 +21,8 @@ dictionary codes built with Python string comparisons (``executor.py:73-94``).
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import threading
 import warnings
@@ -34,6 +36,17 @@ from . import _native as N
 from . import expr as ex
 from .errors import ExecutionError
 from .udf import UdfProgram, trace
+
+# count / selection scans stage nullable columns' NULLs as packed bits (ESC_PACKED_NULLS=0: bytes)
+_PACKED_NULLS = os.environ.get("ESC_PACKED_NULLS", "1") == "1"
+
+
+def set_packed_nulls(on: bool) -> bool:
+    """Stage packed NULL bitmaps in scans (True) or the byte masks; returns the previous setting
+    (tests, measurement).  Affects predicates compiled afterwards."""
+    global _PACKED_NULLS
+    prev, _PACKED_NULLS = _PACKED_NULLS, bool(on)
+    return prev
 
 _I64_MIN, _I64_MAX = -(2**63), 2**63 - 1
 _NP_OF_TORCH = {
@@ -91,6 +104,8 @@ class CompiledPredicate:
             N.require_cuda(col.values, f"column {col.name!r}")
             arr[i].data = col.values.data_ptr() if len(col) else None
             arr[i].nulls = col.nulls.data_ptr() if col.nulls is not None and len(col) else None
+            nb = col.null_bits if _PACKED_NULLS and col.nulls is not None and len(col) else None
+            arr[i].null_bits = nb.data_ptr() if nb is not None else None
             arr[i].dtype = N.dtype_code(col.values)
             arr[i].flags = 0
         return arr

@@ -23,6 +23,7 @@ constexpr unsigned long long kStatusValueMask = (1ull << kStatusValueBits) - 1;
 constexpr unsigned long long kFlagAggregate = 1;
 constexpr unsigned long long kFlagPrefix = 2;
 constexpr uint32_t kNoNulls = 0xFFFFFFFFu;
+constexpr uint32_t kPackedNulls = 0x80000000u;  // KInstr.noff flag: the staged NULLs are 1 bit per row
 
 template <bool COMPACT>
 struct Layout {
@@ -70,7 +71,8 @@ struct KCol {
   int32_t dtype;
   int32_t width;
   int32_t staged;       // values staged in smem for full tiles
-  int32_t nulls_staged; // null bytes staged in smem for full tiles
+  int32_t nulls_staged; // NULLs staged in smem for full tiles: 1 = a byte per row, 2 = a bit per row
+  const uint32_t* null_bits;  // packed NULL bitmap (count / selection scans stage it), or nullptr
   uint32_t smem_off;
   uint32_t smem_null_off;
 };
@@ -289,6 +291,23 @@ __device__ __forceinline__ uint32_t null_bits_staged(const uint8_t* nb, int loca
   }
   return bits;
 }
+// the same 4*C NULL flags from a staged 1-bit-per-row bitmap (row-linear words)
+template <int C>
+__device__ __forceinline__ uint32_t null_bits_packed(const uint8_t* nb, int local0) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(nb);
+  uint32_t bits = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int r = local0 + kChunkRows * c;  // 4 consecutive rows inside one word (r % 4 == 0)
+    bits |= ((w[r >> 5] >> (r & 31)) & 0xFu) << (4 * c);
+  }
+  return bits;
+}
+template <int C>
+__device__ __forceinline__ uint32_t staged_nulls(const uint8_t* stage, uint32_t noff, int local0) {
+  return (noff & kPackedNulls) ? null_bits_packed<C>(stage + (noff & ~kPackedNulls), local0)
+                               : null_bits_staged<C>(stage + noff, local0);
+}
 
 __device__ __forceinline__ bool cmp_any(int cmp, double a, double b) {
   switch (cmp) {
@@ -349,7 +368,12 @@ __device__ __forceinline__ const uint8_t* value_ptr(const KCol& col, const RowRe
 }
 __device__ __forceinline__ bool is_null(const KCol& col, const RowRef& rr, int bit) {
   if (col.nulls == nullptr) return false;
-  if (rr.stage != nullptr && col.nulls_staged) return rr.stage[col.smem_null_off + local_row(rr, bit)] != 0;
+  if (rr.stage != nullptr && col.nulls_staged) {
+    const int32_t l = local_row(rr, bit);
+    if (col.nulls_staged == 2)
+      return (reinterpret_cast<const uint32_t*>(rr.stage + col.smem_null_off)[l >> 5] >> (l & 31)) & 1u;
+    return rr.stage[col.smem_null_off + l] != 0;
+  }
   return __ldg(col.nulls + phys_row(rr, logical_row(rr, bit))) != 0;
 }
 
@@ -609,7 +633,7 @@ __device__ __forceinline__ uint32_t eval_program(const KParams& p, const RowRef&
         r = FAST ? range_f32<C>(col, l0, (float)I.lo.f, (float)I.hi.f) : atom_generic(p, I, rr, valid);
         break;
       case K_NOTNULL:
-        r = FAST ? (I.noff != kNoNulls ? ~null_bits_staged<C>(rr.stage + I.noff, l0) : 0xFFFFFFFFu)
+        r = FAST ? (I.noff != kNoNulls ? ~staged_nulls<C>(rr.stage, I.noff, l0) : 0xFFFFFFFFu)
                  : atom_generic(p, I, rr, valid);
         break;
       default:  // K_RANGE_F64, K_LUT, K_COLCMP
@@ -618,7 +642,7 @@ __device__ __forceinline__ uint32_t eval_program(const KParams& p, const RowRef&
     }
     if (FAST && op <= K_RANGE_F32) {
       if (I.inv) r = ~r;
-      if (I.noff != kNoNulls) r &= ~null_bits_staged<C>(rr.stage + I.noff, l0);
+      if (I.noff != kNoNulls) r &= ~staged_nulls<C>(rr.stage, I.noff, l0);
     }
     if (I.neg) r = ~r;
     acc = combine(I.combine, acc, r);
@@ -933,7 +957,7 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
             const unsigned long long b = ((unsigned long long)r1 * col.width) & ~15ull;
             if (b > a) bulk_prefetch_l2(col.data + a, b - a);
           }
-          if (col.nulls_staged) {
+          if (col.nulls_staged == 1) {
             const unsigned long long a = (unsigned long long)r0 & ~15ull, b = (unsigned long long)r1 & ~15ull;
             if (b > a) bulk_prefetch_l2(col.nulls + a, b - a);
           }
@@ -975,7 +999,10 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
             if (col.staged)
               bulk_g2s(dst + col.smem_off, col.data + (size_t)row0 * col.width, (uint32_t)p.tile_rows * col.width,
                        &full_bar[s], policy);
-            if (col.nulls_staged)
+            if (col.nulls_staged == 2)
+              bulk_g2s(dst + col.smem_null_off, reinterpret_cast<const uint8_t*>(col.null_bits) + row0 / 8,
+                       (uint32_t)p.tile_rows / 8, &full_bar[s], policy);
+            else if (col.nulls_staged)
               bulk_g2s(dst + col.smem_null_off, col.nulls + row0, (uint32_t)p.tile_rows, &full_bar[s], policy);
           }
         } else if (!COMPACT && p.tma_bytes != 0) {
@@ -995,17 +1022,23 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
               tx += a;
             }
             if (col.nulls_staged) {
-              const uint32_t a = rows & ~15u;
-              for (uint32_t j = a; j < rows; ++j) dst[col.smem_null_off + j] = col.nulls[row0 + j];
+              // packed: the bytes holding the tail's bits (the bitmap is padded past the last row)
+              const uint32_t nb = col.nulls_staged == 2 ? (rows + 7) / 8 : rows, a = nb & ~15u;
+              const uint8_t* nsrc = col.nulls_staged == 2 ? reinterpret_cast<const uint8_t*>(col.null_bits) + row0 / 8
+                                                          : col.nulls + row0;
+              for (uint32_t j = a; j < nb; ++j) dst[col.smem_null_off + j] = nsrc[j];
               tx += a;
             }
           }
           mbar_arrive_expect_tx(&full_bar[s], tx);
           for (int i = 0; i < p.ncols; ++i) {
             const KCol& col = p.cols[i];
-            const uint32_t a = (rows * (uint32_t)col.width) & ~15u, an = rows & ~15u;
+            const uint32_t a = (rows * (uint32_t)col.width) & ~15u;
+            const uint32_t an = (col.nulls_staged == 2 ? (rows + 7) / 8 : rows) & ~15u;
+            const uint8_t* nsrc = col.nulls_staged == 2 ? reinterpret_cast<const uint8_t*>(col.null_bits) + row0 / 8
+                                                        : col.nulls + row0;
             if (col.staged && a) bulk_g2s(dst + col.smem_off, col.data + (size_t)row0 * col.width, a, &full_bar[s], policy);
-            if (col.nulls_staged && an) bulk_g2s(dst + col.smem_null_off, col.nulls + row0, an, &full_bar[s], policy);
+            if (col.nulls_staged && an) bulk_g2s(dst + col.smem_null_off, nsrc, an, &full_bar[s], policy);
           }
         } else {
           mbar_arrive(&full_bar[s]);
@@ -2305,6 +2338,29 @@ __global__ void __launch_bounds__(32) count_gate_kernel(const int64_t* __restric
     out[0] = (int64_t)total;
     out[1] = (int64_t)before;
     out[2] = total <= (unsigned long long)capacity ? 0 : (int64_t)(1ull << 62);
+  }
+}
+
+// packed NULL bitmap of a bool mask (esc_pack_nulls): one word per thread
+__global__ void pack_nulls_kernel(const uint8_t* __restrict__ nulls, int64_t n, int64_t words,
+                                  uint32_t* __restrict__ out) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    const int64_t r0 = w * 32;
+    if (r0 + 32 <= n) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // 4 bytes at a time (the mask is only byte-aligned)
+        const uint32_t x = (uint32_t)nulls[r0 + 4 * q] | ((uint32_t)nulls[r0 + 4 * q + 1] << 8) |
+                           ((uint32_t)nulls[r0 + 4 * q + 2] << 16) | ((uint32_t)nulls[r0 + 4 * q + 3] << 24);
+        const uint32_t nz = ((x & 0x01010101u) | ((x >> 1) & 0x01010101u) | ((x >> 2) & 0x01010101u) |
+                             ((x >> 3) & 0x01010101u) | ((x >> 4) & 0x01010101u) | ((x >> 5) & 0x01010101u) |
+                             ((x >> 6) & 0x01010101u) | ((x >> 7) & 0x01010101u));
+        v |= (((nz * 0x01020408u) >> 24) & 0xFu) << (4 * q);
+      }
+    } else {
+      for (int64_t r = r0; r < n && r < r0 + 32; ++r) v |= (nulls[r] != 0 ? 1u : 0u) << (r - r0);
+    }
+    out[w] = v;
   }
 }
 

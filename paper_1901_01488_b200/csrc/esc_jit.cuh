@@ -168,6 +168,15 @@ constexpr double kExact = 9007199254740992.0;  // 2^53
 
 std::string as_double(const Val& v) { return v.is_int ? "(double)" + v.name : v.name; }
 
+// the staged NULL flag of tile row `lr` of column c (a byte, or a bit of the packed bitmap)
+std::string staged_null_expr(const KCol& c, const std::string& lr) {
+  if (c.nulls_staged == 2)
+    return "((reinterpret_cast<const uint32_t*>(st + " + std::to_string(c.smem_null_off) + "u)[(" + lr + ") >> 5] >> ((" +
+           lr + ") & 31)) & 1u)";
+  return "(st[" + std::to_string(c.smem_null_off) + "u + " + lr + "] != 0)";
+}
+const char* nulls_fn(uint32_t noff) { return (noff & kPackedNulls) ? "null_bits_packed" : "null_bits_staged"; }
+
 // UDFs gen_udf_body turns into straight-line code: arithmetic only (no branches, comparisons
 // or math functions — those run through the interpreter's atom_udf)
 bool straight_line_udf(const KParams& kp, int ui) {
@@ -372,7 +381,7 @@ void gen_capture(const KParams& kp, std::ostringstream& o) {
         << "], rr, 4 * c + j));\n";
     if (kp.sel.cap_nulls[k] != nullptr) {
       if (c.nulls == nullptr) o << "        cn" << k << "[(size_t)r * stride] = 0;\n";
-      else if (c.nulls_staged) o << "        cn" << k << "[(size_t)r * stride] = st[" << c.smem_null_off << "u + lr];\n";
+      else if (c.nulls_staged) o << "        cn" << k << "[(size_t)r * stride] = " << staged_null_expr(c, "lr") << " ? 1 : 0;\n";
       else o << "        cn" << k << "[(size_t)r * stride] = is_null(p.cols[" << slot << "], rr, 4 * c + j) ? 1 : 0;\n";
     }
   }
@@ -418,7 +427,7 @@ bool gen_pred(const KParams& kp, int C, std::ostringstream& o) {
     switch (K.op) {
       case K_FALSE: o << "      r = 0u;\n"; break;
       case K_NOTNULL:
-        if (K.noff != kNoNulls) o << "      r = ~null_bits_staged<C>(st + " << K.noff << "u, l0);\n";
+        if (K.noff != kNoNulls) o << "      r = ~" << nulls_fn(K.noff) << "<C>(st + " << (K.noff & ~kPackedNulls) << "u, l0);\n";
         else o << "      r = 0xFFFFFFFFu;\n";
         break;
       case K_RANGE_S8: case K_RANGE_U8: case K_RANGE_S16: case K_RANGE_U16: case K_RANGE_S32: {
@@ -457,7 +466,7 @@ bool gen_pred(const KParams& kp, int C, std::ostringstream& o) {
         std::string nulls;
         for (int a = 0; a < u.n_args; ++a) {
           const KCol& c = kp.cols[u.arg_col[a]];
-          if (c.nulls != nullptr) nulls += " || st[" + std::to_string(c.smem_null_off) + "u + lr] != 0";
+          if (c.nulls != nullptr) nulls += " || " + staged_null_expr(c, "lr");
         }
         o << "        if (!(false" << nulls << ") && v " << cmp_op(K.cmp) << " " << I << ".lo.f) r |= 1u << bit;\n"
           << "      }\n";
@@ -469,7 +478,7 @@ bool gen_pred(const KParams& kp, int C, std::ostringstream& o) {
     }
     if (K.op <= K_RANGE_F32) {
       if (K.inv) o << "      r = ~r;\n";
-      if (K.noff != kNoNulls) o << "      r &= ~null_bits_staged<C>(st + " << K.noff << "u, l0);\n";
+      if (K.noff != kNoNulls) o << "      r &= ~" << nulls_fn(K.noff) << "<C>(st + " << (K.noff & ~kPackedNulls) << "u, l0);\n";
     }
     if (K.neg) o << "      r = ~r;\n";
     o << "      " << acc << " " << comb_stmt(K.combine) << " r;\n    }\n";

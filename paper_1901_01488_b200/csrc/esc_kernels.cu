@@ -396,7 +396,12 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     const bool want = ((used >> i) & 1ull) || (cols[i].flags & ESC_COL_STAGE);
     c.staged = want && !gather && (reinterpret_cast<uintptr_t>(c.data) % 16 == 0);
     c.nulls_staged = want && !gather && c.nulls != nullptr && (reinterpret_cast<uintptr_t>(c.nulls) % 16 == 0);
-    per_row += (c.staged ? c.width : 0) + (c.nulls_staged ? 1 : 0);
+    // count / selection scans stage a packed bitmap when the column has one: N/8 bytes of NULL
+    // state instead of N (the one-pass compaction keeps bytes: it copies them out as outputs)
+    if (want && !gather && c.nulls != nullptr && outs == nullptr && c.null_bits != nullptr &&
+        reinterpret_cast<uintptr_t>(c.null_bits) % 16 == 0)
+      c.nulls_staged = 2;
+    per_row += (c.staged ? c.width : 0) + (c.nulls_staged == 1 ? 1 : 0);
   }
   // compaction regions (bytes per row of scratch)
   uint32_t scratch_row = 0;
@@ -447,8 +452,8 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
     kp.cols[best].staged = 0;
     per_row -= kp.cols[best].width;
     if (kp.cols[best].nulls_staged) {
+      if (kp.cols[best].nulls_staged == 1) per_row -= 1;
       kp.cols[best].nulls_staged = 0;
-      per_row -= 1;
     }
     fast = false;
   }
@@ -458,7 +463,7 @@ Geometry plan_geometry(KParams& kp, const esc_program_t* prog, const esc_column_
   for (int i = 0; i < ncols; ++i) {
     KCol& c = kp.cols[i];
     if (c.staged) { c.smem_off = off; off += (uint32_t)tile_rows * c.width; }
-    if (c.nulls_staged) { c.smem_null_off = off; off += (uint32_t)tile_rows; }
+    if (c.nulls_staged) { c.smem_null_off = off; off += c.nulls_staged == 2 ? (uint32_t)tile_rows / 8 : (uint32_t)tile_rows; }
   }
   const uint32_t tma_bytes = off;  // what the producer's bulk copies fill per stage
   if (fast) {
@@ -531,6 +536,7 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
     if (cols[i].data == nullptr && nrows > 0) return fail(ESC_ERR_INVALID, "null column data");
     kp.cols[i].data = static_cast<const uint8_t*>(cols[i].data);
     kp.cols[i].nulls = cols[i].nulls;
+    kp.cols[i].null_bits = cols[i].null_bits;
     kp.cols[i].dtype = cols[i].dtype;
     kp.cols[i].width = w;
   }
@@ -577,7 +583,7 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
     KInstr& K = kp.ins[i];
     const KCol& c = kp.cols[K.col];
     K.soff = c.smem_off;
-    K.noff = c.nulls != nullptr ? c.smem_null_off : kNoNulls;
+    K.noff = c.nulls != nullptr ? (c.smem_null_off | (c.nulls_staged == 2 ? kPackedNulls : 0u)) : kNoNulls;
     const KCol& b = kp.cols[K.col_b];
     K.soff_b = b.smem_off;
     K.noff_b = b.nulls != nullptr ? b.smem_null_off : kNoNulls;
@@ -1299,6 +1305,21 @@ int esc_gather(const esc_column_t* col, const int64_t* d_idx, int64_t n, void* o
   return ESC_OK;
 }
 
+int64_t esc_null_bits_words(int64_t n) { return n < 0 ? 0 : ((n + 31) / 32 + 3) / 4 * 4 + 4; }
+
+int esc_pack_nulls(const uint8_t* nulls, int64_t n, uint32_t* out, void* stream) {
+  if (n < 0 || out == nullptr || (n > 0 && nulls == nullptr)) return fail(ESC_ERR_INVALID, "bad pack arguments");
+  const int64_t words = esc_null_bits_words(n);
+  const int sms = sm_count_cached();
+  if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
+  int64_t blocks = (words + 255) / 256;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  ++g_launches;
+  pack_nulls_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(nulls, n, words, out);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ESC_OK : fail(ESC_ERR_CUDA, std::string("pack nulls: ") + cudaGetErrorString(e));
+}
+
 int esc_copy_regions(int32_t n, void* const* dst, const void* const* src, const int64_t* bytes, void* stream) {
   if (n < 0 || n > ESC_MAX_REGIONS) return fail(ESC_ERR_INVALID, "region count out of range");
   if (n == 0) return ESC_OK;
@@ -1411,6 +1432,7 @@ int esc_tile_rows(const esc_program_t* prog, const esc_column_t* cols, int32_t n
   for (int i = 0; i < ncols; ++i) {
     kp.cols[i].data = static_cast<const uint8_t*>(cols[i].data);
     kp.cols[i].nulls = cols[i].nulls;
+    kp.cols[i].null_bits = cols[i].null_bits;
     kp.cols[i].dtype = cols[i].dtype;
     kp.cols[i].width = dtype_width(cols[i].dtype);
   }

@@ -182,7 +182,7 @@ class Column:
     conversion, exactly as in the reference ``executor.py:113-125``).
     """
 
-    __slots__ = ("name", "kind", "values", "nulls", "dictionary", "_zero_mask")
+    __slots__ = ("name", "kind", "values", "nulls", "dictionary", "_zero_mask", "_null_bits")
 
     def __init__(self, name: str, kind: ColumnKind, values, null_mask=None,
                  dictionary: Dictionary | None = None, device=None):
@@ -210,6 +210,29 @@ class Column:
             dictionary = Dictionary()
         self.dictionary = dictionary
         self._zero_mask = None
+        self._null_bits = None
+
+    @property
+    def null_bits(self) -> "torch.Tensor | None":
+        """The NULL mask packed 1 bit per row (row-linear int32 words), built once on the device
+        (``esc_pack_nulls``) and staged by count / selection scans instead of the byte mask:
+        N/8 bytes of NULL state per scan instead of N.  None for a column without NULLs."""
+        if self.nulls is None or not self.values.is_cuda:
+            return None
+        if self._null_bits is None:
+            import ctypes as C
+
+            from . import _native as N
+
+            lib = N.load_library()
+            n = len(self)
+            bits = torch.zeros(max(int(lib.esc_null_bits_words(n)), 4), dtype=torch.int32, device=self.values.device)
+            if n:
+                N.check(lib.esc_pack_nulls(C.c_void_p(self.nulls.data_ptr()), n, C.c_void_p(bits.data_ptr()),
+                                           C.c_void_p(torch.cuda.current_stream(self.values.device).cuda_stream)),
+                        "esc_pack_nulls")
+            self._null_bits = bits
+        return self._null_bits
 
     @classmethod
     def device_column(cls, name: str, kind: ColumnKind, values: torch.Tensor, nulls: torch.Tensor | None,
@@ -223,6 +246,7 @@ class Column:
         c.name, c.kind, c.values, c.nulls = name, kind, values, None
         c.dictionary = Dictionary() if kind.is_text and dictionary is None else dictionary
         c._zero_mask = None
+        c._null_bits = None
         return c
 
     # -- reference-compatible surface ------------------------------------------------------

@@ -417,3 +417,40 @@ def test_ticketed_scan_tails(cuda, n):
     assert count == want.size
     assert np.array_equal(out[0].values.cpu().numpy(), cols["d"][want])
     assert np.array_equal(out[1].values.cpu().numpy(), cols["a"][want])
+
+
+@pytest.mark.parametrize("packed", [True, False])
+@pytest.mark.parametrize("jit", [0, 2])
+def test_packed_and_byte_null_staging(mixed, packed, jit):
+    """Count / selection scans stage nullable columns' NULLs as a packed 1-bit bitmap (default)
+    or as the byte mask: both equal the oracle (NULL floor, two-valued NOT, UDF NULL rows)."""
+    from paper_1901_01488_b200 import _native as N, compiler, count_star, eval_predicate
+
+    arrays, t, ot = mixed
+    prev = compiler.set_packed_nulls(packed)
+    N.set_jit(jit, 0)
+    try:
+        corpus = Corpus(arrays, random.Random(99 + jit + 2 * packed))
+        for _ in range(25):
+            j = corpus.pred()
+            want = _oracle(O.count_star, ot, j, UDFS)
+            assert _device(count_star, t, _pred(j)) == want, j
+            if want[0] == "ok":
+                got = eval_predicate(t, _pred(j)).to_indices().cpu().numpy()
+                assert np.array_equal(got, O.eval_predicate(ot, j, None, UDFS)), j
+    finally:
+        compiler.set_packed_nulls(prev)
+        N.set_jit(1, 1 << 22)
+
+
+def test_packed_null_bitmap_layout(cuda):
+    """esc_pack_nulls: bit r % 32 of word r / 32, zero padding past the last row."""
+    from paper_1901_01488_b200.storage import KIND_INT32, Column
+
+    for n in (1, 31, 32, 33, 1000, 65_537):
+        m = np.random.default_rng(n).random(n) < 0.3
+        m[0] = True
+        c = Column("x", KIND_INT32, np.zeros(n, np.int32), m, device=cuda)
+        words = c.null_bits.cpu().numpy().view(np.uint32)
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")
+        assert np.array_equal(bits[:n].astype(bool), m) and not bits[n:].any()
