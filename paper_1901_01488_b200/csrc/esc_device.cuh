@@ -2128,67 +2128,61 @@ struct StreamParams {
   uint32_t off_val[ESC_MAX_PROJ];
   uint32_t off_null[ESC_MAX_PROJ];
   esc_outputs_t outs;
+  // what the consumers copy, as byte streams grouped by width: streams [cls[c], cls[c+1]) are
+  // 8, 4, 2, 1 bytes wide for c = 0..3 (values and staged null bytes alike), then `n_zero` null
+  // outputs without a source (written 0)
+  int32_t cls[5];
+  int32_t n_zero;
+  int32_t consumers;       // consumer warps (<= kStreamConsumers; the block is 1 + consumers warps)
+  uint32_t s_off[2 * ESC_MAX_PROJ];         // stage offset of the stream's tile
+  const uint8_t* s_src[2 * ESC_MAX_PROJ];   // its column in HBM (the tail tile)
+  uint8_t* s_dst[2 * ESC_MAX_PROJ];         // its output buffer
+  uint8_t* zero_dst[ESC_MAX_PROJ];
 };
 
 constexpr int kStreamConsumers = 16;
 
-// Write the hits of `nw` consecutive bitmap words (<= 4) of one warp segment: every lane owns one
-// row per word; the values of each column are loaded for all words first, then stored, so a lane
-// keeps up to 4 loads in flight.  `src(k, row)`: staged smem (tile-local row) or HBM (global row).
+// Write the hits of up to 4 consecutive bitmap words of one warp segment, for the streams of one
+// width class: lane l of word j owns tile row lr + 32j; bit j of `h` says it writes that row (a hit
+// inside the output capacity) to output base + of[j].  Each stream loads its (up to) 4 values
+// first, then stores them, so a lane keeps 4 loads in flight; the store of a word is contiguous
+// across its hit lanes.  Staged tiles read shared memory, the tail tile the column in HBM.
+template <typename T, bool STAGED>
+__device__ __forceinline__ void stream_class(const StreamParams& p, int k0, int k1, const uint8_t* st,
+                                             int64_t row_base, unsigned long long base, uint32_t h,
+                                             const uint32_t (&of)[4], int lr) {
+  for (int k = k0; k < k1; ++k) {
+    const T* src = STAGED ? reinterpret_cast<const T*>(st + p.s_off[k])
+                          : reinterpret_cast<const T*>(p.s_src[k]) + row_base;
+    T* dst = reinterpret_cast<T*>(p.s_dst[k]) + base;
+    T v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = ((h >> j) & 1u) ? src[lr + 32 * j] : T(0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((h >> j) & 1u) dst[of[j]] = v[j];
+  }
+}
+
 template <bool STAGED>
 __device__ __forceinline__ void stream_words(const StreamParams& p, const uint8_t* st, int64_t row_base,
-                                             const uint32_t (&word)[4], const unsigned long long (&pos)[4],
-                                             int lr0, int lane) {
-  const long long cap = p.outs.capacity;
-  bool hit[4];
-  int lr[4];
+                                             unsigned long long base, uint32_t h, const uint32_t (&of)[4],
+                                             int lr) {
+  stream_class<unsigned long long, STAGED>(p, p.cls[0], p.cls[1], st, row_base, base, h, of, lr);
+  stream_class<uint32_t, STAGED>(p, p.cls[1], p.cls[2], st, row_base, base, h, of, lr);
+  stream_class<uint16_t, STAGED>(p, p.cls[2], p.cls[3], st, row_base, base, h, of, lr);
+  stream_class<uint8_t, STAGED>(p, p.cls[3], p.cls[4], st, row_base, base, h, of, lr);
+  for (int k = 0; k < p.n_zero; ++k) {
+    uint8_t* dst = p.zero_dst[k] + base;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    hit[j] = ((word[j] >> lane) & 1u) && (long long)pos[j] < cap;
-    lr[j] = lr0 + 32 * j + lane;
-  }
-  for (int k = 0; k < p.n_proj; ++k) {
-    const int w = p.width[k];
-    const uint8_t* base = STAGED ? st + p.off_val[k] : p.data[k] + (size_t)row_base * w;
-    void* out = p.outs.out_values[k];
-    if (w == 4) {
-      uint32_t v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? reinterpret_cast<const uint32_t*>(base)[lr[j]] : 0u;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<uint32_t*>(out)[pos[j]] = v[j];
-    } else if (w == 8) {
-      unsigned long long v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? reinterpret_cast<const unsigned long long*>(base)[lr[j]] : 0ull;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<unsigned long long*>(out)[pos[j]] = v[j];
-    } else if (w == 2) {
-      uint16_t v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? reinterpret_cast<const uint16_t*>(base)[lr[j]] : (uint16_t)0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<uint16_t*>(out)[pos[j]] = v[j];
-    } else {
-      uint8_t v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = hit[j] ? base[lr[j]] : (uint8_t)0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<uint8_t*>(out)[pos[j]] = v[j];
-    }
-    uint8_t* on = p.outs.out_nulls[k];
-    if (on != nullptr) {
-      const uint8_t* nb = p.nulls[k] == nullptr ? nullptr : (STAGED ? st + p.off_null[k] : p.nulls[k] + row_base);
-      uint8_t v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = (hit[j] && nb != nullptr) ? nb[lr[j]] : (uint8_t)0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) if (hit[j]) on[pos[j]] = v[j];
-    }
+    for (int j = 0; j < 4; ++j)
+      if ((h >> j) & 1u) dst[of[j]] = 0;
   }
   if (p.outs.out_row_ids != nullptr) {
+    int64_t* ro = p.outs.out_row_ids + base;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) if (hit[j]) p.outs.out_row_ids[pos[j]] = row_base + lr[j];
+    for (int j = 0; j < 4; ++j)
+      if ((h >> j) & 1u) ro[of[j]] = row_base + lr + 32 * j;
   }
 }
 
@@ -2208,7 +2202,7 @@ __global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_ker
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kStreamConsumers);
+      mbar_init(&empty_bar[s], p.consumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -2248,12 +2242,13 @@ __global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_ker
     return;
   }
   const int cw = warp - 1;
-  const int wps = kStreamConsumers / p.segs_per_tile;  // warps per segment (host: <= words per segment)
+  const int wps = p.consumers / p.segs_per_tile;  // warps per segment (host: <= words per segment)
   const int seg = cw / wps;
   const int W = p.seg_rows / 32;
   const int wpart = W / wps;                            // words this warp writes
   const int w0 = (cw % wps) * wpart;
   const uint32_t lt = (1u << lane) - 1u;
+  const long long cap = p.outs.capacity;
   int s = 0;
   uint32_t ph = 0;
   for (;; s = (s + 1 == S) ? 0 : s + 1, ph ^= (s == 0)) {
@@ -2263,31 +2258,29 @@ __global__ void __launch_bounds__((1 + kStreamConsumers) * 32, 1) sel_stream_ker
     const uint8_t* st = ring + (size_t)s * p.stage_bytes;
     const uint32_t* bm = reinterpret_cast<const uint32_t*>(st + p.off_bitmap) + seg * W;
     const unsigned long long base = reinterpret_cast<const unsigned long long*>(st + p.off_offsets)[seg];
-    const uint32_t mine = lane < W ? bm[lane] : 0u;
-    const uint32_t pc = __popc(mine);
-    uint32_t excl = pc;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, excl, d);
-      if (lane >= d) excl += t;
-    }
-    excl -= pc;
+    // hits before this warp's words, and in the whole segment (one reduction each, no scan)
+    const uint32_t pc = lane < W ? __popc(bm[lane]) : 0u;
+    uint32_t pre = __reduce_add_sync(0xFFFFFFFFu, lane < w0 ? pc : 0u);
+    const uint32_t seg_hits = __reduce_add_sync(0xFFFFFFFFu, pc);
+    // outputs [base, base + seg_hits) of this segment; past the capacity nothing is written
+    const bool fits = (long long)(base + seg_hits) <= cap;
+    const long long room_ll = cap - (long long)base;
+    const uint32_t room = room_ll <= 0 ? 0u : (room_ll >= (1ll << 32) ? 0xFFFFFFFFu : (uint32_t)room_ll);
     const bool full = tile < p.n_full_tiles;
     const int64_t row_base = tile * p.tile_rows;
     for (int i0 = w0; i0 < w0 + wpart; i0 += 4) {
-      uint32_t word[4];
-      unsigned long long pos[4];
+      uint32_t of[4], h = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int i = i0 + j;
-        const bool in = i < w0 + wpart;
-        word[j] = __shfl_sync(0xFFFFFFFFu, mine, in ? i : 0);
-        if (!in) word[j] = 0;
-        pos[j] = base + __shfl_sync(0xFFFFFFFFu, excl, in ? i : 0) + __popc(word[j] & lt);
+        const uint32_t word = i0 + j < w0 + wpart ? bm[i0 + j] : 0u;  // broadcast read
+        of[j] = pre + __popc(word & lt);
+        pre += __popc(word);
+        if (((word >> lane) & 1u) && (fits || of[j] < room)) h |= 1u << j;
       }
-      const int lr0 = seg * p.seg_rows + 32 * i0;
-      if (full) stream_words<true>(p, st, row_base, word, pos, lr0, lane);
-      else stream_words<false>(p, st, row_base, word, pos, lr0, lane);
+      if (__ballot_sync(0xFFFFFFFFu, h != 0) == 0) continue;
+      const int lr = seg * p.seg_rows + 32 * i0 + lane;
+      if (full) stream_words<true>(p, st, row_base, base, h, of, lr);
+      else stream_words<false>(p, st, row_base, base, h, of, lr);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);

@@ -744,7 +744,16 @@ bool plan_stream(StreamParams& tp, const SelParams& sp, const esc_column_t* cols
   };
   const int W = tp.seg_rows / 32;
   auto warps_ok = [&](int s) { return kStreamConsumers / s <= W; };  // >= 1 word per consumer warp
-  while (spt > 2 && warps_ok(spt >> 1) && stage_for(spt) * 3 > kSmemBudget) spt >>= 1;
+  // >= 3 stages in the ring, unless at most ~1/3 of the rows can be written (the output capacity
+  // bounds it): then the consumers' fixed cost per tile dominates and twice-larger tiles in two
+  // stages stream faster (600M-row config-5 shape, s = 0.05-0.3: 2.71 -> 2.48 ms; at s = 0.5 the
+  // two stages lose, 3.33 -> 3.64 ms; tools/diag_stream_ab.py)
+  const int min_stages = outs->capacity <= nrows / 3 ? 2 : 3;
+  while (spt > 2 && warps_ok(spt >> 1) && stage_for(spt) * min_stages > kSmemBudget) spt >>= 1;
+  if (const char* e = getenv("ESC_STREAM_SPT")) {  // tuning override (experiments only)
+    const int v = atoi(e);
+    if ((v == 2 || v == 4 || v == 8) && warps_ok(v)) spt = v;
+  }
   if (!warps_ok(spt) || stage_for(spt) * 2 > kSmemBudget) return false;
   (void)per_row;
   tp.segs_per_tile = spt;
@@ -775,9 +784,40 @@ bool plan_stream(StreamParams& tp, const SelParams& sp, const esc_column_t* cols
       tp.tma_bytes += rows;
     }
   }
+  // the consumers' byte streams, grouped by width (8, 4, 2, 1)
+  int ns = 0;
+  for (int c = 0; c < 4; ++c) {
+    tp.cls[c] = ns;
+    const int cw = 8 >> c;
+    for (int k = 0; k < outs->n_proj; ++k) {
+      if (tp.width[k] == cw) {
+        tp.s_off[ns] = tp.off_val[k];
+        tp.s_src[ns] = tp.data[k];
+        tp.s_dst[ns++] = static_cast<uint8_t*>(outs->out_values[k]);
+      }
+      if (cw == 1 && tp.nulls[k] != nullptr) {
+        tp.s_off[ns] = tp.off_null[k];
+        tp.s_src[ns] = tp.nulls[k];
+        tp.s_dst[ns++] = outs->out_nulls[k];
+      }
+    }
+  }
+  tp.cls[4] = ns;
+  tp.n_zero = 0;
+  for (int k = 0; k < outs->n_proj; ++k)
+    if (outs->out_nulls[k] != nullptr && tp.nulls[k] == nullptr) tp.zero_dst[tp.n_zero++] = outs->out_nulls[k];
   tp.stage_bytes = (off + 127u) & ~127u;
   tp.stages = (int)(kSmemBudget / tp.stage_bytes);
   if (tp.stages > kMaxStages) tp.stages = kMaxStages;
+  if (const char* e = getenv("ESC_STREAM_STAGES")) {  // tuning override (experiments only)
+    const int v = atoi(e);
+    if (v >= 2 && v < tp.stages) tp.stages = v;
+  }
+  tp.consumers = kStreamConsumers;
+  if (const char* e = getenv("ESC_STREAM_WARPS")) {  // tuning override (experiments only)
+    const int v = atoi(e);
+    if ((v == 4 || v == 8 || v == 16) && v / spt >= 1 && v / spt <= W) tp.consumers = v;
+  }
   (void)sp;
   return tp.stages >= 2;
 }
@@ -985,7 +1025,7 @@ int issue_mat(const MatLaunch& M, cudaStream_t st) {
     e = launch_pdl(tile_scan_apply, M.segs, kScanThreads, 0, st, M.seg_counts, sp.n_segs,
                    static_cast<const unsigned long long*>(M.partials), M.offsets, sp.rule);
   if (e == cudaSuccess && M.streaming)
-    e = launch_pdl(sel_stream_kernel, M.stream_grid, (1 + kStreamConsumers) * 32, M.stream_smem, st, M.tp);
+    e = launch_pdl(sel_stream_kernel, M.stream_grid, (1 + M.tp.consumers) * 32, M.stream_smem, st, M.tp);
   if (e == cudaSuccess) e = launch_pdl(sel_compact_kernel, M.compact_grid, kSelWarps * 32, 0, st, sp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("selection compaction launch: ") + cudaGetErrorString(e));
