@@ -15,6 +15,8 @@ $N -k regex:esc_scan_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/prof/
     python tools/kprof_count.py > gpurun_out/prof/k1c.log 2>&1
 $N -k regex:sel_stream --launch-skip 2 --launch-count 1 -o gpurun_out/prof/stream_config5_s0.5 \
     python tools/kprof_stream.py 0.5 200000000 > gpurun_out/prof/stream.log 2>&1
+$N -k regex:sel_stream --launch-skip 2 --launch-count 1 -o gpurun_out/prof/stream_config5_s0.1 \
+    python tools/kprof_stream.py 0.1 200000000 > gpurun_out/prof/stream01.log 2>&1
 else
 $N -k regex:join_bits --launch-skip 3 --launch-count 1 -o gpurun_out/prof/join_bits_star python tools/diag_join.py \
     > gpurun_out/prof/join.log 2>&1
@@ -22,8 +24,8 @@ $N -k regex:csv_ --launch-skip 8 --launch-count 4 -o gpurun_out/prof/csv_ingest 
     > gpurun_out/prof/csv.log 2>&1
 $N -k regex:esc_scan_kernel --launch-skip 30 --launch-count 1 -o gpurun_out/prof/k1_config2 python tools/diag_config2.py \
     > gpurun_out/prof/k1c2.log 2>&1
-$N -k regex:sel_compact --launch-skip 10 --launch-count 1 -o gpurun_out/prof/selc_config2 python tools/diag_config2.py \
-    > gpurun_out/prof/selc2.log 2>&1
+$N -k regex:sel_mid --launch-skip 10 --launch-count 1 -o gpurun_out/prof/mid_config2 python tools/diag_config2.py \
+    > gpurun_out/prof/mid2.log 2>&1
 $N -k regex:esc_scan_kernel --launch-skip 60 --launch-count 1 -o gpurun_out/prof/onepass_dim python tools/diag_onepass.py \
     > gpurun_out/prof/op.log 2>&1
 fi
