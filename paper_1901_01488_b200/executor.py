@@ -655,12 +655,18 @@ def _release(ps: PendingStep, ws):
 
 
 def _take_outputs(ps: PendingStep, ws, k: int) -> list[Column]:
-    """The first ``k`` rows of a finished step's outputs as temp columns; small one-pass outputs
-    are handed over as views (their plan is not cached again), others trimmed by one copy."""
+    """The first ``k`` rows of a finished step's outputs as temp columns.  Small one-pass outputs
+    are handed over as views (their plan is not cached again).  A queued step's outputs are lent:
+    the temp columns are views of the plan's buffers, and the plan goes back to the cache only
+    once no view of them is left (:func:`_step_plan` checks), so no trim copy runs on the step.
+    Other outputs are trimmed by one copy."""
     plan = ps.plan
-    if ps.kind == "onepass" and plan.nbytes <= SMALL_OUTPUT_BYTES:
-        return [Column.device_column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
+    if (ps.kind == "onepass" and plan.nbytes <= SMALL_OUTPUT_BYTES) or (ps.kind == "queued" and LEND_OUTPUTS):
+        cols = [Column.device_column(c.name, c.kind, v[:k], m[:k] if m is not None else None, c.dictionary)
                 for c, v, m in zip(ps.proj, plan.out_values, plan.out_nulls)]
+        if ps.kind == "queued":
+            _plan_lend(ws, plan)
+        return cols
     if plan.trim_cache is None:
         plan.trim_cache = {}
     cols = _trim(ps.proj, plan.out_values, plan.out_nulls, k, _stream(ps.table.device), plan.trim_cache)
@@ -708,6 +714,13 @@ def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: 
     plan = ws.scratch.setdefault("plans", {}).pop(key, None)  # checked out until finish_step
     if plan is not None:
         return plan
+    lent = ws.scratch.get("lent")
+    if lent:  # the latest plan whose lent outputs are no longer referenced (its temps were swept);
+        # other free plans of the same key are dropped (their buffers go back to the allocator)
+        free = [q for q in lent if q.key == key and _outputs_free(q)]
+        if free:
+            lent[:] = [q for q in lent if not any(q is f for f in free)]
+            return free[-1]
     n = table.row_count
     _, _, sel = _plan_selection(cp, table, n, [c.name for c in proj], ws)
     slot_of = dict(sel.slot_of)
@@ -749,10 +762,34 @@ def _plan_checkin(ws, plan):
         plans.pop(next(iter(plans)))
 
 
+# queued steps hand their capacity-sized outputs over as views (no trim copy on the step)
+LEND_OUTPUTS = os.environ.get("ESC_LEND_OUTPUTS", "1") != "0"
+LENT_PLANS = 8  # lent plans tracked per stream (older ones are forgotten: their views keep the outputs)
+
+
+def _outputs_free(plan) -> bool:
+    """No tensor besides the plan's own refers to its output buffers (one reference from the
+    plan, one from the temporary storage object of the query)."""
+    for t in (*plan.out_values, *[m for m in plan.out_nulls if m is not None]):
+        if torch._C._storage_Use_Count(t.untyped_storage()._cdata) > 2:
+            return False
+    return True
+
+
+def _plan_lend(ws, plan):
+    """A step's outputs became temp columns (views): the plan is reusable once they are gone."""
+    lent = ws.scratch.setdefault("lent", [])
+    lent.append(plan)
+    if len(lent) > LENT_PLANS:
+        lent.pop(0)
+
+
 def release_step_plans(device: torch.device | None = None):
     """Drop the cached step plans (and their device buffers) of the current stream."""
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    N.workspace(dev, torch.cuda.current_stream(dev)).scratch.pop("plans", None)
+    scratch = N.workspace(dev, torch.cuda.current_stream(dev)).scratch
+    scratch.pop("plans", None)
+    scratch.pop("lent", None)
 
 
 def materialize_onepass(table: ColumnTable, pred: ex.Expr, needed, capacity: int | None = None):

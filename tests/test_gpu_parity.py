@@ -396,6 +396,41 @@ def test_onepass_plan_rebinds_new_outputs(cuda):
     assert len(compile_predicate(t, p).c_plans) == 1  # one prepared launch, rebound each time
 
 
+def test_queued_step_lends_outputs_until_released(cuda):
+    """A queued step's temp columns are views of its plan's output buffers: while an earlier
+    step's columns (or a view derived from them) are alive, later steps write to another plan's
+    buffers; once they are dropped, the plan is reused (no new buffers)."""
+    from paper_1901_01488_b200 import ColumnTable, executor, expr as ex
+    from paper_1901_01488_b200.storage import KIND_INT32, KIND_INT64, Column
+
+    n = 3_000_017
+    g = np.random.default_rng(29)
+    x = g.integers(0, 100_000, n).astype(np.int32)
+    y = g.integers(-(1 << 40), 1 << 40, n).astype(np.int64)
+    t = ColumnTable("t", [Column("x", KIND_INT32, x, device=cuda), Column("y", KIND_INT64, y, device=cuda)])
+    p = ex.Range(ex.ColumnRef("t", "x"), 0, 999)
+    want = np.flatnonzero(x <= 999)
+    cap = n // 5
+    _, first = executor.count_and_materialize(t, p, ["y", "x"], cap)
+    derived = first[0].values[:10]  # a view of a view keeps the buffer lent too
+    ptr0 = first[0].values.data_ptr()
+    del first
+    for _ in range(4):  # the same predicate again (same plan key): must not reuse the lent buffer
+        count, cols = executor.count_and_materialize(t, p, ["y", "x"], cap)
+        assert count == want.size and cols[0].values.data_ptr() != ptr0
+        assert np.array_equal(cols[0].values.cpu().numpy(), y[want])
+        del cols
+    assert np.array_equal(derived.cpu().numpy(), y[want[:10]])
+    del derived
+    ptrs = set()
+    for _ in range(3):  # everything released: steady state reuses the same buffers
+        count, cols = executor.count_and_materialize(t, p, ["y", "x"], cap)
+        ptrs.add(cols[0].values.data_ptr())
+        assert np.array_equal(cols[1].values.cpu().numpy(), x[want])
+        del cols
+    assert len(ptrs) == 1
+
+
 @pytest.mark.parametrize("n", [600 * 8192 + 77, 2 * 148 * 4096 * 2 + 4096 * 3 + 5])
 def test_ticketed_scan_tails(cuda, n):
     """K1 hands out multi-tile tickets on large scans; counts and selections stay exact when the

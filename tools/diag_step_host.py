@@ -55,4 +55,21 @@ for i in range(40):
         for k, v in zip(secs, (b - a, c - b, d - c, e - d, f - e)):
             secs[k].append(v * 1e6)
 print("sharded sections (us):", {k: round(statistics.median(v), 1) for k, v in secs.items()})
+# inside _finish: the pieces it calls (timed by wrapping them)
+import functools
+parts = {}
+def timed(mod, name):
+    f = getattr(mod, name)
+    @functools.wraps(f)
+    def g(*a, **k):
+        t = time.perf_counter(); r = f(*a, **k); parts.setdefault(name, []).append((time.perf_counter() - t) * 1e6); return r
+    setattr(mod, name, g)
+timed(multigpu, "_global_replay"); timed(executor, "_take_outputs"); timed(multigpu, "allreduce_min")
+for i in range(30):
+    it = multigpu._Launched("t", tt, pred, list(w.project), n, True, gcap, min(gcap, tt.row_count))
+    multigpu._launch(it, 1); executor._stream(dev).synchronize()
+    local, counts, cols = multigpu._finish(it)
+    scratch.materialize_temp(cols); scratch.temps.sweep()
+print("finish parts (us):", {k: round(statistics.median(v[10:]), 1) for k, v in parts.items()},
+      "may_fail", it.ps.cp.may_fail, "unbound", it.ps.cp.unbound)
 dist.destroy_process_group()
