@@ -27,6 +27,7 @@ stay sharded in probe order.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass
 from fractions import Fraction
@@ -178,6 +179,15 @@ class _CountExchange:
         hbuf.copy_(dbuf, non_blocking=True)
         self.host = hbuf
 
+    def after(self, plan, stream):
+        """Ungated variant: the step ran as on one GPU (its compaction checked the LOCAL count
+        against the local capacity); the counts are gathered behind it for the host."""
+        sh = self.shard
+        dbuf, hbuf = executor.gate_buffers(plan, plan.sel.table.device, sh.world)
+        _device_all_gather(dbuf[: sh.world], N.workspace(plan.sel.table.device, stream).dcount, sh.group)
+        hbuf.copy_(dbuf, non_blocking=True)
+        self.host = hbuf
+
     def counts(self) -> list[int]:
         return [int(x) for x in self.host[: self.shard.world].tolist()]
 
@@ -197,6 +207,17 @@ class _Launched:
     sync_sel: object = None   # (count, fails, Selection) of the synchronous large-output path
 
 
+# Where the count exchange sits in the sharded step.  Default (ungated): the step runs as on one
+# GPU — scan + compaction in one graph with the PDL overlap, the compaction testing the LOCAL
+# count against the local capacity — and the all_gather of the counts is queued behind it; the
+# host decides on the global count.  A rank whose table does not qualify globally may have
+# compacted for nothing (bounded by its capacity).  Gated (ESC_MG_GATED=1): all_gather +
+# esc_count_gate between the scan and the compaction, which then tests the GLOBAL count; it
+# measured 5 us slower at the 8-GPU shard size on one GPU, and it puts the compaction after
+# the cross-rank exchange (the slowest rank's scan) instead of before it.
+GATED = os.environ.get("ESC_MG_GATED", "0") == "1"
+
+
 def _launch(item: _Launched, slot: int):
     t = item.table
     n = t.row_count
@@ -211,10 +232,13 @@ def _launch(item: _Launched, slot: int):
             item.sync_sel = (count, fails, sel, cp)
             return
         item.exchange = _CountExchange(t.shard, item.gcap)
+    gated = item.exchange is not None and GATED
     item.ps = executor.launch_step(t, item.predicate, item.needed, item.cap, materialize=item.fused, slot=slot,
-                                   between=item.exchange)
+                                   between=item.exchange if gated else None)
     if item.exchange is not None and item.ps.kind != "queued":
         item.exchange = None
+    if item.exchange is not None and not gated:
+        item.exchange.after(item.ps.plan, executor._stream(t.device))
 
 
 def _global_replay(table: ColumnTable, cp, local_fails: list, n_global: int):

@@ -195,8 +195,11 @@ def _run(scenario, world):
     return [res[r] for r in range(world)]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_esc_step_equals_single_gpu(cuda, world):
+@pytest.mark.parametrize("world,gated", [(2, "0"), (3, "0"), (2, "1")])
+def test_sharded_esc_step_equals_single_gpu(cuda, world, gated, monkeypatch):
+    """Both placements of the count exchange (multigpu.GATED): behind the step, or between the
+    scan and the gated compaction."""
+    monkeypatch.setenv("ESC_MG_GATED", gated)  # the spawned ranks read it when they import
     ranks = _run("esc", world)
     for i, first in enumerate(ranks[0]):
         if "errors" in first:
