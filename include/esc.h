@@ -408,9 +408,12 @@ int esc_hash_build_temp_bytes(int64_t n, size_t* bytes);
  * store the group's size there (esc_join_step_t.factor / factor_bits). */
 int esc_factor_array(const int64_t* unique_keys, const int64_t* counts, int64_t u, int64_t lo, int64_t span,
                      int32_t bits, void* out, size_t out_bytes, void* stream);
-/* A star step's (key, factor) pair table for sparse key ranges: pairs = int64[2 * capacity]
- * (16-byte aligned), capacity a power of two > u; factor 0 marks an empty slot; splitmix64 +
- * linear probing as esc_hash_insert.  Probed by esc_join_count in ESC_JOIN_PAIRS mode. */
+/* A star step's (key, factor) pair table for sparse key ranges: pairs = esc_pairs_bytes(capacity)
+ * bytes (16-byte aligned): int64[2 * capacity] (key, factor) slots, then the slots' occupancy
+ * bits (capacity / 8 bytes); capacity a power of two > u; factor 0 marks an empty slot;
+ * splitmix64 + linear probing as esc_hash_insert.  Probed by esc_join_count in ESC_JOIN_PAIRS
+ * mode, which stages the occupancy bits on chip: a key whose home slot is empty is absent. */
+size_t esc_pairs_bytes(int64_t capacity);
 int esc_pairs_build(const int64_t* unique_keys, const int64_t* counts, int64_t u, int64_t* pairs, int64_t capacity,
                     void* stream);
 int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int64_t n, int64_t* out_group_rows,

@@ -166,6 +166,7 @@ _SIGNATURES = {
     "esc_hash_insert": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
     "esc_factor_array": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
                                    C.c_size_t, C.c_void_p]),
+    "esc_pairs_bytes": (C.c_size_t, [C.c_int64]),
     "esc_pairs_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
     "esc_hash_build_temp_bytes": (C.c_int, [C.c_int64, C.POINTER(C.c_size_t)]),
     "esc_hash_build": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -40,9 +40,13 @@ __global__ void hash_insert_kernel(const long long* __restrict__ uk, int64_t n, 
   }
 }
 
+// occ: the table's occupancy bits (staged in shared memory) or nullptr.  A key whose home slot is
+// empty is absent (linear probing), so at load <= 1/4 about three quarters of the non-members
+// are rejected on chip, without the dependent L2 load
 __device__ __forceinline__ unsigned long long pairs_find(const longlong2* __restrict__ pairs, unsigned long long mask,
-                                                         long long k) {
+                                                         long long k, const uint32_t* occ) {
   unsigned long long h = splitmix64((unsigned long long)k) & mask;
+  if (occ != nullptr && !((occ[h >> 5] >> (h & 31)) & 1u)) return 0;
   for (;;) {
     const longlong2 e = __ldg(pairs + h);
     if (e.y == 0) return 0;
@@ -128,6 +132,7 @@ struct JoinStepK {
   unsigned long long mask;
   const long long* uk;
   const unsigned long long* weight[ESC_MAX_STEPS + 1];
+  const uint32_t* occ;    // PAIRS: the table's occupancy bits (capacity / 32 words after the pairs)
 };
 
 constexpr uint32_t kNoSmem = 0xFFFFFFFFu;
@@ -162,11 +167,14 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_count_kernel(const __gri
   // stage the small dense factor arrays (all lookups of the pass then stay on chip)
   for (int t = 0; t < p.n_steps; ++t) {
     const JoinStepK& s = p.steps[t];
-    if (s.mode != ESC_JOIN_DENSE || s.smem_off == kNoSmem) continue;
-    const long long bytes = s.fbits == 1 ? ((s.dlen + 31) / 32) * 4 : s.dlen * (s.fbits / 8);
+    if (s.smem_off == kNoSmem) continue;
+    const bool pairs = s.mode == ESC_JOIN_PAIRS;
+    const long long bytes = pairs ? (long long)((s.mask + 1) / 8)
+                                  : s.fbits == 1 ? ((s.dlen + 31) / 32) * 4 : s.dlen * (s.fbits / 8);
     const long long words = (bytes + 15) / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(pairs ? reinterpret_cast<const uint8_t*>(s.occ) : s.factor);
     for (long long i = threadIdx.x; i < words; i += blockDim.x)
-      reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(reinterpret_cast<const uint4*>(s.factor) + i);
+      reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(src + i);
   }
   __syncthreads();
   // every loop over steps / stages is fully unrolled with compile-time indices, so the per-stage
@@ -198,7 +206,8 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_count_kernel(const __gri
             const long long i = k - s.dmin;
             if (i >= 0 && i < s.dlen) f = factor_at(s.smem_off != kNoSmem ? jsm + s.smem_off : s.factor, s.fbits, i);
           } else if (s.mode == ESC_JOIN_PAIRS) {
-            f = pairs_find(reinterpret_cast<const longlong2*>(s.slots), s.mask, k);
+            f = pairs_find(reinterpret_cast<const longlong2*>(s.slots), s.mask, k,
+                           s.smem_off != kNoSmem ? reinterpret_cast<const uint32_t*>(jsm + s.smem_off) : nullptr);
           } else {
             const long long g = hash_find(s.slots, s.mask, s.uk, k);
             if (g >= 0) f = __ldg(s.weight[t + 1] + g);
@@ -242,6 +251,85 @@ __global__ void __launch_bounds__(kJoinThreads, 2) join_count_kernel(const __gri
   }
   __syncthreads();
   if (threadIdx.x <= p.n_stages) {
+    unsigned long long v = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) v += red[w2][threadIdx.x];
+    if (v) atomicAdd(p.out + threadIdx.x, v);
+  }
+}
+
+// Star over sparse key ranges or wide keys (pair-table, hash or dense steps in any mix): one row
+// per thread.  Every step's key is loaded up front (coalesced, all in flight together), so only
+// the lookups form the dependent chain; a step is looked up only while the row is alive (issuing
+// every step's pair-table lookup at once measured slower: 1.58 vs 1.15 ms, three times the L2
+// lookups).  Pair-table lookups test the on-chip occupancy bits first.
+template <int NS>
+__global__ void __launch_bounds__(kJoinThreads, 2) join_star_kernel(const __grid_constant__ JoinParams p) {
+  extern __shared__ __align__(16) uint8_t jsm[];
+  for (int t = 0; t < NS; ++t) {
+    const JoinStepK& s = p.steps[t];
+    if (s.smem_off == kNoSmem) continue;
+    const bool pairs = s.mode == ESC_JOIN_PAIRS;
+    const long long bytes = pairs ? (long long)((s.mask + 1) / 8)
+                                  : s.fbits == 1 ? ((s.dlen + 31) / 32) * 4 : s.dlen * (s.fbits / 8);
+    const long long words = (bytes + 15) / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(pairs ? reinterpret_cast<const uint8_t*>(s.occ) : s.factor);
+    for (long long i = threadIdx.x; i < words; i += blockDim.x)
+      reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  unsigned long long acc[NS + 1];
+#pragma unroll
+  for (int i = 0; i <= NS; ++i) acc[i] = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwords = (p.nrows + 31) / 32;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = gw; w < nwords; w += nw) {
+    const int64_t row = w * 32 + lane;
+    bool sel = row < p.nrows;
+    if (sel && p.bitmap != nullptr) sel = (__ldg(p.bitmap + w) >> lane) & 1u;
+    if (!sel) continue;
+    acc[0] += 1;
+    long long k[NS];
+    bool ok[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const JoinStepK& s = p.steps[t];
+      ok[t] = s.nulls == nullptr || s.nulls[row] == 0;
+      k[t] = ld_key(s.keys, s.dtype, row);
+    }
+    unsigned long long run = 1;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const JoinStepK& s = p.steps[t];
+      unsigned long long f = 0;
+      if (run != 0 && ok[t]) {
+        if (s.mode == ESC_JOIN_DENSE) {
+          const long long i = k[t] - s.dmin;
+          if (i >= 0 && i < s.dlen) f = factor_at(s.smem_off != kNoSmem ? jsm + s.smem_off : s.factor, s.fbits, i);
+        } else if (s.mode == ESC_JOIN_PAIRS) {
+          f = pairs_find(reinterpret_cast<const longlong2*>(s.slots), s.mask, k[t],
+                         s.smem_off != kNoSmem ? reinterpret_cast<const uint32_t*>(jsm + s.smem_off) : nullptr);
+        } else {
+          const long long g = hash_find(s.slots, s.mask, s.uk, k[t]);
+          f = g >= 0 ? __ldg(s.weight[t + 1] + g) : 0ull;
+        }
+      }
+      run *= f;
+      acc[t + 1] += run;
+    }
+  }
+  __shared__ unsigned long long red[kJoinThreads / 32][NS + 1];
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int st = 0; st <= NS; ++st) {
+    unsigned long long v = acc[st];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+    if (lane == 0) red[warp][st] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x <= NS) {
     unsigned long long v = 0;
     for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) v += red[w2][threadIdx.x];
     if (v) atomicAdd(p.out + threadIdx.x, v);
@@ -681,13 +769,14 @@ __global__ void factor_array_kernel(const long long* __restrict__ unique_keys, c
 
 // (key, factor) pair tables of star steps over sparse key ranges
 __global__ void pairs_insert_kernel(const long long* __restrict__ uk, const long long* __restrict__ counts, int64_t u,
-                                    unsigned long long* pairs, unsigned long long mask) {
+                                    unsigned long long* pairs, unsigned long long mask, uint32_t* occ) {
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < u; g += (int64_t)gridDim.x * blockDim.x) {
     const long long key = uk[g];
     const unsigned long long f = (unsigned long long)counts[g];  // >= 1
     unsigned long long h = splitmix64((unsigned long long)key) & mask;
     while (atomicCAS(pairs + 2 * h + 1, 0ull, f) != 0ull) h = (h + 1) & mask;
     pairs[2 * h] = (unsigned long long)key;
+    atomicOr(occ + (h >> 5), 1u << (h & 31));
   }
 }
 
@@ -740,6 +829,12 @@ int esc_factor_array(const int64_t* unique_keys, const int64_t* counts, int64_t 
   return ESC_OK;
 }
 
+size_t esc_pairs_bytes(int64_t capacity) {
+  if (capacity <= 0) return 0;
+  const size_t occ = ((size_t)capacity / 8 + 15) & ~(size_t)15;
+  return (size_t)capacity * 16 + (occ < 16 ? 16 : occ);
+}
+
 int esc_pairs_build(const int64_t* unique_keys, const int64_t* counts, int64_t u, int64_t* pairs, int64_t capacity,
                     void* stream) {
   if (capacity <= 0 || (capacity & (capacity - 1)) != 0) return fail(ESC_ERR_INVALID, "capacity must be a power of two");
@@ -747,7 +842,8 @@ int esc_pairs_build(const int64_t* unique_keys, const int64_t* counts, int64_t u
   if (pairs == nullptr || (u > 0 && (unique_keys == nullptr || counts == nullptr)))
     return fail(ESC_ERR_INVALID, "null pair table buffers");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(pairs, 0, (size_t)capacity * 16, st);
+  // the pairs, then the occupancy bits (capacity / 8 bytes, at least one 16-byte line)
+  cudaError_t e = cudaMemsetAsync(pairs, 0, esc_pairs_bytes(capacity), st);
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("pair table init: ") + cudaGetErrorString(e));
   if (u == 0) return ESC_OK;
   const int sms = sm_count_cached();
@@ -758,7 +854,8 @@ int esc_pairs_build(const int64_t* unique_keys, const int64_t* counts, int64_t u
   esc::pairs_insert_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const long long*>(unique_keys),
                                                              reinterpret_cast<const long long*>(counts), u,
                                                              reinterpret_cast<unsigned long long*>(pairs),
-                                                             (unsigned long long)capacity - 1);
+                                                             (unsigned long long)capacity - 1,
+                                                             reinterpret_cast<uint32_t*>(pairs + 2 * capacity));
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("pair table launch: ") + cudaGetErrorString(e));
   return ESC_OK;
@@ -975,6 +1072,13 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
         return fail(ESC_ERR_INVALID, "bad pair table");
       k.slots = reinterpret_cast<const long long*>(s.slots);
       k.mask = (unsigned long long)s.capacity - 1;
+      k.occ = reinterpret_cast<const uint32_t*>(s.slots + 2 * s.capacity);
+      const uint32_t need = (uint32_t)((((unsigned long long)s.capacity / 8) + 15) / 16 * 16);
+      static const bool occ_on = [] { const char* e = getenv("ESC_PAIRS_OCC"); return !(e && e[0] == '0'); }();
+      if (occ_on && (long long)s.capacity / 8 <= (long long)smem_cap && smem + need <= smem_cap) {  // occupancy bits on chip
+        k.smem_off = smem;
+        smem += need;
+      }
     } else if (s.mode == ESC_JOIN_HASH) {
       if (s.capacity <= 0 || (s.capacity & (s.capacity - 1)) != 0 || s.slots == nullptr || s.unique_keys == nullptr)
         return fail(ESC_ERR_INVALID, "bad hash table");
@@ -1013,14 +1117,19 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
       nullptr, esc::join_quad_kernel<1>, esc::join_quad_kernel<2>, esc::join_quad_kernel<3>,
       esc::join_quad_kernel<4>, esc::join_quad_kernel<5>, esc::join_quad_kernel<6>, esc::join_quad_kernel<7>,
       esc::join_quad_kernel<8>};
+  static void (*const star_kernels[ESC_MAX_STEPS + 1])(const esc::JoinParams) = {
+      nullptr, esc::join_star_kernel<1>, esc::join_star_kernel<2>, esc::join_star_kernel<3>,
+      esc::join_star_kernel<4>, esc::join_star_kernel<5>, esc::join_star_kernel<6>, esc::join_star_kernel<7>,
+      esc::join_star_kernel<8>};
   static void (*const small_kernels[ESC_MAX_STEPS + 1])(const esc::JoinParams) = {
       nullptr, esc::join_small_kernel<1>, esc::join_small_kernel<2>, esc::join_small_kernel<3>,
       esc::join_small_kernel<4>, esc::join_small_kernel<5>, esc::join_small_kernel<6>, esc::join_small_kernel<7>,
       esc::join_small_kernel<8>};
   if (p.n_steps == 0) p.bits = 0;
   // semi-join bitmaps -> join_bits_kernel; 1/8-bit factors over int32 keys -> join_small_kernel;
-  // any other star -> join_quad_kernel; snowflake (stage-dependent weights) -> join_count_kernel
-  // (hash and pair-table steps: the one-row kernel measured faster — pairs 1.24 vs 1.40 ms)
+  // any other all-dense star -> join_quad_kernel; a star with pair-table or hash steps ->
+  // join_star_kernel (one row per thread, every step's key loaded up front); snowflake
+  // (stage-dependent weights) -> join_count_kernel
   bool quad = !p.bits && p.star && p.n_steps > 0;
   for (int t = 0; t < p.n_steps; ++t)
     if (p.steps[t].mode != ESC_JOIN_DENSE) quad = false;
@@ -1031,12 +1140,18 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
             reinterpret_cast<uintptr_t>(k.keys) % 16 == 0 && k.smem_off != esc::kNoSmem && k.dmin >= INT32_MIN &&
             k.dmin <= INT32_MAX && k.dlen <= INT32_MAX;
   }
-  auto kern = p.bits ? bits_kernels[p.n_steps]
+  const bool star1 = !p.bits && !quad && p.star && p.n_steps > 0;
+  auto kern = p.bits  ? bits_kernels[p.n_steps]
               : small ? small_kernels[p.n_steps]
               : quad  ? quad_kernels[p.n_steps]
+              : star1 ? star_kernels[p.n_steps]
                       : esc::join_count_kernel;
-  static thread_local uint32_t configured[3 * ESC_MAX_STEPS + 3] = {};
-  const int ci = p.bits ? p.n_steps : small ? 2 * (ESC_MAX_STEPS + 1) + p.n_steps : quad ? ESC_MAX_STEPS + 1 + p.n_steps : 0;
+  static thread_local uint32_t configured[4 * ESC_MAX_STEPS + 4] = {};
+  const int ci = p.bits ? p.n_steps
+                 : small ? 2 * (ESC_MAX_STEPS + 1) + p.n_steps
+                 : quad  ? ESC_MAX_STEPS + 1 + p.n_steps
+                 : star1 ? 3 * (ESC_MAX_STEPS + 1) + p.n_steps
+                         : 0;
   if (smem > 48 * 1024 && smem > configured[ci]) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

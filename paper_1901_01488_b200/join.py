@@ -318,7 +318,7 @@ def _count_pipeline(probe: ColumnTable, probe_alias: str, probe_pred, steps: lis
             cap = 16
             while cap < 4 * max(idx.distinct_keys, 1):
                 cap *= 2
-            pairs = torch.empty(2 * cap, dtype=torch.int64, device=probe.device)
+            pairs = torch.empty((int(lib.esc_pairs_bytes(cap)) + 7) // 8, dtype=torch.int64, device=probe.device)
             keep.append(pairs)
             N.check(lib.esc_pairs_build(C.c_void_p(idx.unique_keys.data_ptr()) if idx.distinct_keys else None,
                                         C.c_void_p(idx.group_counts.data_ptr()) if idx.distinct_keys else None,

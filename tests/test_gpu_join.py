@@ -91,25 +91,26 @@ class TestHashIndex:
             assert idx.lookup(k).cpu().tolist() == [i for i, x in enumerate(keys) if x == k]
 
 
-@pytest.mark.parametrize("mode", ["bits", "small", "dense", "hash"])
+@pytest.mark.parametrize("mode", ["bits", "small", "dense", "hash", "mixed"])
 def test_star_count_large_probe(cuda, mode):
     """A 3M-row probe table (a ragged tail of 1 row past a multiple of 4, a probe predicate, NULL
     keys) through four builds — the semi-join bitmap kernel (primary-key dimensions), the
     small-factor kernel (a duplicate-key u8 dimension, int32 keys without NULLs), generic dense
     factors (NULL probe keys) and the hash path for a sparse key range — equals the oracle's stage
-    counts."""
-    dense = mode != "hash"
+    counts.  "mixed": dense int64 steps and pair-table steps in one star (join_star_kernel)."""
+    dense = mode not in ("hash", "mixed")
     from oracle import esc_oracle as O
     from paper_1901_01488_b200 import expr as ex, join
     from paper_1901_01488_b200.storage import KIND_INT32, KIND_INT64, Column, ColumnTable
 
-    g = np.random.default_rng({"bits": 2, "small": 5, "dense": 3, "hash": 4}[mode])
+    g = np.random.default_rng({"bits": 2, "small": 5, "dense": 3, "hash": 4, "mixed": 6}[mode])
     n = 3_000_017
-    mult = 1 if dense else 1_000_003  # spread keys so the key range is too sparse for a direct array
     dims, otabs, steps_o, steps_d, fk = {}, {}, [], [], {}
     probe_cols_o = {}
     probe_cols_d = []
     for s, (nd, dup) in enumerate(((2556, False), (30000, False), (2000, True), (200000, False))):
+        # spread keys so the key range is too sparse for a direct array
+        mult = 1 if dense or (mode == "mixed" and s % 2 == 0) else 1_000_003
         keys = np.arange(1, nd + 1, dtype=np.int64) * mult
         if dup and mode != "bits":
             keys = np.concatenate([keys, keys[::3]])  # duplicate build keys -> factors up to 2
