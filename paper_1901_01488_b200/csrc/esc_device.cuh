@@ -114,6 +114,9 @@ struct KParams {
   int32_t prefetch_l2;        // K1 over a table whose staged bytes fit in L2: every CTA first asks L2 to
                               // prefetch its static share of the full tiles (bulk prefetch), so DRAM
                               // has the whole scan queued from the start instead of ramping with the ring
+  unsigned long long* scan_done;  // select: the last CTA sets it (release) once the count, bitmap and
+                                  // captures are complete: sel_mid_kernel starts on it, not on the grid's
+                                  // completion (griddepcontrol.wait returns ~3 us later), or nullptr
 };
 
 // Programmatic dependent launch: the compaction chain's kernels are launched with
@@ -895,6 +898,7 @@ __device__ __forceinline__ void finish_cta(const KParams& p, unsigned long long 
     __stcg(&h->count, 0ull);
     __stcg(&h->ticket, 0ull);
     __stcg(&h->done, 0ull);
+    if (p.scan_done != nullptr) st_release(p.scan_done, 1ull);  // after the count and the resets
     // no system-scope fence: the host reads the result only after the kernel has completed (a
     // stream/event wait), and kernel completion makes every write visible (the fence cost ~5 us)
     if (p.trace != nullptr) p.trace[blockIdx.x * 8 + 6] = gtimer();
@@ -1853,6 +1857,10 @@ struct MidParams {
   unsigned long long* ticket;    // block tickets (cleared by the last block)
   unsigned long long* done;      // blocks past their prefix read (cleared by the last block)
   unsigned long long* trace;     // diagnostics (esc_debug_trace): 8 %globaltimer stamps per block, or nullptr
+  // early start: the scan of the same step sets this word when its last CTA has published the
+  // count (release); the blocks poll it instead of waiting for the scan grid's completion
+  // (griddepcontrol.wait), and the last block clears it
+  unsigned long long* scan_done;  // nullptr: wait for the scan's completion (PDL)
 };
 
 // one thread's share of a batch round: entries e0 + j*256 (j < kMidJ), projections k0 .. k0+3
@@ -1952,14 +1960,38 @@ __global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_co
   __shared__ unsigned long long s_red[kMidThreads / 32];
   __shared__ unsigned long long s_scan[33];
   __shared__ long long s_block;
+  __shared__ bool s_last;
   extern __shared__ uint32_t s_cnt[];  // [segs_per_block]: counts, then exclusive offsets in the block
   const unsigned long long t_start = m.trace != nullptr ? gtimer() : 0ull;
-  pdl_wait();
-  pdl_trigger();
-  if (skip_materialize(p.rule)) return;
+  const bool early = m.scan_done != nullptr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_block = (long long)atomicAdd(m.ticket, 1ull);
-  __syncthreads();
+  if (early) {
+    // the ticket is taken while the flag is polled; thread 0's acquire + the barrier order every
+    // thread's later loads after the scan's last writes.  (Bounded: a compaction issued without
+    // its scan would otherwise never return; after 0.5 s it reads what an earlier, completed
+    // scan left, which is then the whole truth.)
+    if (threadIdx.x == 0) {
+      s_block = (long long)atomicAdd(m.ticket, 1ull);
+      const unsigned long long t_wait = gtimer();
+      while (ld_acquire(m.scan_done) == 0ull && gtimer() - t_wait < 500000000ull) __nanosleep(64);
+    }
+    __syncthreads();
+    pdl_trigger();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+    if (skip_materialize(p.rule)) return;
+    if (threadIdx.x == 0) s_block = (long long)atomicAdd(m.ticket, 1ull);
+    __syncthreads();
+  }
+  if (early && skip_materialize(p.rule)) {  // (the count is final here) every block still settles
+    if (threadIdx.x == 0 && atomicAdd(m.done, 1ull) == (unsigned long long)m.n_blocks - 1) {
+      __stcg(m.ticket, 0ull);
+      __stcg(m.done, 0ull);
+      __stcg(m.scan_done, 0ull);
+    }
+    return;
+  }
   const int64_t b = s_block;
   unsigned long long* tr = (m.trace != nullptr && threadIdx.x == 0) ? m.trace + 8 * 1024 + b * 8 : nullptr;
   if (tr) { tr[0] = t_start; tr[1] = gtimer(); }
@@ -2026,6 +2058,7 @@ __global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_co
         const uint32_t word = pre ? (q == 0 ? wpre[0] : q == 1 ? wpre[1] : q == 2 ? wpre[2] : wpre[3])
                                   : (lane < W ? __ldcg(p.bitmap + seg * W + lane) : 0u);
         const uint32_t pc = __popc(word);
+        if (tr && si == 0 && sb == 0) tr[7] = gtimer() + (pc & 0);  // (diagnostic: first word in hand)
         uint32_t incl = pc;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -2083,11 +2116,17 @@ __global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_co
           have_base = true;
           if (threadIdx.x == 0) {
             if (tr) tr[5] = gtimer();
-            // the last block past its base read resets the table for the next launch
-            if (atomicAdd(m.done, 1ull) == (unsigned long long)m.n_blocks - 1) {
-              for (int64_t q = 0; q < m.n_blocks; ++q) __stcg(m.agg + q, 0ull);
+            // the last block past its base read resets the table for the next launch (all its
+            // threads: one thread clearing ~600 words serially made it the step's last block)
+            s_last = atomicAdd(m.done, 1ull) == (unsigned long long)m.n_blocks - 1;
+          }
+          __syncthreads();
+          if (s_last) {
+            for (int64_t q = threadIdx.x; q < m.n_blocks; q += kMidThreads) __stcg(m.agg + q, 0ull);
+            if (threadIdx.x == 0) {
               __stcg(m.ticket, 0ull);
               __stcg(m.done, 0ull);
+              if (early) __stcg(m.scan_done, 0ull);
             }
           }
         }

@@ -147,8 +147,9 @@ WsLayout ws_layout(int64_t nrows) {
   L.bitmap_words = ((nrows + t_max - 1) / t_max + 1) * (t_max / 32);  // covers every C's last tile
   const int64_t segs = L.max_tiles / kScanSeg + 2;
   auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  L.mid = sizeof(WsHeader);  // sel_mid_kernel block sums: a FIXED place (every launch size sees the same
-                             // words, which its last block leaves zero)
+  // [header][one line: sel_mid_kernel's early-start flag, away from the header's atomics]
+  L.mid = sizeof(WsHeader) + 128;  // sel_mid_kernel block sums: a FIXED place (every launch size sees the
+                                   // same words, which its last block leaves zero)
   L.offsets = up(L.mid + kMidMaxBlocks * sizeof(unsigned long long));
   L.partials = up(L.offsets + (size_t)L.max_tiles * 8);
   L.counts = up(L.partials + (size_t)segs * 8);
@@ -564,7 +565,13 @@ int build_params(KParams& kp, const esc_program_t* prog, const esc_column_t* col
     const int64_t per = g.tma_bytes > 0 ? g.tma_bytes : (int64_t)g.tile_rows * 4;
     int64_t kb = (131072 + per - 1) / per;
     const int sms = sm_count_cached() > 0 ? sm_count_cached() : 148;
-    const int64_t spread = kp.n_tiles / (2 * (int64_t)sms);  // small scans keep one tile per ticket
+    // small and mid scans keep one tile per ticket: >= ~8 tickets per CTA, so the last wave of
+    // tickets is short (config 2, 732 tiles: 2-tile tickets left CTAs ending 4 or 6 tiles deep)
+    int64_t spread = kp.n_tiles / (8 * (int64_t)sms);
+    if (const char* e = getenv("ESC_TICKET_SPREAD")) {  // tuning override (experiments only)
+      const int v = atoi(e);
+      if (v > 0) spread = kp.n_tiles / ((int64_t)v * sms);
+    }
     if (kb > spread) kb = spread;
     kp.ticket_tiles = (int32_t)(kb < 1 ? 1 : (kb > 8 ? 8 : kb));
     // tables whose staged bytes fit comfortably in L2: prefetch them all up front (DRAM ramp)
@@ -698,6 +705,11 @@ std::atomic<int> g_stream_div{[] {
 // selections over at most this many rows compact with ONE sel_mid_kernel launch (ESC_MID_MAX_ROWS;
 // 0 turns it off): below it the chain's launch + ramp costs dominate, above it the streamed
 // (TMA) compaction of dense tiles reads less than per-hit gathers
+// early start of the mid-size compaction on the scan's completion flag (ESC_MID_EARLY=0: PDL wait)
+std::atomic<int> g_mid_early{[] {
+  const char* e = getenv("ESC_MID_EARLY");
+  return e ? atoi(e) : 1;
+}()};
 std::atomic<long long> g_mid_max_rows{[] {
   const char* e = getenv("ESC_MID_MAX_ROWS");
   return e ? atoll(e) : (32ll << 20);
@@ -1102,6 +1114,7 @@ struct StepPlanImpl {
   ScanLaunch scan;
   MatLaunch mat;
   bool onepass = false;  // one launch of the look-back kernel (no selection, no queued compaction)
+  bool scan_pending = false;  // part 1 issued, its part 2 not yet (early-start compactions)
   // queued plans: the launches of parts 1, 2 and 3 captured once into CUDA graphs (their
   // parameters never change), so a re-issue is one graph launch instead of up to five kernel
   // launches with kilobytes of parameters each
@@ -1209,6 +1222,13 @@ int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, in
     delete plan;
     return rc;
   }
+  // a mid-size compaction in the same plan as its scan starts on the scan's completion flag (set
+  // by its last CTA) instead of the grid's completion
+  if (plan->mat.mid && !plan->mat.empty && g_mid_early.load()) {
+    auto* flag = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(d_ws) + sizeof(WsHeader));
+    plan->kp.scan_done = flag;
+    plan->mat.mp.scan_done = flag;
+  }
   *out_plan = plan;
   return ESC_OK;
 }
@@ -1224,6 +1244,10 @@ int esc_step_plan_launch(void* plan, int32_t parts, void* stream) {
   if (p->onepass) {
     const int rc = next_epoch(p->kp, p->kp.nrows, p->kp.hdr, st);
     return rc != ESC_OK ? rc : issue_scan(p->scan, p->kp, st);
+  }
+  if (p->mat.mp.scan_done != nullptr) {  // an early-start compaction follows its own scan only
+    if (parts == 2 && !p->scan_pending) return fail(ESC_ERR_INVALID, "compaction part issued without its scan");
+    p->scan_pending = parts == 1;
   }
   // graphs for whole steps, or for a part when asked (ESC_PLAN_GRAPH): the profiling split
   // (parts 1 / 2 with events between) launches directly — as two graphs it measured 30-40 us

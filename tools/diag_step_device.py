@@ -17,7 +17,11 @@ p2 = serde.from_json(w2.pred, "lineitem")
 cap = int(0.2 * t2.row_count)
 
 
-def measure(label, parts=None, reps=15, clean=False):
+REPS = int(os.environ.get("REPS", "15"))
+
+
+def measure(label, parts=None, reps=None, clean=False):
+    reps = reps or REPS
     for _ in range(3):
         ps = executor.launch_step(t2, p2, w2.project, cap)
         torch.cuda.synchronize(); executor.finish_step(ps)
@@ -32,7 +36,7 @@ def measure(label, parts=None, reps=15, clean=False):
         torch.cuda.synchronize()
         executor.finish_step(ps)
         ts.append(e0.elapsed_time(e1) * 1e3)
-    print(f"{label:28s} device step {statistics.median(ts):6.1f} us  (min {min(ts):6.1f})")
+    print(f"{label:28s} device step {statistics.median(ts):6.1f} us  (min {min(ts):6.1f}, mean {statistics.mean(ts):6.2f})")
 
 
 measure("default")

@@ -35,3 +35,12 @@ def show(name, a, names):
         if len(v): print(f"  {nm:15s} min {v.min():7.1f}  med {np.median(v):7.1f}  max {v.max():7.1f} us")
 show("K1", k1, ["start", "first tile", "consumers done", "producer done", "cta finished", "last: final begin", "last: final end"])
 show("mid", mid, ["start", "ticket", "published", "offsets", "expanded", "base read", "end"])
+# the slowest mid blocks (block id = ticket order) with their phase stamps
+rel = (mid - t0) / 1e3
+order = np.argsort(-rel[:, 6])[:6]
+blocks = (np.nonzero(st[1024:, 1] > 0)[0])[order]
+v = rel[:, 7][mid[:, 7] > 0]
+if len(v): print(f"  first word     min {v.min():7.1f}  med {np.median(v):7.1f}  max {v.max():7.1f} us")
+print("slowest mid blocks (ticket, start, ticket, published, offsets, expanded, base read, end):")
+for b, r in zip(blocks, rel[order]):
+    print(f"  {b:5d} " + " ".join(f"{x:6.1f}" for x in r[:7]))
