@@ -721,6 +721,11 @@ __device__ __forceinline__ uint32_t valid_bits(int64_t grow0, int64_t nrows, int
 // ------------------------------------------------------------------------------------------
 // Relaxed loads suffice: the status word itself is the only datum read, and it carries its own
 // epoch/flag/value; relaxed (unlike acquire) loads of the window pipeline.
+// ... and the matching relaxed store: a status word publishes only its own value (no other data
+// hangs on it), so no release fence is needed before it
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

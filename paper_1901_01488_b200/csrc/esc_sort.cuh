@@ -80,13 +80,13 @@ __device__ __forceinline__ unsigned long long sort_lookback(const unsigned long 
 }
 
 template <typename K, bool VALS>
-__global__ void __launch_bounds__(kSortThreads) sort_pass_kernel(const __grid_constant__ SortPass p) {
+__global__ void __launch_bounds__(kSortThreads, sizeof(K) == 8 && VALS ? 3 : 4) sort_pass_kernel(const __grid_constant__ SortPass p) {
   __shared__ uint32_t s_wcnt[kSortThreads / 32][256];  // per-warp digit counters, then warp bases
   __shared__ uint32_t s_local[256];                     // tile-local exclusive offset of each digit
   __shared__ unsigned long long s_gbase[256];           // global destination of each digit's first element
   __shared__ unsigned long long s_scan[33];
-  __shared__ K s_keys[kSortTile];
-  __shared__ unsigned long long s_vals[VALS ? kSortTile : 1];
+  __shared__ K s_keys[kSortTile];                       // keys in sorted (digit) order
+  __shared__ unsigned long long s_vals[VALS ? kSortTile : 1];  // their values
   __shared__ long long s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = (long long)atomicAdd(p.ticket, 1ull);
@@ -129,19 +129,14 @@ __global__ void __launch_bounds__(kSortThreads) sort_pass_kernel(const __grid_co
     tot += c;
   }
   unsigned long long* st = p.status + t * 256;
-  st_release(st + d, p.tag | ((t == 0 ? kSortPre : kSortAgg) << 46) | tot);
+  st_relaxed(st + d, p.tag | ((t == 0 ? kSortPre : kSortAgg) << 46) | tot);
   unsigned long long tile_n;
   const unsigned long long loc = block_excl_scan(tot, s_scan, &tile_n);
   s_local[d] = (uint32_t)loc;
   unsigned long long g_all;
-  const unsigned long long gd = block_excl_scan(p.hist[d], s_scan, &g_all);
-  unsigned long long excl = 0;
-  if (t > 0) {
-    excl = sort_lookback(p.status, t, 256, d, p.tag);
-    st_release(st + d, p.tag | (kSortPre << 46) | (excl + tot));
-  }
-  s_gbase[d] = gd + excl;
-  __syncthreads();
+  const unsigned long long gd = block_excl_scan(p.hist[d], s_scan, &g_all);  // (its barriers publish s_local)
+  // the tile-local sort into shared memory BEFORE the look-back: the keys' and values' registers
+  // are free while the digit threads wait on their predecessors (no spills at 3-4 blocks per SM)
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     if (dig[j] < 256) {
@@ -150,6 +145,12 @@ __global__ void __launch_bounds__(kSortThreads) sort_pass_kernel(const __grid_co
       if (VALS) s_vals[pos] = val[j];
     }
   }
+  unsigned long long excl = 0;
+  if (t > 0) {
+    excl = sort_lookback(p.status, t, 256, d, p.tag);
+    st_relaxed(st + d, p.tag | (kSortPre << 46) | (excl + tot));
+  }
+  s_gbase[d] = gd + excl;
   __syncthreads();
   K* kout = static_cast<K*>(p.keys_out);
   for (int i = threadIdx.x; i < (int)tile_n; i += kSortThreads) {  // runs of one digit: coalesced
