@@ -212,11 +212,11 @@ __global__ void __launch_bounds__(kSortThreads) runs_kernel(const __grid_constan
   unsigned long long tile_runs;
   const unsigned long long ex = block_excl_scan((unsigned long long)nf, s_scan, &tile_runs);
   if (threadIdx.x == 0) {
-    st_release(p.status + t, p.tag | ((t == 0 ? kSortPre : kSortAgg) << 46) | tile_runs);
+    st_relaxed(p.status + t, p.tag | ((t == 0 ? kSortPre : kSortAgg) << 46) | tile_runs);
     unsigned long long b = 0;
     if (t > 0) {
       b = sort_lookback(p.status, t, 1, 0, p.tag);
-      st_release(p.status + t, p.tag | (kSortPre << 46) | (b + tile_runs));
+      st_relaxed(p.status + t, p.tag | (kSortPre << 46) | (b + tile_runs));
     }
     s_base = b;
     const int64_t last = (p.n - 1) / kSortTile;
