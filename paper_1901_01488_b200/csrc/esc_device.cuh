@@ -180,6 +180,11 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// a status word that publishes only its own value (no other data hangs on it) needs no release
+// fence before it: look-back readers take the value and nothing else
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -721,11 +726,6 @@ __device__ __forceinline__ uint32_t valid_bits(int64_t grow0, int64_t nrows, int
 // ------------------------------------------------------------------------------------------
 // Relaxed loads suffice: the status word itself is the only datum read, and it carries its own
 // epoch/flag/value; relaxed (unlike acquire) loads of the window pipeline.
-// ... and the matching relaxed store: a status word publishes only its own value (no other data
-// hangs on it), so no release fence is needed before it
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -770,7 +770,7 @@ __device__ unsigned long long lookback_warp(unsigned long long* status, int64_t 
     if (done) break;
     q -= 32 * consumed;
   }
-  if (lane == 0) st_release(&status[tile], tag | (kFlagPrefix << kStatusValueBits) | (excl + agg));
+  if (lane == 0) st_relaxed(&status[tile], tag | (kFlagPrefix << kStatusValueBits) | (excl + agg));
   return excl;
 }
 
@@ -1294,7 +1294,7 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
           s_tsum[s] = 0;
           const unsigned long long tag = (unsigned long long)p.epoch << 48;
           const unsigned long long flag = tile == 0 ? kFlagPrefix : kFlagAggregate;
-          st_release(&p.status[tile], tag | (flag << kStatusValueBits) | (now & 0xFFFFFu));
+          st_relaxed(&p.status[tile], tag | (flag << kStatusValueBits) | (now & 0xFFFFFu));
         }
         mbar_arrive(&agg_bar[s]);
       }
@@ -2021,7 +2021,7 @@ __global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_co
   }
   const unsigned long long block_sum = mid_block_sum(mine, s_red);
   if (threadIdx.x == 0) {
-    st_release(m.agg + b, block_sum + 1);
+    st_relaxed(m.agg + b, block_sum + 1);  // (the value is the only datum: no release fence)
     if (tr) tr[2] = gtimer();
   }
   // exclusive offsets of the block's segments (in place; chunks of 256 with a running carry;
