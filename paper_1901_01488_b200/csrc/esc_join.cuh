@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_bits_kerne
     const long long words = (((s.dlen + 31) / 32) * 4 + 15) / 16;
     for (long long i = threadIdx.x; i < words; i += blockDim.x)
       reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(reinterpret_cast<const uint4*>(s.factor) + i);
+    if (threadIdx.x == 0) reinterpret_cast<uint4*>(jsm + s.smem_off)[words] = make_uint4(0u, 0u, 0u, 0u);
   }
   __syncthreads();
   uint32_t acc[ESC_MAX_STEPS + 1];
@@ -411,8 +412,10 @@ __global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_bits_kerne
         uint32_t hit = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t i = (uint32_t)kv[j] - (uint32_t)kmin[t];  // wraps below min: out of span
-          if (((m >> j) & 1u) && i < klen[t]) hit |= ((bmap[t][i >> 5] >> (i & 31)) & 1u) << j;
+          // out of span (a key below min wraps) -> bit klen, a zero bit of the padding; rows
+          // outside m are masked below, so no per-row predicate
+          const uint32_t i = min((uint32_t)kv[j] - (uint32_t)kmin[t], klen[t]);
+          hit |= ((bmap[t][i >> 5] >> (i & 31)) & 1u) << j;
         }
         m &= hit;
         acc[t + 1] += __popc(m);
@@ -478,6 +481,7 @@ __global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_small_kern
     const long long words = (bytes + 15) / 16;
     for (long long i = threadIdx.x; i < words; i += blockDim.x)
       reinterpret_cast<uint4*>(jsm + s.smem_off)[i] = __ldg(reinterpret_cast<const uint4*>(s.factor) + i);
+    if (threadIdx.x == 0) reinterpret_cast<uint4*>(jsm + s.smem_off)[words] = make_uint4(0u, 0u, 0u, 0u);
   }
   __syncthreads();
   unsigned long long acc[ESC_MAX_STEPS + 1];
@@ -516,10 +520,10 @@ __global__ void __launch_bounds__(kJoinThreads, NS <= 4 ? 2 : 1) join_small_kern
         const int kv[4] = {k[t].x, k[t].y, k[t].z, k[t].w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t i = (uint32_t)kv[j] - (uint32_t)kmin[t];  // wraps below min: out of span
-          uint32_t f = 0;
-          if (run[j] != 0 && i < klen[t])
-            f = one_bit[t] ? (reinterpret_cast<const uint32_t*>(fac[t])[i >> 5] >> (i & 31)) & 1u : fac[t][i];
+          // out of span (a key below min wraps) -> entry klen, a zero of the padding line; a dead
+          // row's product stays 0, so no per-row predicate
+          const uint32_t i = min((uint32_t)kv[j] - (uint32_t)kmin[t], klen[t]);
+          const uint32_t f = one_bit[t] ? (reinterpret_cast<const uint32_t*>(fac[t])[i >> 5] >> (i & 31)) & 1u : fac[t][i];
           run[j] *= f;
         }
         acc[t + 1] += run[0] + run[1] + run[2] + run[3];
@@ -1060,7 +1064,9 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream) 
       k.factor = static_cast<const uint8_t*>(s.factor);
       k.fbits = s.factor_bits;
       const long long bytes = s.factor_bits == 1 ? ((s.dense_len + 31) / 32) * 4 : s.dense_len * (s.factor_bits / 8);
-      const uint32_t need = (uint32_t)((bytes + 15) / 16 * 16);
+      // (one zero line after the array: join_bits_kernel / join_small_kernel clamp an out-of-span
+      // key to entry dense_len, which must read 0)
+      const uint32_t need = (uint32_t)((bytes + 15) / 16 * 16) + 16u;
       if (bytes <= (long long)smem_cap && smem + need <= smem_cap) {
         k.smem_off = smem;
         smem += need;
