@@ -2005,12 +2005,15 @@ __global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_co
   const int nseg = (int)((seg0 + SPB <= p.n_segs) ? SPB : (p.n_segs > seg0 ? p.n_segs - seg0 : 0));
   const int W = p.seg_rows / 32;
   // the bitmap words of this warp's first four segments are loaded with the counts (the
-  // expansion of the first batch then needs no further round trip)
+  // expansion of the first batch then needs no further round trip) — unless captured segments
+  // need no bitmap at all (every projection captured, no row ids): then only the (rare)
+  // uncaptured segments read theirs
+  const bool cap_only = !p.need_bitmap_captured;
   uint32_t wpre[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int si = warp + q * (kMidThreads / 32);
-    wpre[q] = (si < nseg && lane < W) ? __ldcg(p.bitmap + (seg0 + si) * W + lane) : 0u;
+    wpre[q] = (!cap_only && si < nseg && lane < W) ? __ldcg(p.bitmap + (seg0 + si) * W + lane) : 0u;
   }
   // 1. this block's segment counts; their sum is published at once
   unsigned long long mine = 0;
@@ -2059,7 +2062,15 @@ __global__ void __launch_bounds__(kMidThreads, 4) sel_mid_kernel(const __grid_co
         if (off_of(si + 1) == o) continue;  // empty segment
         const bool captured = (s_cnt[si] & ESC_SEG_CAPTURED) != 0;
         const int64_t seg = seg0 + si;
-        const bool pre = sb == 0 && q < 4;
+        if (captured && cap_only) {  // the hits' values sit in the capture slots, in row order
+          const uint32_t cnt = off_of(si + 1) - o;
+          for (uint32_t jj = lane; jj < cnt; jj += 32) {
+            l_row[o - first + jj] = 0u;  // (unused: no gather, no row id)
+            l_slot[o - first + jj] = (uint32_t)((size_t)jj * p.cap_stride + seg);
+          }
+          continue;
+        }
+        const bool pre = !cap_only && sb == 0 && q < 4;
         const uint32_t word = pre ? (q == 0 ? wpre[0] : q == 1 ? wpre[1] : q == 2 ? wpre[2] : wpre[3])
                                   : (lane < W ? __ldcg(p.bitmap + seg * W + lane) : 0u);
         const uint32_t pc = __popc(word);

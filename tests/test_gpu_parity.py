@@ -342,6 +342,13 @@ def test_stream_selectivity_sweep(cuda, stream_mode):
         assert np.array_equal(hv, np.where(hn, 0, h)[want])
         got = eval_predicate(t, p).to_indices().cpu().numpy()
         assert np.array_equal(got, want)
+        # only predicate columns projected: sparse segments' values all come from the capture
+        # slots (the mid kernel then reads no bitmap for them)
+        p2 = ex.And((p, ex.Range(ex.ColumnRef("t", "z"), -90, 99)))
+        want2 = np.flatnonzero((x <= hi) & (z >= -90))
+        cz2, cx2 = materialize(t, p2, ["z", "x"])
+        assert np.array_equal(cx2.values.cpu().numpy(), x[want2])
+        assert np.array_equal(cz2.values.cpu().numpy(), z[want2])
 
 
 def test_queued_compaction_checks_count_on_device(cuda):
