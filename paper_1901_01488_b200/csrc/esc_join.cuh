@@ -888,7 +888,9 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
   if (n > 0 && temp_bytes < T.total) return fail(ESC_ERR_WORKSPACE, "hash build temp too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* t = static_cast<uint8_t*>(d_temp);
-  const bool small_path = dtype_width(key_dtype) <= 4 && n > 0 && n <= (int64_t)esc::kBuildSmallThreads * 16;
+  // one block up to 8K rows: a 16K-row one-block sort (16 items per thread) took 148 us on config
+  // 3's part build, the device-wide sort ~40 (query 1.04 -> 0.94 ms; tools/diag_query3.py)
+  const bool small_path = dtype_width(key_dtype) <= 4 && n > 0 && n <= (int64_t)esc::kBuildSmallThreads * 8;
   cudaError_t e = cudaSuccess;
   if (n == 0) e = cudaMemsetAsync(out_stats, 0, 4 * sizeof(int64_t), st);
   if (e == cudaSuccess && n == 0) e = cudaMemsetAsync(out_group_start, 0, sizeof(int64_t), st);
@@ -916,8 +918,7 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
                                                      reinterpret_cast<long long*>(out_group_start), out_stats);
       return cudaGetLastError();
     };
-    e = n <= (int64_t)esc::kBuildSmallThreads * 8 ? run(esc::build_small_kernel<8>, esc::BuildSmall<8>::kSmem, 1)
-                                                   : run(esc::build_small_kernel<16>, esc::BuildSmall<16>::kSmem, 2);
+    e = run(esc::build_small_kernel<8>, esc::BuildSmall<8>::kSmem, 1);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("small hash build: ") + cudaGetErrorString(e));
     return ESC_OK;
   }

@@ -230,7 +230,7 @@ def test_build_indexes_batch_equals_single_builds(cuda):
 
     g = np.random.default_rng(41)
     specs = []
-    # sizes on both sides of the one-block path (<= 16384 rows with keys of <= 4 bytes)
+    # sizes on both sides of the one-block path (<= 8192 rows with keys of <= 4 bytes)
     for i, (kind, dt, lo, hi, n) in enumerate((("INT8", np.int8, -100, 100, 5000), ("INT16", np.int16, -3000, 3000, 9000),
                                                ("INT32", np.int32, -10**6, 10**6, 16384),
                                                ("INT32", np.int32, -2**31, 2**31 - 1, 50_021),

@@ -148,7 +148,8 @@ def test_large_hash_build_grouping(cuda, dtype):
 
 @pytest.mark.parametrize("dtype", ["uint8", "uint16", "uint32", "int8", "int16", "int32"])
 def test_one_block_hash_build_matches_numpy(cuda, dtype):
-    """The one-block build (<= 16K rows, keys <= 4 bytes) against numpy's unique + stable argsort,
+    """The one-block build (<= 8K rows, keys <= 4 bytes; larger ones take the device-wide sort)
+    against numpy's unique + stable argsort,
     for unsigned keys (bias 0) and keys equal to the 32-bit padding sentinel (0xFFFFFFFF after
     the bias: INT32_MAX, UINT32_MAX), with duplicates and a row subset."""
     from paper_1901_01488_b200 import join
@@ -157,7 +158,7 @@ def test_one_block_hash_build_matches_numpy(cuda, dtype):
     np_dt = np.dtype(dtype)
     info = np.iinfo(np_dt)
     g = np.random.default_rng(5)
-    for n in (1, 100, 8192, 16_384):
+    for n in (1, 100, 8192, 8193, 16_384):
         keys = g.integers(int(info.min), int(info.max) + 1, n, dtype=np.int64).astype(np_dt)
         keys[: min(n, 3)] = info.max  # the sentinel after biasing, and duplicates of it
         if n > 10:
