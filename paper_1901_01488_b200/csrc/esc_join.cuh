@@ -680,10 +680,12 @@ struct BuildSmall {
   using Sort = cub::BlockRadixSort<uint32_t, kBuildSmallThreads, ITEMS, int64_t>;
   using Scan = cub::BlockScan<int, kBuildSmallThreads>;
   using Reduce = cub::BlockReduce<long long, kBuildSmallThreads>;
+  using ReduceU = cub::BlockReduce<uint32_t, kBuildSmallThreads>;
   union Temp {
     typename Sort::TempStorage sort;
     typename Scan::TempStorage scan;
     typename Reduce::TempStorage reduce;
+    typename ReduceU::TempStorage reduce_u;
   };
   static constexpr size_t kSmem = sizeof(Temp) + sizeof(uint32_t) * kBuildSmallThreads;
 };
@@ -712,7 +714,36 @@ build_small_kernel(const uint8_t* __restrict__ keys, int dtype, int width, const
       v[i] = -1;
     }
   }
-  typename B::Sort(tmp.sort).Sort(k, v);  // blocked arrangement, ascending, stable
+  // sort only the bits the keys span: offsets from the block's smallest key, padding at the top
+  // of the range (stable: it stays behind every real row with the same offset).  A dimension's
+  // keys span a few thousand values, so the block sort makes 3 passes of 4 bits instead of 8
+  __shared__ uint32_t s_lo, s_hi;
+  {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if ((int64_t)t * ITEMS + i < n) {
+        lo = min(lo, k[i]);
+        hi = max(hi, k[i]);
+      }
+    const uint32_t blo = typename B::ReduceU(tmp.reduce_u).Reduce(lo, cub::Min());
+    __syncthreads();
+    const uint32_t bhi = typename B::ReduceU(tmp.reduce_u).Reduce(hi, cub::Max());
+    if (t == 0) {
+      s_lo = blo;
+      s_hi = bhi;
+    }
+    __syncthreads();
+  }
+  const uint32_t klo = s_lo;
+  const uint32_t span = s_hi - klo;
+  const int end_bit = span == 0 ? 1 : 32 - __clz(span);
+  const uint32_t pad = end_bit >= 32 ? 0xFFFFFFFFu : ((1u << end_bit) - 1u);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) k[i] = (int64_t)t * ITEMS + i < n ? k[i] - klo : pad;
+  typename B::Sort(tmp.sort).Sort(k, v, 0, end_bit);  // blocked arrangement, ascending, stable
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) k[i] += klo;  // (padding wraps harmlessly: never read as a key)
   last_key[t] = k[ITEMS - 1];
   __syncthreads();
   int flag[ITEMS];
@@ -918,7 +949,11 @@ int esc_hash_build(const void* keys, int32_t key_dtype, const int64_t* rows, int
                                                      reinterpret_cast<long long*>(out_group_start), out_stats);
       return cudaGetLastError();
     };
-    e = run(esc::build_small_kernel<8>, esc::BuildSmall<8>::kSmem, 1);
+    // the fewest items per thread that hold the build (a smaller block sort per launch)
+    e = n <= esc::kBuildSmallThreads     ? run(esc::build_small_kernel<1>, esc::BuildSmall<1>::kSmem, 1)
+        : n <= 2 * esc::kBuildSmallThreads ? run(esc::build_small_kernel<2>, esc::BuildSmall<2>::kSmem, 2)
+        : n <= 4 * esc::kBuildSmallThreads ? run(esc::build_small_kernel<4>, esc::BuildSmall<4>::kSmem, 4)
+                                           : run(esc::build_small_kernel<8>, esc::BuildSmall<8>::kSmem, 8);
     if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("small hash build: ") + cudaGetErrorString(e));
     return ESC_OK;
   }
