@@ -117,6 +117,8 @@ struct KParams {
   unsigned long long* scan_done;  // select: the last CTA sets it (release) once the count, bitmap and
                                   // captures are complete: sel_mid_kernel starts on it, not on the grid's
                                   // completion (griddepcontrol.wait returns ~3 us later), or nullptr
+  int32_t bitmap_lean;        // select in a step plan whose compaction reads no bitmap for captured
+                              // or empty segments: their bitmap words are not written (DenseRule.lean)
 };
 
 // Programmatic dependent launch: the compaction chain's kernels are launched with
@@ -1190,22 +1192,25 @@ __global__ void __launch_bounds__(Layout<COMPACT>::kThreads, 1) esc_scan_kernel(
       const uint32_t pc = __popc(bits);
       my_count += pc;
       if (p.sel_on) {
-        // 8 lanes x 4 rows of a chunk = one 32-row bitmap word (row-linear order)
-        const int64_t word0 = tile * (p.tile_rows / 32) + cw * (4 * C) + (lane >> 3);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          uint32_t v = ((bits >> (4 * c)) & 0xFu) << (4 * (lane & 7));
-          v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
-          v |= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
-          v |= __shfl_xor_sync(0xFFFFFFFFu, v, 4);
-          if ((lane & 7) == 0) p.sel.bitmap[word0 + 4 * c] = v;
-        }
         const int64_t seg = tile * kConsumerWarps + cw;
-        const uint32_t pc = __popc(bits);
-        uint32_t wtot = pc, flag = 0;
+        const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)__popc(bits));
+        const bool capt = C <= 4 && p.sel.n_cap > 0 && wtot > 0 && wtot <= (uint32_t)(4 * C);  // 8-bit fields: C <= 4
+        if (!(p.bitmap_lean && (capt || wtot == 0))) {
+          // 8 lanes x 4 rows of a chunk = one 32-row bitmap word (row-linear order); a lean
+          // step skips the words of captured and empty segments (their 75 MB on config 4 cost
+          // ~50 us of the scan: writes interleaved with the read stream)
+          const int64_t word0 = tile * (p.tile_rows / 32) + cw * (4 * C) + (lane >> 3);
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) wtot += __shfl_xor_sync(0xFFFFFFFFu, wtot, d);
-        if (C <= 4 && p.sel.n_cap > 0 && wtot > 0 && wtot <= (uint32_t)(4 * C)) {  // 8-bit chunk fields: C <= 4
+          for (int c = 0; c < C; ++c) {
+            uint32_t v = ((bits >> (4 * c)) & 0xFu) << (4 * (lane & 7));
+            v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+            v |= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+            v |= __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+            if ((lane & 7) == 0) p.sel.bitmap[word0 + 4 * c] = v;
+          }
+        }
+        uint32_t flag = 0;
+        if (capt) {
           // very sparse segment: capture the hits' projected values now, while they sit in smem
           // (warp-local ranks: per-chunk lane counts in 8-bit fields, one scan ranks every chunk)
           flag = ESC_SEG_CAPTURED;
@@ -1344,7 +1349,20 @@ struct DenseRule {
   uint32_t* n_dense;       // out: number of dense tiles
   const unsigned long long* skip_count;  // ESC_OUT_SKIP_OVER_CAPACITY: the selection's count ...
   long long skip_capacity;               // ... and the capacity it must not exceed
+  uint32_t lean;           // K1 wrote no bitmap words for captured / empty segments: a stream tile
+                           // holding one is never dense (its segments go to sel_compact_kernel)
 };
+
+// a segment's share in its stream tile's density (dense_rule_ok): the hit count, or with a lean
+// bitmap a marker for a captured or empty segment that keeps its tile out of the dense list
+constexpr uint32_t kLeanMarker = 1u << 24;  // > any tile's hits (<= 8 segments x 1024 rows)
+__device__ __forceinline__ uint32_t dense_share(const DenseRule& r, uint32_t raw) {
+  const uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
+  return (r.lean && ((raw & ESC_SEG_CAPTURED) || cnt == 0)) ? kLeanMarker : cnt;
+}
+__device__ __forceinline__ bool dense_rule_ok(const DenseRule& r, uint32_t tile_share) {
+  return tile_share >= r.dense_min && tile_share < kLeanMarker;
+}
 
 __device__ __forceinline__ bool skip_materialize(const DenseRule& r) {
   return r.skip_count != nullptr && (long long)*r.skip_count > r.skip_capacity;
@@ -1445,16 +1463,20 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_apply(const uint32_t* 
   }
   if (rule.dense_min == 0xFFFFFFFFu) return;
   // dense stream tiles among this thread's 4 segments (8-segment tiles: thread pairs)
-  const uint32_t pair = (uint32_t)v + __shfl_xor_sync(0xFFFFFFFFu, (uint32_t)v, 1);
+  uint32_t sh4[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sh4[j] = (base + j < n) ? dense_share(rule, counts[base + j]) : 0u;
+  const uint32_t vs = sh4[0] + sh4[1] + sh4[2] + sh4[3];
+  const uint32_t pair = vs + __shfl_xor_sync(0xFFFFFFFFu, vs, 1);
   bool d0 = false, d1 = false;
   int64_t t0 = -1, t1 = -1;
   if (rule.segs_per_tile == 8) {
-    if ((threadIdx.x & 1) == 0) { t0 = base / 8; d0 = pair >= rule.dense_min; }
+    if ((threadIdx.x & 1) == 0) { t0 = base / 8; d0 = dense_rule_ok(rule, pair); }
   } else if (rule.segs_per_tile == 4) {
-    t0 = base / 4; d0 = v >= rule.dense_min;
+    t0 = base / 4; d0 = dense_rule_ok(rule, vs);
   } else {
-    t0 = base / 2; d0 = x[0] + x[1] >= rule.dense_min;
-    t1 = t0 + 1;   d1 = x[2] + x[3] >= rule.dense_min;
+    t0 = base / 2; d0 = dense_rule_ok(rule, sh4[0] + sh4[1]);
+    t1 = t0 + 1;   d1 = dense_rule_ok(rule, sh4[2] + sh4[3]);
   }
   d0 = d0 && t0 >= 0 && t0 < rule.n_tiles;
   d1 = d1 && t1 >= 0 && t1 < rule.n_tiles;
@@ -1601,9 +1623,9 @@ __device__ __forceinline__ bool in_dense_tile(const SelParams& p, int64_t seg) {
   uint32_t ts = 0;
   for (int j = 0; j < p.rule.segs_per_tile; ++j) {
     const int64_t q = t * p.rule.segs_per_tile + j;
-    if (q < p.n_segs) ts += __ldg(p.seg_counts + q) & ~ESC_SEG_CAPTURED;
+    if (q < p.n_segs) ts += dense_share(p.rule, __ldg(p.seg_counts + q));
   }
-  return ts >= p.rule.dense_min;
+  return dense_rule_ok(p.rule, ts);
 }
 
 __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
@@ -1651,9 +1673,10 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
     }
     uint32_t cnt = raw & ~ESC_SEG_CAPTURED;
     if (p.rule.dense_min != 0xFFFFFFFFu) {
-      uint32_t ts = cnt;  // hits of my stream tile (segments_per_tile consecutive lanes)
+      // my stream tile's density (segments_per_tile consecutive lanes; lanes past the end add 0)
+      uint32_t ts = myseg < p.n_segs ? dense_share(p.rule, raw) : 0u;
       for (int d = 1; d < p.rule.segs_per_tile; d <<= 1) ts += __shfl_xor_sync(0xFFFFFFFFu, ts, d);
-      if (ts >= p.rule.dense_min && (myseg >> (__ffs(p.rule.segs_per_tile) - 1)) < p.rule.n_tiles) cnt = 0;
+      if (dense_rule_ok(p.rule, ts) && (myseg >> (__ffs(p.rule.segs_per_tile) - 1)) < p.rule.n_tiles) cnt = 0;
     }
     const bool captured = (raw & ESC_SEG_CAPTURED) != 0;
     const bool bitmap_work = cnt > 0 && (!captured || p.need_bitmap_captured);

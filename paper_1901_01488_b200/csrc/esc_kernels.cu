@@ -710,6 +710,11 @@ std::atomic<int> g_mid_early{[] {
   const char* e = getenv("ESC_MID_EARLY");
   return e ? atoi(e) : 1;
 }()};
+// lean selection bitmaps in step plans (ESC_BITMAP_LEAN=0: every segment's words written)
+std::atomic<int> g_bitmap_lean{[] {
+  const char* e = getenv("ESC_BITMAP_LEAN");
+  return e ? atoi(e) : 1;
+}()};
 std::atomic<long long> g_mid_max_rows{[] {
   const char* e = getenv("ESC_MID_MAX_ROWS");
   return e ? atoll(e) : (32ll << 20);
@@ -1221,6 +1226,13 @@ int esc_step_plan_create(const esc_program_t* prog, const esc_column_t* cols, in
   if (rc != ESC_OK) {
     delete plan;
     return rc;
+  }
+  // the plan's selection lives only for its own compaction: when that reads no bitmap for
+  // captured segments (every projection captured, no row ids), K1 skips the bitmap words of
+  // captured and empty segments and the dense-tile rule keeps their tiles off the streamed path
+  if (!plan->mat.empty && !plan->mat.sp.need_bitmap_captured && sel->n_cap > 0 && g_bitmap_lean.load()) {
+    plan->kp.bitmap_lean = 1;
+    plan->mat.sp.rule.lean = 1;
   }
   // a mid-size compaction in the same plan as its scan starts on the scan's completion flag (set
   // by its last CTA) instead of the grid's completion

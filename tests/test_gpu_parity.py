@@ -351,6 +351,36 @@ def test_stream_selectivity_sweep(cuda, stream_mode):
         assert np.array_equal(cz2.values.cpu().numpy(), z[want2])
 
 
+def test_lean_bitmap_step_mixed_density(cuda, stream_mode):
+    """A queued step whose projections are all predicate columns (the plan's K1 writes no bitmap
+    words for captured or empty segments): clustered hits give tiles that mix dense, captured and
+    empty segments, and every route (streamed dense tiles, captured copies, sparse gathers) must
+    still yield the rows in order — with streaming always on, the lean rule keeps tiles holding a
+    captured or empty segment off the streamed path."""
+    from paper_1901_01488_b200 import ColumnTable, executor, expr as ex
+    from paper_1901_01488_b200.storage import KIND_INT32, KIND_INT64, Column
+
+    n = 3_000_029
+    g = np.random.default_rng(31)
+    x = g.integers(0, 1_000_000, n).astype(np.int32)
+    # clusters: runs of rows that all pass, runs that pass sparsely, and runs with no hit at all
+    block = np.arange(n) // 3000
+    kind = block % 5
+    x = np.where(kind == 0, g.integers(0, 1000, n), x).astype(np.int32)          # dense runs
+    x = np.where(kind == 1, np.where(g.random(n) < 0.004, 5, 999_999), x).astype(np.int32)  # sparse
+    x = np.where(kind == 2, 999_999, x).astype(np.int32)                           # empty
+    y = g.integers(-(1 << 40), 1 << 40, n).astype(np.int64)
+    t = ColumnTable("t", [Column("x", KIND_INT32, x, device=cuda), Column("y", KIND_INT64, y, device=cuda)])
+    for hi in (999, 49_999, 199_999):
+        p = ex.And((ex.Range(ex.ColumnRef("t", "x"), 0, hi), ex.Comparison(ex.ColumnRef("t", "y"), ">", -(1 << 40) + 5)))
+        want = np.flatnonzero((x <= hi) & (y > -(1 << 40) + 5))
+        count, cols = executor.count_and_materialize(t, p, ["y", "x"], n)
+        assert count == want.size
+        cy, cx = cols
+        assert np.array_equal(cx.values.cpu().numpy(), x[want]), hi
+        assert np.array_equal(cy.values.cpu().numpy(), y[want]), hi
+
+
 def test_queued_compaction_checks_count_on_device(cuda):
     """count_and_materialize queues the compaction behind the scan with a device-side capacity
     check: a qualifying table is materialised exactly, an overflowing one yields no temp and its
