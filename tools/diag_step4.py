@@ -47,3 +47,14 @@ for capture in (True, False):
     mat = statistics.median(x for x, k in tt if k == "materialize")
     print(f"capture={capture}: K1 select {sel:.4f} ms, compaction {mat:.4f} ms")
     executor.set_capture(prev)
+# the one-pass kernel (K2: scan + decoupled look-back + compaction in one launch) on the same table
+if "--onepass" in sys.argv:
+    def one():
+        return executor.materialize_onepass(t, pred, w.project, cap)
+    for _ in range(3): one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10): one()
+    e1.record(); torch.cuda.synchronize()
+    print(f"one-pass K2 materialize (host-inclusive) {e0.elapsed_time(e1) / 10:.4f} ms")
