@@ -721,6 +721,7 @@ def _step_plan(cp: CompiledPredicate, table: ColumnTable, proj: list, capacity: 
         if free:
             lent[:] = [q for q in lent if not any(q is f for f in free)]
             return free[-1]
+        _reclaim_lent(ws)
     n = table.row_count
     _, _, sel = _plan_selection(cp, table, n, [c.name for c in proj], ws)
     slot_of = dict(sel.slot_of)
@@ -778,10 +779,27 @@ def _outputs_free(plan) -> bool:
 
 def _plan_lend(ws, plan):
     """A step's outputs became temp columns (views): the plan is reusable once they are gone."""
+    _reclaim_lent(ws)
     lent = ws.scratch.setdefault("lent", [])
     lent.append(plan)
     if len(lent) > LENT_PLANS:
         lent.pop(0)
+
+
+def _reclaim_lent(ws):
+    """Lent plans whose outputs are free again go back to the plan cache, where its byte budget
+    (STEP_PLAN_BYTES, least recently used first) applies: plans of tables that are gone (a new
+    table object per step) do not pile up with their capacity-sized buffers."""
+    lent = ws.scratch.get("lent")
+    if not lent:
+        return
+    keep = []
+    for q in lent:
+        if _outputs_free(q):
+            _plan_checkin(ws, q)
+        else:
+            keep.append(q)
+    lent[:] = keep
 
 
 def release_step_plans(device: torch.device | None = None):
