@@ -210,3 +210,48 @@ def test_histogram_arm_needs_the_device():
         plan(q, cat, EscConfig(enabled=False, estimator_mode="histogram"))
     p = plan(q, cat, EscConfig(enabled=False))   # baseline arm: no sub-queries, base cardinalities
     assert p.decisions == [] and p.build_order == ["d"] and p.build_card_sum == 3
+
+
+def test_lent_step_plan_bookkeeping():
+    """A queued step's plan lends its output buffers to the temp columns (views): it is reused only
+    once nothing refers to them, and free lent plans return to the byte-bounded plan cache (CPU
+    tensors stand in for the device buffers: the bookkeeping reads storage use counts only)."""
+    import torch
+
+    from paper_1901_01488_b200 import executor
+
+    class _Ws:
+        def __init__(self):
+            self.scratch = {}
+
+    class _Plan:
+        def __init__(self, key, n):
+            self.key = key
+            self.out_values = [torch.empty(n, dtype=torch.int32)]
+            self.out_nulls = [None]
+            self.nbytes = 4 * n
+
+    ws = _Ws()
+    p1 = _Plan(("k", 1), 1000)
+    view = p1.out_values[0][:10]  # a temp column's view
+    executor._plan_lend(ws, p1)
+    assert not executor._outputs_free(p1)
+    executor._reclaim_lent(ws)
+    assert ws.scratch["lent"] == [p1] and "plans" not in ws.scratch  # still lent
+    derived = view[2:5]  # a view of the view keeps it lent too
+    del view
+    executor._reclaim_lent(ws)
+    assert ws.scratch["lent"] == [p1]
+    del derived
+    assert executor._outputs_free(p1)
+    p2 = _Plan(("k", 2), 10)
+    executor._plan_lend(ws, p2)  # lending reclaims the free ones first
+    assert ws.scratch["plans"] == {("k", 1): p1} and ws.scratch["lent"] == [p2]
+    # the cache's byte budget drops the least recently used plans
+    old = executor.STEP_PLAN_BYTES
+    executor.STEP_PLAN_BYTES = 4000
+    try:
+        executor._plan_checkin(ws, _Plan(("k", 3), 500))
+        assert list(ws.scratch["plans"]) == [("k", 3)]
+    finally:
+        executor.STEP_PLAN_BYTES = old
