@@ -539,6 +539,12 @@ int esc_set_stream_div(int div);
  * every size and density, < 0 leaves it.  Default 32M rows (env ESC_MID_MAX_ROWS).  Returns the
  * previous setting. */
 int64_t esc_set_mid_max_rows(int64_t max_rows);
+/* Warp hit lists in the gathered compaction: sparse hits are listed per warp and gathered 32 at a
+ * time by the whole warp (every projected column's loads in flight together) instead of by the
+ * lane that found them.  mode 0 = off, 1 = auto (output capacity <= 1 row in 500, on tables
+ * whose 32-segment groups fill the GPU; default, env ESC_HIT_LISTS), 2 = always; other values
+ * leave it.  Returns the previous setting. */
+int esc_set_hit_lists(int mode);
 /* Diagnostics: when d_stamps (device, >= 8 x grid uint64) is non-null, every later scan launch
  * writes per-CTA %globaltimer stamps (start, first tile, consumers done, producer done, CTA
  * finished; last CTA: finalisation begin / end) into it.

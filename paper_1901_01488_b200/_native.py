@@ -149,6 +149,7 @@ _SIGNATURES = {
     "esc_jit_selftest": (C.c_int, []),
     "esc_set_stream_div": (C.c_int, [C.c_int]),
     "esc_set_mid_max_rows": (C.c_int64, [C.c_int64]),
+    "esc_set_hit_lists": (C.c_int, [C.c_int]),
     "esc_debug_trace": (C.c_int, [C.c_void_p]),
     "esc_copy_regions": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "esc_sort_temp_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32]),
@@ -241,6 +242,13 @@ def set_mid_max_rows(rows: int) -> int:
     the previous setting."""
     TUNING[0] += 1
     return int(load_library().esc_set_mid_max_rows(int(rows)))
+
+
+def set_hit_lists(mode: int) -> int:
+    """Warp hit lists in the gathered compaction (0 off, 1 auto, 2 always); returns the previous
+    setting."""
+    TUNING[0] += 1
+    return int(load_library().esc_set_hit_lists(int(mode)))
 
 
 def set_stream_div(div: int) -> int:

@@ -1542,10 +1542,8 @@ __device__ __forceinline__ unsigned long long ld_w(int width, const void* src, u
   }
 }
 
-// 4 rows of one column: loads first (independent, in flight together), then the stores.  The
-// loads bypass L1 (ld.global.cg): scattered rows would otherwise each pull a whole 128-byte line
-// through L1 into L2/DRAM traffic (measured: 4 sectors per request at 1% selectivity, ~5x the
-// 32-byte sectors the hits occupy)
+// 4 rows of one column: loads first (in flight together), then the stores (ld.global.cg, see
+// ldcg_rows).  The dense segments' path: one row per lane of each word, column by column.
 template <typename T>
 __device__ __forceinline__ void gather4(const uint8_t* data, void* out, const bool (&hit)[4], const int64_t (&prow)[4],
                                         const unsigned long long (&pos)[4]) {
@@ -1555,6 +1553,87 @@ __device__ __forceinline__ void gather4(const uint8_t* data, void* out, const bo
   for (int j = 0; j < 4; ++j) v[j] = hit[j] ? __ldcg(src + prow[j]) : (T)0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) if (hit[j]) static_cast<T*>(out)[pos[j]] = v[j];
+}
+
+// H rows of one column loaded into v (hit rows only; the width switch is per column).  The loads
+// bypass L1 (ld.global.cg): scattered rows would otherwise each pull a whole 128-byte line
+// through L1 into L2/DRAM traffic (measured: 4 sectors per request at 1% selectivity, ~5x the
+// 32-byte sectors the hits occupy)
+template <int H>
+__device__ __forceinline__ void ldcg_rows(int width, const uint8_t* data, const bool (&hit)[H], const int64_t (&prow)[H],
+                                          unsigned long long (&v)[H]) {
+  switch (width) {
+    case 1:
+#pragma unroll
+      for (int j = 0; j < H; ++j) v[j] = hit[j] ? __ldcg(data + prow[j]) : 0u;
+      break;
+    case 2:
+#pragma unroll
+      for (int j = 0; j < H; ++j) v[j] = hit[j] ? __ldcg(reinterpret_cast<const uint16_t*>(data) + prow[j]) : 0u;
+      break;
+    case 4:
+#pragma unroll
+      for (int j = 0; j < H; ++j) v[j] = hit[j] ? __ldcg(reinterpret_cast<const uint32_t*>(data) + prow[j]) : 0u;
+      break;
+    default:
+#pragma unroll
+      for (int j = 0; j < H; ++j) v[j] = hit[j] ? __ldcg(reinterpret_cast<const unsigned long long*>(data) + prow[j]) : 0ull;
+      break;
+  }
+}
+template <int H>
+__device__ __forceinline__ void st_rows(int width, void* out, const bool (&hit)[H], const unsigned long long (&pos)[H],
+                                        const unsigned long long (&v)[H]) {
+  switch (width) {
+    case 1:
+#pragma unroll
+      for (int j = 0; j < H; ++j) if (hit[j]) static_cast<uint8_t*>(out)[pos[j]] = (uint8_t)v[j];
+      break;
+    case 2:
+#pragma unroll
+      for (int j = 0; j < H; ++j) if (hit[j]) static_cast<uint16_t*>(out)[pos[j]] = (uint16_t)v[j];
+      break;
+    case 4:
+#pragma unroll
+      for (int j = 0; j < H; ++j) if (hit[j]) static_cast<uint32_t*>(out)[pos[j]] = (uint32_t)v[j];
+      break;
+    default:
+#pragma unroll
+      for (int j = 0; j < H; ++j) if (hit[j]) static_cast<unsigned long long*>(out)[pos[j]] = v[j];
+      break;
+  }
+}
+
+// H rows of every projected column (captured ones skipped when `skip_captured`): the value loads
+// of up to 4 columns are all in flight before any of their stores, so a row's columns cost one
+// DRAM round trip, not one per column.  NULL bytes (no BASELINE shape has them) follow per column.
+template <int H>
+__device__ __forceinline__ void gather_rows(const SelParams& p, const bool (&hit)[H], const int64_t (&prow)[H],
+                                            const unsigned long long (&pos)[H], bool skip_captured) {
+#pragma unroll 1
+  for (int k0 = 0; k0 < p.n_proj; k0 += 4) {
+    unsigned long long v[4][H];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k0 + kk;
+      if (k < p.n_proj && !(skip_captured && p.cap_index[k] >= 0)) ldcg_rows<H>(p.cols[k].width, p.cols[k].data, hit, prow, v[kk]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k0 + kk;
+      if (k < p.n_proj && !(skip_captured && p.cap_index[k] >= 0)) st_rows<H>(p.cols[k].width, p.outs.out_values[k], hit, pos, v[kk]);
+    }
+  }
+#pragma unroll 1
+  for (int k = 0; k < p.n_proj; ++k) {
+    if (p.outs.out_nulls[k] == nullptr || (skip_captured && p.cap_index[k] >= 0)) continue;
+    const uint8_t* nulls = p.cols[k].nulls;
+    uint8_t nb[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) nb[j] = (hit[j] && nulls) ? __ldcg(nulls + prow[j]) : (uint8_t)0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) if (hit[j]) p.outs.out_nulls[k][pos[j]] = nb[j];
+  }
 }
 
 // Two grid-stride phases over the selection (segments of dense stream tiles are skipped:
@@ -1569,7 +1648,7 @@ __device__ __forceinline__ void gather4(const uint8_t* data, void* out, const bo
 //     groups alone fill the GPU (sparse_in_a), phase A writes its own sparse segments the same
 //     way, chunk by chunk, and phase B is skipped: no second pass over the segment counts.
 // The hits of one 128-row chunk (4 bitmap words `w4` of segment `seg`, chunk `sub`), written
-// from output position `pos` on, four at a time: every column's loads in flight before the stores.
+// from output position `pos` on, four at a time (phase B: small selections).
 __device__ __forceinline__ void sparse_chunk(const SelParams& p, int64_t seg, int sub, uint4 w4,
                                              unsigned long long pos, bool scap) {
   const int W = p.seg_rows / 32;
@@ -1628,7 +1707,67 @@ __device__ __forceinline__ bool in_dense_tile(const SelParams& p, int64_t seg) {
   return dense_rule_ok(p.rule, ts);
 }
 
-__global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __grid_constant__ SelParams p) {
+// A warp's list of sparse hits (phase A): entries (row, output position | kHitSkipCaptured) in
+// row order.  A round adds at most 32 / CPS segments x 4*CPS bits = 128 entries, and the list is
+// flushed whenever it holds 32 or more, so 160 entries suffice.
+constexpr int kHitList = 160;
+constexpr unsigned long long kHitSkipCaptured = 1ull << 63;  // the entry's captured columns are written elsewhere
+
+// gathers the list's first entries with the whole warp, two per lane per pass (every column's
+// loads of both in flight before the stores): all of them when `all`, else the largest multiple
+// of 32; the rest move to the front.  Returns the entries left.
+__device__ __noinline__ int flush_hits(const SelParams& p, int64_t* hl_row, unsigned long long* hl_pos, int n,
+                                       bool all) {
+  const int lane = threadIdx.x & 31;
+  const long long cap = p.outs.capacity;
+  __syncwarp();
+  const int nf = all ? n : (n & ~31);
+  for (int e0 = 0; e0 < nf; e0 += 64) {
+    bool hit[2];
+    int64_t prow[2];
+    unsigned long long pos[2];
+    bool scap = false;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int e = e0 + 32 * j + lane;
+      const unsigned long long pe = e < nf ? hl_pos[e] : 0ull;
+      pos[j] = pe & ~kHitSkipCaptured;
+      hit[j] = e < nf && (long long)pos[j] < cap;
+      scap = scap || (hit[j] && (pe & kHitSkipCaptured));
+      const int64_t row = e < nf ? hl_row[e] : 0;
+      prow[j] = (hit[j] && p.row_ids) ? __ldg(p.row_ids + row) : row;
+    }
+    if (scap) {  // a captured segment's entry: write its uncaptured columns one entry at a time
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int e = e0 + 32 * j + lane;
+        const bool sj = hit[j] && (hl_pos[e] & kHitSkipCaptured);
+        bool h1[1] = {hit[j]};
+        int64_t r1[1] = {prow[j]};
+        unsigned long long p1[1] = {pos[j]};
+        gather_rows<1>(p, h1, r1, p1, sj);
+        hit[j] = false;
+        if (p.outs.out_row_ids != nullptr && h1[0]) p.outs.out_row_ids[p1[0]] = r1[0];
+      }
+    }
+    gather_rows<2>(p, hit, prow, pos, false);
+    if (p.outs.out_row_ids != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) if (hit[j]) p.outs.out_row_ids[pos[j]] = prow[j];
+    }
+  }
+  const int rem = n - nf;
+  int64_t r = 0;
+  unsigned long long q = 0;
+  if (lane < rem) { r = hl_row[nf + lane]; q = hl_pos[nf + lane]; }
+  __syncwarp();
+  if (lane < rem) { hl_row[lane] = r; hl_pos[lane] = q; }
+  __syncwarp();
+  return rem;
+}
+
+template <bool kList>
+__global__ void __launch_bounds__(kSelWarps * 32, kList ? 3 : 4) sel_compact_kernel(const __grid_constant__ SelParams p) {
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x & 31;
@@ -1639,6 +1778,12 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t sparse_max = (uint32_t)W;
   if (skip_materialize(p.rule)) return;
+  __shared__ uint8_t cand_lanes[kSelWarps][32];
+  __shared__ int64_t hit_rows[kSelWarps][kList ? kHitList : 1];
+  __shared__ unsigned long long hit_pos[kSelWarps][kList ? kHitList : 1];
+  int64_t* hl_row = hit_rows[threadIdx.x >> 5];
+  unsigned long long* hl_pos = hit_pos[threadIdx.x >> 5];
+  int hl_n = 0;  // warp-uniform: entries in the warp's hit list
   // ---------------- A: captured and dense segments ----------------
   // a_split (R, a power of two) warps share a group: warp r of it takes captured entries
   // r*32 + lane (mod 32R) and every R-th dense segment, so small selections use the whole grid
@@ -1736,38 +1881,106 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
       }
     }
     const bool sparse_work = bitmap_work && cnt <= sparse_max;
-    if (p.sparse_in_a && __any_sync(0xFFFFFFFFu, sparse_work)) {
-      // large selections: this warp's own sparse segments, C lanes per segment, one 128-row chunk
-      // each (32 chunks in flight per round); small ones leave them to phase B's wider spread
+    if constexpr (!kList) {
+      if (p.sparse_in_a && __any_sync(0xFFFFFFFFu, sparse_work)) {
+        // large selections: this warp's own sparse segments, C lanes per segment, one 128-row chunk
+        // each (32 chunks in flight per round); small ones leave them to phase B's wider spread
+        const unsigned long long soff_l = off_l;
+        const int CPS = W / 4;
+        const int cps_log = __ffs(CPS) - 1;
+        // the next round's bitmap chunk is loaded one round ahead (its latency hides behind this
+        // round's ranking and gathers)
+        auto load_round = [&](int b) {
+          const int sl = (b * 32 + lane) >> cps_log;
+          const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
+          return work ? __ldg(reinterpret_cast<const uint4*>(p.bitmap + (seg0 + sl) * W + ((b * 32 + lane) & (CPS - 1)) * 4))
+                      : make_uint4(0u, 0u, 0u, 0u);
+        };
+        uint4 w4n = load_round(0);
+        for (int b = 0; b < CPS; ++b) {
+          const int c = b * 32 + lane;
+          const int sl = c >> cps_log;  // lane owning the chunk's segment
+          const int sub = c & (CPS - 1);
+          const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
+          const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, soff_l, sl);
+          const bool scap = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, sl) != 0;
+          const int64_t seg = seg0 + sl;
+          const uint4 w4 = w4n;
+          if (b + 1 < CPS) w4n = load_round(b + 1);
+          const uint32_t pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+          uint32_t incl = pc;
+          for (int d = 1; d < CPS; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d, CPS);
+            if ((lane & (CPS - 1)) >= d) incl += t;
+          }
+          if (work && pc != 0) sparse_chunk(p, seg, sub, w4, soff + incl - pc, scap);
+        }
+      }
+    }
+    const uint32_t cand = (kList && p.sparse_in_a) ? __ballot_sync(0xFFFFFFFFu, sparse_work) : 0u;
+    if (kList && cand != 0u) {
+      // large selections: this warp's own sparse segments, CPS lanes per segment (one 128-row
+      // chunk each).  Rounds run over the group's CANDIDATE segments only (32 / CPS per round):
+      // at low selectivity most segments of a group are empty, and a round per 32 / CPS segments
+      // regardless of hits cost a bitmap round trip per round with nothing to write.  The next
+      // round's bitmap chunk is loaded one round ahead.
       const unsigned long long soff_l = off_l;
       const int CPS = W / 4;
       const int cps_log = __ffs(CPS) - 1;
-      // the next round's bitmap chunk is loaded one round ahead (its latency hides behind this
-      // round's ranking and gathers)
-      auto load_round = [&](int b) {
-        const int sl = (b * 32 + lane) >> cps_log;
-        const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
-        return work ? __ldg(reinterpret_cast<const uint4*>(p.bitmap + (seg0 + sl) * W + ((b * 32 + lane) & (CPS - 1)) * 4))
-                    : make_uint4(0u, 0u, 0u, 0u);
+      const int ncand = __popc(cand);
+      const int sub = lane & (CPS - 1);
+      // the candidates' group lanes in order, through a per-warp shared-memory list
+      uint8_t* clist = cand_lanes[threadIdx.x >> 5];
+      __syncwarp();  // the previous group's reads of the list are done
+      if (sparse_work) clist[__popc(cand & lt)] = (uint8_t)lane;
+      __syncwarp();
+      auto cand_lane = [&](int q0) {  // group lane (segment) of this lane's candidate in round q0, or -1
+        const int ci = q0 + (lane >> cps_log);
+        return ci < ncand ? (int)clist[ci] : -1;
       };
-      uint4 w4n = load_round(0);
-      for (int b = 0; b < CPS; ++b) {
-        const int c = b * 32 + lane;
-        const int sl = c >> cps_log;  // lane owning the chunk's segment
-        const int sub = c & (CPS - 1);
-        const bool work = __shfl_sync(0xFFFFFFFFu, sparse_work ? 1 : 0, sl) != 0;
-        const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, soff_l, sl);
-        const bool scap = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, sl) != 0;
-        const int64_t seg = seg0 + sl;
+      auto load_round = [&](int sl) {
+        return sl >= 0 ? __ldg(reinterpret_cast<const uint4*>(p.bitmap + (seg0 + sl) * W + sub * 4))
+                       : make_uint4(0u, 0u, 0u, 0u);
+      };
+      const int per_round = 32 >> cps_log;
+      int sl_n = cand_lane(0);
+      uint4 w4n = load_round(sl_n);
+      for (int q0 = 0; q0 < ncand; q0 += per_round) {
+        const int sl = sl_n;
         const uint4 w4 = w4n;
-        if (b + 1 < CPS) w4n = load_round(b + 1);
+        if (q0 + per_round < ncand) {
+          sl_n = cand_lane(q0 + per_round);
+          w4n = load_round(sl_n);
+        }
+        const int src = sl >= 0 ? sl : 0;
+        const unsigned long long soff = __shfl_sync(0xFFFFFFFFu, soff_l, src);
+        const bool scap = __shfl_sync(0xFFFFFFFFu, captured ? 1 : 0, src) != 0;
         const uint32_t pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
         uint32_t incl = pc;
         for (int d = 1; d < CPS; d <<= 1) {
           const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d, CPS);
-          if ((lane & (CPS - 1)) >= d) incl += t;
+          if (sub >= d) incl += t;
         }
-        if (work && pc != 0) sparse_chunk(p, seg, sub, w4, soff + incl - pc, scap);
+        // the round's hits go to the warp's hit list (row order = output order), and every full
+        // 32 entries are gathered by the whole warp at once
+        const uint32_t mine = sl >= 0 ? pc : 0u;
+        uint32_t wincl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wincl, d);
+          if (lane >= d) wincl += t;
+        }
+        if (mine != 0u) {
+          int at = hl_n + (int)(wincl - mine);
+          unsigned long long pos = (soff + incl - pc) | (scap ? kHitSkipCaptured : 0ull);
+          const int64_t row_base = ((seg0 + sl) * W + sub * 4) * 32;
+          unsigned long long lo = ((unsigned long long)w4.y << 32) | w4.x;
+          unsigned long long hi = ((unsigned long long)w4.w << 32) | w4.z;
+          while (lo) { hl_row[at] = row_base + __ffsll((long long)lo) - 1; hl_pos[at++] = pos++; lo &= lo - 1; }
+          while (hi) { hl_row[at] = row_base + 64 + __ffsll((long long)hi) - 1; hl_pos[at++] = pos++; hi &= hi - 1; }
+        }
+        hl_n += (int)__shfl_sync(0xFFFFFFFFu, wincl, 31);
+        if (hl_n >= 32) hl_n = flush_hits(p, hl_row, hl_pos, hl_n, false);
       }
     }
     uint32_t dense = __ballot_sync(0xFFFFFFFFu, dense_work);
@@ -1825,6 +2038,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) sel_compact_kernel(const __gri
       }
     }
   }
+  if (kList && hl_n > 0) flush_hits(p, hl_row, hl_pos, hl_n, true);
   // ---------------- B: sparse segments, one lane per 128-row chunk ----------------
   if (p.sparse_in_a) return;
   const int CPS = W / 4;  // chunks per segment (1, 2, 4, 8): a power of two dividing 32

@@ -715,6 +715,12 @@ std::atomic<int> g_bitmap_lean{[] {
   const char* e = getenv("ESC_BITMAP_LEAN");
   return e ? atoi(e) : 1;
 }()};
+// warp hit lists in the gathered compaction (ESC_HIT_LISTS: 0 off, 1 auto = sparse selections of
+// tables whose segment groups fill the GPU, 2 always)
+std::atomic<int> g_hit_lists{[] {
+  const char* e = getenv("ESC_HIT_LISTS");
+  return e ? atoi(e) : 1;
+}()};
 std::atomic<long long> g_mid_max_rows{[] {
   const char* e = getenv("ESC_MID_MAX_ROWS");
   return e ? atoll(e) : (32ll << 20);
@@ -845,6 +851,7 @@ struct MatLaunch {
   StreamParams tp;
   MidParams mp;
   bool mid = false;        // one sel_mid_kernel launch instead of the scan + compaction chain
+  bool hit_list = false;   // sel_compact_kernel<true>: sparse hits gathered through warp hit lists
   size_t mid_smem = 0;
   bool streaming = false;
   bool empty = true;
@@ -870,6 +877,7 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   const WsLayout L = ws_layout(nrows);
   if (d_ws == nullptr || ws_bytes < L.total) return fail(ESC_ERR_WORKSPACE, "workspace too small");
   M->mid = false;  // M may be a reused (thread-local) launch: every route flag is re-decided here
+  M->hit_list = false;
   M->streaming = false;
   M->empty = true;
   std::memset(&sp, 0, sizeof(sp));
@@ -990,15 +998,26 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   // phase A: 32 segments per warp; when those groups alone give every SM 4+ CTAs, phase A also
   // writes the sparse segments; otherwise phase B spreads 128-row chunks (32 per warp)
   const int64_t groups_ctas = (sp.n_segs + 32 * kSelWarps - 1) / (32 * kSelWarps);
-  sp.sparse_in_a = groups_ctas >= 4LL * sms ? 1 : 0;
+  const int hl_mode = g_hit_lists.load();
+  sp.sparse_in_a = (groups_ctas >= 4LL * sms || hl_mode == 2) ? 1 : 0;
   const int64_t chunks = sp.n_segs * (sp.seg_rows / kChunkRows);
   const int64_t want = sp.sparse_in_a ? groups_ctas : (chunks + 32 * kSelWarps - 1) / (32 * kSelWarps);
+  // warp hit lists for sparse selections (capacity <= 1 row in 500): a few hits per 32 segments,
+  // so lanes gathering their own chunk's hits would leave most of the warp idle (config-5 shape,
+  // 600M rows: s = 1e-4 98 -> 52 us, 1e-3 170 -> 141 us; at 3e-3 the lanes win, 228 vs 262 us)
+  M->hit_list = hl_mode == 2 || (hl_mode == 1 && sp.sparse_in_a && outs->capacity * 500 <= nrows);
   // one wave of resident CTAs: warps loop over groups with the next group's loads in flight
-  static const int resident = [] {
+  static const int resident_lanes = [] {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sel_compact_kernel, kSelWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sel_compact_kernel<false>, kSelWarps * 32, 0);
     return b > 0 ? b : 4;
   }();
+  static const int resident_list = [] {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sel_compact_kernel<true>, kSelWarps * 32, 0);
+    return b > 0 ? b : 3;
+  }();
+  const int resident = M->hit_list ? resident_list : resident_lanes;
   const int64_t cap_grid = (int64_t)sms * resident;
   M->compact_grid = (unsigned)(want < cap_grid ? want : cap_grid);
   sp.a_split = 1;
@@ -1043,7 +1062,9 @@ int issue_mat(const MatLaunch& M, cudaStream_t st) {
                    static_cast<const unsigned long long*>(M.partials), M.offsets, sp.rule);
   if (e == cudaSuccess && M.streaming)
     e = launch_pdl(sel_stream_kernel, M.stream_grid, (1 + M.tp.consumers) * 32, M.stream_smem, st, M.tp);
-  if (e == cudaSuccess) e = launch_pdl(sel_compact_kernel, M.compact_grid, kSelWarps * 32, 0, st, sp);
+  if (e == cudaSuccess)
+    e = M.hit_list ? launch_pdl(sel_compact_kernel<true>, M.compact_grid, kSelWarps * 32, 0, st, sp)
+                   : launch_pdl(sel_compact_kernel<false>, M.compact_grid, kSelWarps * 32, 0, st, sp);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ESC_ERR_CUDA, std::string("selection compaction launch: ") + cudaGetErrorString(e));
   return ESC_OK;
@@ -1476,6 +1497,12 @@ int esc_debug_trace(void* d_stamps) {
 int esc_set_stream_div(int div) {
   const int prev = g_stream_div.load();
   g_stream_div = div;
+  return prev;
+}
+
+int esc_set_hit_lists(int mode) {
+  const int prev = g_hit_lists.load();
+  if (mode >= 0 && mode <= 2) g_hit_lists = mode;
   return prev;
 }
 

@@ -65,7 +65,7 @@ SIZES = [1, 127, 128, 1025, 4097, 8193, 65_537, (1 << 21) + 3, 3_000_005]
 
 
 @pytest.mark.parametrize("n", SIZES)
-@pytest.mark.parametrize("route", ["chain", "mid", "stream"])
+@pytest.mark.parametrize("route", ["chain", "mid", "stream", "hitlist"])
 def test_select_and_materialize_stay_in_bounds(cuda, n, route):
     from paper_1901_01488_b200 import _native as N, expr as ex
     from paper_1901_01488_b200.compiler import compile_predicate
@@ -73,6 +73,7 @@ def test_select_and_materialize_stay_in_bounds(cuda, n, route):
     lib = N.load_library()
     prev_mid = N.set_mid_max_rows(1 << 40 if route == "mid" else 0)
     prev_div = N.set_stream_div(1 << 30 if route == "stream" else 32)
+    prev_hl = N.set_hit_lists(2 if route == "hitlist" else 1)
     try:
         t, a, b, bn = _table(n, cuda)
         for hi in (9, 499, 999):  # ~1%, 50%, 100% of the rows
@@ -133,6 +134,7 @@ def test_select_and_materialize_stay_in_bounds(cuda, n, route):
     finally:
         N.set_mid_max_rows(prev_mid)
         N.set_stream_div(prev_div)
+        N.set_hit_lists(prev_hl)
 
 
 @pytest.mark.parametrize("n", [1, 127, 4097, 65_537, 300_001])

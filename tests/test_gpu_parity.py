@@ -268,18 +268,21 @@ def test_selection_reuse(mixed):
 
 
 # ---- scan-time capture and streamed compaction of dense tiles ---------------------------------
-@pytest.fixture(params=["off", "default", "always", "mid"])
+@pytest.fixture(params=["off", "default", "always", "mid", "hitlist"])
 def stream_mode(request, cuda):
     """The compaction route: the scan + gathered chain with streaming of dense tiles off /
-    default / always, or the one-launch mid-size kernel."""
+    default / always, the gathered chain with warp hit lists forced on, or the one-launch
+    mid-size kernel."""
     from paper_1901_01488_b200 import _native as N
 
-    div = {"off": 0, "default": 32, "always": 1 << 30, "mid": 32}[request.param]
+    div = {"off": 0, "default": 32, "always": 1 << 30, "mid": 32, "hitlist": 32}[request.param]
     prev = N.set_stream_div(div)
     prev_mid = N.set_mid_max_rows(1 << 40 if request.param == "mid" else 0)
+    prev_hl = N.set_hit_lists(2 if request.param == "hitlist" else 1)
     yield request.param
     N.set_stream_div(prev)
     N.set_mid_max_rows(prev_mid)
+    N.set_hit_lists(prev_hl)
 
 
 @pytest.mark.parametrize("capture", [False, True])
