@@ -1707,17 +1707,16 @@ __device__ __forceinline__ bool in_dense_tile(const SelParams& p, int64_t seg) {
   return dense_rule_ok(p.rule, ts);
 }
 
-// A warp's list of sparse hits (phase A): entries (row, output position | kHitSkipCaptured) in
-// row order.  A round adds at most 32 / CPS segments x 4*CPS bits = 128 entries, and the list is
+// A warp's list of sparse hits (phase A): entries (row | kHitSkipCaptured, output position), both
+// 32-bit (the host uses lists only for tables of < 2^31 rows: 1.25 KB per warp), in row order.  A round adds at most 32 / CPS segments x 4*CPS bits = 128 entries, and the list is
 // flushed whenever it holds 32 or more, so 160 entries suffice.
 constexpr int kHitList = 160;
-constexpr unsigned long long kHitSkipCaptured = 1ull << 63;  // the entry's captured columns are written elsewhere
+constexpr uint32_t kHitSkipCaptured = 1u << 31;  // the entry's captured columns are written elsewhere
 
 // gathers the list's first entries with the whole warp, two per lane per pass (every column's
 // loads of both in flight before the stores): all of them when `all`, else the largest multiple
 // of 32; the rest move to the front.  Returns the entries left.
-__device__ __noinline__ int flush_hits(const SelParams& p, int64_t* hl_row, unsigned long long* hl_pos, int n,
-                                       bool all) {
+__device__ __noinline__ int flush_hits(const SelParams& p, uint32_t* hl_row, uint32_t* hl_pos, int n, bool all) {
   const int lane = threadIdx.x & 31;
   const long long cap = p.outs.capacity;
   __syncwarp();
@@ -1730,18 +1729,18 @@ __device__ __noinline__ int flush_hits(const SelParams& p, int64_t* hl_row, unsi
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int e = e0 + 32 * j + lane;
-      const unsigned long long pe = e < nf ? hl_pos[e] : 0ull;
-      pos[j] = pe & ~kHitSkipCaptured;
+      const uint32_t re = e < nf ? hl_row[e] : 0u;
+      pos[j] = e < nf ? hl_pos[e] : 0u;
       hit[j] = e < nf && (long long)pos[j] < cap;
-      scap = scap || (hit[j] && (pe & kHitSkipCaptured));
-      const int64_t row = e < nf ? hl_row[e] : 0;
+      scap = scap || (hit[j] && (re & kHitSkipCaptured));
+      const int64_t row = re & ~kHitSkipCaptured;
       prow[j] = (hit[j] && p.row_ids) ? __ldg(p.row_ids + row) : row;
     }
     if (scap) {  // a captured segment's entry: write its uncaptured columns one entry at a time
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int e = e0 + 32 * j + lane;
-        const bool sj = hit[j] && (hl_pos[e] & kHitSkipCaptured);
+        const bool sj = hit[j] && (hl_row[e] & kHitSkipCaptured);
         bool h1[1] = {hit[j]};
         int64_t r1[1] = {prow[j]};
         unsigned long long p1[1] = {pos[j]};
@@ -1757,8 +1756,7 @@ __device__ __noinline__ int flush_hits(const SelParams& p, int64_t* hl_row, unsi
     }
   }
   const int rem = n - nf;
-  int64_t r = 0;
-  unsigned long long q = 0;
+  uint32_t r = 0, q = 0;
   if (lane < rem) { r = hl_row[nf + lane]; q = hl_pos[nf + lane]; }
   __syncwarp();
   if (lane < rem) { hl_row[lane] = r; hl_pos[lane] = q; }
@@ -1779,10 +1777,10 @@ __global__ void __launch_bounds__(kSelWarps * 32, kList ? 3 : 4) sel_compact_ker
   const uint32_t sparse_max = (uint32_t)W;
   if (skip_materialize(p.rule)) return;
   __shared__ uint8_t cand_lanes[kSelWarps][32];
-  __shared__ int64_t hit_rows[kSelWarps][kList ? kHitList : 1];
-  __shared__ unsigned long long hit_pos[kSelWarps][kList ? kHitList : 1];
-  int64_t* hl_row = hit_rows[threadIdx.x >> 5];
-  unsigned long long* hl_pos = hit_pos[threadIdx.x >> 5];
+  __shared__ uint32_t hit_rows[kSelWarps][kList ? kHitList : 1];
+  __shared__ uint32_t hit_pos[kSelWarps][kList ? kHitList : 1];
+  uint32_t* hl_row = hit_rows[threadIdx.x >> 5];
+  uint32_t* hl_pos = hit_pos[threadIdx.x >> 5];
   int hl_n = 0;  // warp-uniform: entries in the warp's hit list
   // ---------------- A: captured and dense segments ----------------
   // a_split (R, a power of two) warps share a group: warp r of it takes captured entries
@@ -1972,8 +1970,8 @@ __global__ void __launch_bounds__(kSelWarps * 32, kList ? 3 : 4) sel_compact_ker
         }
         if (mine != 0u) {
           int at = hl_n + (int)(wincl - mine);
-          unsigned long long pos = (soff + incl - pc) | (scap ? kHitSkipCaptured : 0ull);
-          const int64_t row_base = ((seg0 + sl) * W + sub * 4) * 32;
+          uint32_t pos = (uint32_t)(soff + incl - pc);
+          const uint32_t row_base = (uint32_t)(((seg0 + sl) * W + sub * 4) * 32) | (scap ? kHitSkipCaptured : 0u);
           unsigned long long lo = ((unsigned long long)w4.y << 32) | w4.x;
           unsigned long long hi = ((unsigned long long)w4.w << 32) | w4.z;
           while (lo) { hl_row[at] = row_base + __ffsll((long long)lo) - 1; hl_pos[at++] = pos++; lo &= lo - 1; }

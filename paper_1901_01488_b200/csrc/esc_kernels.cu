@@ -1005,7 +1005,7 @@ int prepare_mat(const esc_selection_t* sel, int64_t nrows, const esc_column_t* c
   // warp hit lists for sparse selections (capacity <= 1 row in 500): a few hits per 32 segments,
   // so lanes gathering their own chunk's hits would leave most of the warp idle (config-5 shape,
   // 600M rows: s = 1e-4 98 -> 52 us, 1e-3 170 -> 141 us; at 3e-3 the lanes win, 228 vs 262 us)
-  M->hit_list = hl_mode == 2 || (hl_mode == 1 && sp.sparse_in_a && outs->capacity * 500 <= nrows);
+  M->hit_list = nrows < (1ll << 31) && (hl_mode == 2 || (hl_mode == 1 && sp.sparse_in_a && outs->capacity * 500 <= nrows));
   // one wave of resident CTAs: warps loop over groups with the next group's loads in flight
   static const int resident_lanes = [] {
     int b = 0;

@@ -1,0 +1,53 @@
+"""Python profile of the single-GPU ESC step's host path (config-4 recipe, default 75M rows):
+cProfile over 200 steps, top functions by own time, plus the step's event time and host wall.
+Usage: diag_step_pyprof.py [rows] [sharded]"""
+import cProfile
+import os
+import pstats
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_1901_01488_b200 import datagen, optimizer, serde
+from paper_1901_01488_b200.catalog import Catalog
+from paper_1901_01488_b200.storage import Column, ColumnTable, parse_kind
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 75_000_000
+dev = torch.device("cuda", 0)
+w = datagen.config4_blocked(n, 0, n)
+t = ColumnTable("t", [Column(k, parse_kind(w.columns[k][0]), w.columns[k][1], device=dev) for k in "ABCD"])
+pred = serde.from_json(w.pred, "t", w.udfs)
+cfg = optimizer.EscConfig()
+cat = Catalog()
+cat.register(t)
+
+
+def step():
+    optimizer.esc_subquery(cat, "t", pred, w.project, cfg)
+    cat.temps.sweep()
+
+
+for _ in range(10):
+    step()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+walls = []
+e0.record()
+for _ in range(50):
+    a = time.perf_counter()
+    step()
+    walls.append((time.perf_counter() - a) * 1e6)
+e1.record()
+torch.cuda.synchronize()
+print(f"step {e0.elapsed_time(e1) / 50 * 1e3:.1f} us (events), host wall per step {statistics.median(walls):.1f} us")
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(200):
+    step()
+pr.disable()
+st = pstats.Stats(pr)
+st.sort_stats("tottime").print_stats(30)
+st.sort_stats("cumulative").print_stats(25)
