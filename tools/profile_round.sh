@@ -5,7 +5,7 @@ set -u
 mkdir -p gpurun_out/prof
 B="python bench.py --steps 2 --warmup 1 --no-extras --no-e2e --no-cpu-baseline"
 N="ncu --set full --clock-control none --import-source on"
-PART=${1:-1}   # two halves: gpurun copies back at most 64 MiB per call
+PART=${1:-1}   # parts 1, 2, 3: gpurun copies back at most 64 MiB per call
 if [ "$PART" = 1 ]; then
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv \
     --log-file gpurun_out/prof/launches_config4.csv $B > gpurun_out/prof/launches.log 2>&1
@@ -17,6 +17,15 @@ $N -k regex:sel_stream --launch-skip 2 --launch-count 1 -o gpurun_out/prof/strea
     python tools/kprof_stream.py 0.5 200000000 > gpurun_out/prof/stream.log 2>&1
 $N -k regex:sel_stream --launch-skip 2 --launch-count 1 -o gpurun_out/prof/stream_config5_s0.1 \
     python tools/kprof_stream.py 0.1 200000000 > gpurun_out/prof/stream01.log 2>&1
+elif [ "$PART" = 3 ]; then
+# gathered compaction of a sparse selection (config-5 shape, 600M rows, s = 1e-3): warp hit lists
+# (the default at this density) vs lane-per-chunk gathers
+$N -k regex:sel_compact --launch-skip 2 --launch-count 1 -o gpurun_out/prof/selcompact_hitlist_s1e-3 \
+    python tools/kprof_stream.py 0.001 600000000 > gpurun_out/prof/hl.log 2>&1
+ESC_HIT_LISTS=0 $N -k regex:sel_compact --launch-skip 2 --launch-count 1 -o gpurun_out/prof/selcompact_lanes_s1e-3 \
+    python tools/kprof_stream.py 0.001 600000000 > gpurun_out/prof/hl0.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/prof/launches_f_paths.csv python tools/launches_f.py > gpurun_out/prof/lf.log 2>&1
 else
 $N -k regex:join_bits --launch-skip 3 --launch-count 1 -o gpurun_out/prof/join_bits_star python tools/diag_join.py \
     > gpurun_out/prof/join.log 2>&1
