@@ -484,7 +484,8 @@ int esc_join_count(const esc_join_t* j, uint64_t* d_stage_counts, void* stream);
  *    or lone '\r' / 3 "\r\n"; rec_end_field[r] = separator index ending record r;
  * 3. esc_csv_parse per column: values (INT64 / DECIMAL scaled by 10**scale / DATE epoch days /
  *    TEXT FNV-1a-64 of the unescaped content + its length), nulls (the \N token), and
- *    first_error = min over failing cells of ((row * ncols + col) << 4 | code).
+ *    first_error = min over failing cells of ((row * ncols + col) << 4 | code); *d_null_seen
+ *    (optional) is set to 1 when the column holds a NULL.
  * The workspace (esc_csv_workspace_bytes) carries the chunk summaries from step 1 to step 2. */
 enum { ESC_CSV_INT64 = 0, ESC_CSV_DECIMAL = 1, ESC_CSV_DATE = 2, ESC_CSV_TEXT = 3 };
 size_t esc_csv_workspace_bytes(int64_t nbytes);
@@ -494,7 +495,8 @@ int esc_csv_fields(const uint8_t* d_bytes, int64_t nbytes, int64_t* d_field_end,
                    int64_t* d_rec_end_field, void* d_ws, size_t ws_bytes, void* stream);
 int esc_csv_parse(const uint8_t* d_bytes, const int64_t* d_field_end, const uint8_t* d_field_kind, int64_t first_field,
                   int64_t nrows, int32_t ncols, int32_t col, int32_t kind, int32_t scale, int64_t* d_values,
-                  int64_t* d_lengths, uint8_t* d_nulls, uint64_t* d_first_error, void* stream);
+                  int64_t* d_lengths, uint8_t* d_nulls, uint64_t* d_first_error, uint32_t* d_null_seen,
+                  void* stream);
 /* Record validation (the reference's csv.reader + per-record field count, storage.py:247-275):
  * d_out[0] = min over malformed data records of (record << 32 | fields held; an empty line holds
  * 0), ~0 when all hold ncols fields; d_out[1] = the first record-ending '\r' that is not the last

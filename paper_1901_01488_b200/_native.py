@@ -188,7 +188,8 @@ _SIGNATURES = {
     "esc_csv_fields": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                  C.c_void_p]),
     "esc_csv_parse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
-                                C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p]),
     "esc_csv_check": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                 C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     "esc_csv_verify_text": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
@@ -302,9 +303,10 @@ class _Workspace:
         # more result blocks for steps queued together before one host wait (slots 1..RESULT_SLOTS)
         self.results = torch.zeros(RESULT_SLOTS * C.sizeof(EscResult), dtype=torch.uint8, pin_memory=True)
         # device-side result block (for NCCL reductions of counts)
-        self.dresult = torch.zeros(C.sizeof(EscResult), dtype=torch.uint8, device=device)
+        # device words initialised by host copies (no fill kernels in the launch list)
+        self.dresult = torch.zeros(C.sizeof(EscResult), dtype=torch.uint8).to(device)
         # device copy of the last selection count (queued compactions check it on the device)
-        self.dcount = torch.zeros(1, dtype=torch.int64, device=device)
+        self.dcount = torch.zeros(1, dtype=torch.int64).to(device)
         # the queued ESC step's cached launch plan (executor._step_plan)
         self.scratch: dict = {}
 

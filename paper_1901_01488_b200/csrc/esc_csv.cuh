@@ -270,6 +270,7 @@ struct CsvParse {
   long long* lengths;      // TEXT: content length (+ quoted flag in bit 62), else unused
   uint8_t* nulls;
   unsigned long long* first_error;  // (row * ncols + col) << 2 | code, atomicMin
+  uint32_t* null_seen;              // set to 1 when any cell is NULL (or nullptr)
 };
 
 __device__ __forceinline__ bool csv_space(uint8_t c) {  // str.strip()'s ASCII whitespace
@@ -374,6 +375,7 @@ __device__ __forceinline__ unsigned long long fnv_step(unsigned long long h, uin
 }
 
 __global__ void csv_parse_kernel(const CsvParse p) {
+  bool seen = false;  // this thread parsed a NULL cell (one store per thread at the end)
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < p.nrows;
        r += (long long)gridDim.x * blockDim.x) {
     const long long f = p.first_field + r * p.ncols + p.col;
@@ -436,7 +438,9 @@ __global__ void csv_parse_kernel(const CsvParse p) {
     }
     p.values[r] = null_cell ? 0 : val;
     p.nulls[r] = null_cell ? 1 : 0;
+    seen = seen || null_cell;
   }
+  if (seen && p.null_seen != nullptr) *p.null_seen = 1u;
 }
 
 // TEXT dictionary check: every cell's content equals its group representative's (no 64-bit hash
@@ -584,7 +588,8 @@ int esc_csv_fields(const uint8_t* d_bytes, int64_t nbytes, int64_t* d_field_end,
 
 int esc_csv_parse(const uint8_t* d_bytes, const int64_t* d_field_end, const uint8_t* d_field_kind, int64_t first_field,
                   int64_t nrows, int32_t ncols, int32_t col, int32_t kind, int32_t scale, int64_t* d_values,
-                  int64_t* d_lengths, uint8_t* d_nulls, uint64_t* d_first_error, void* stream) {
+                  int64_t* d_lengths, uint8_t* d_nulls, uint64_t* d_first_error, uint32_t* d_null_seen,
+                  void* stream) {
   if (nrows < 0 || ncols <= 0 || col < 0 || col >= ncols || kind < ESC_CSV_INT64 || kind > ESC_CSV_TEXT || scale < 0 || scale > 18)
     return fail(ESC_ERR_INVALID, "bad CSV parse arguments");
   if (nrows == 0) return ESC_OK;
@@ -605,6 +610,7 @@ int esc_csv_parse(const uint8_t* d_bytes, const int64_t* d_field_end, const uint
   p.lengths = reinterpret_cast<long long*>(d_lengths);
   p.nulls = d_nulls;
   p.first_error = reinterpret_cast<unsigned long long*>(d_first_error);
+  p.null_seen = d_null_seen;
   const int sms = sm_count_cached();
   if (sms <= 0) return fail(ESC_ERR_CUDA, "no CUDA device");
   int64_t blocks = (nrows + 255) / 256;

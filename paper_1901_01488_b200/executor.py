@@ -255,10 +255,11 @@ def finish_select(sel: Selection, cp: CompiledPredicate):
 
 
 def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int, want_row_ids: bool,
-                                 skip_over_capacity: bool = False):
+                                 skip_over_capacity: bool = False, with_nulls: bool = True):
     """Order-preserving compaction of the selected rows of ``proj_cols`` (and/or their physical
     row ids) into fresh buffers of ``capacity`` rows.  ``skip_over_capacity``: the launch may be
-    queued before the count is known; it does nothing when the count exceeds ``capacity``."""
+    queued before the count is known; it does nothing when the count exceeds ``capacity``.
+    ``with_nulls`` False: no NULL outputs (the caller's selection excludes NULLs)."""
     lib = N.load_library()
     table = sel.table
     stream = _stream(table.device)
@@ -290,7 +291,7 @@ def launch_materialize_selection(sel: Selection, proj_cols: list, capacity: int,
     dev = table.device
     for k, col in enumerate(proj_cols):
         v = torch.empty(capacity, dtype=col.values.dtype, device=dev)
-        m = torch.empty(capacity, dtype=torch.bool, device=dev) if col.nulls is not None else None
+        m = torch.empty(capacity, dtype=torch.bool, device=dev) if col.nulls is not None and with_nulls else None
         values.append(v)
         nulls.append(m)
         outs.slot[k] = slot_of[col.name]
@@ -339,7 +340,7 @@ def launch_compact(cp: CompiledPredicate, table: ColumnTable, ids: torch.Tensor 
     dev = table.device
     for k, col in enumerate(proj_cols):
         v = torch.empty(capacity, dtype=col.values.dtype, device=dev)
-        m = torch.empty(capacity, dtype=torch.bool, device=dev) if col.nulls is not None else None
+        m = torch.empty(capacity, dtype=torch.bool, device=dev) if col.nulls is not None and with_nulls else None
         values.append(v)
         nulls.append(m)
         outs.slot[k] = slots[k]

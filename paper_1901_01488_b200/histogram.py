@@ -62,8 +62,9 @@ def build_histogram(table: ColumnTable, column: str, buckets: int) -> EquiDepthH
     if buckets < 1:
         raise ValueError("bucket count must be >= 1")
     if col.nulls is not None and table.row_count:
-        (vals,) = executor.materialize(table, ex.FoldedAtom(ex.ColumnRef(table.name, column), True), [column])
-        valid = vals.values
+        # the non-NULL values in row order (the selection excludes NULLs: no NULL outputs)
+        sel = executor.select(table, ex.FoldedAtom(ex.ColumnRef(table.name, column), True), capture=[column])
+        valid = executor.launch_materialize_selection(sel, [col], sel.count, False, with_nulls=False)[0][0]
     else:
         valid = col.values
     n = int(valid.numel())

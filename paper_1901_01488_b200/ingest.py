@@ -201,7 +201,8 @@ def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=N
         d_bytes = torch.zeros(1, dtype=torch.uint8, device=dev)
     ws_bytes = int(lib.esc_csv_workspace_bytes(n))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-    totals = torch.zeros(3, dtype=torch.int64, device=dev)
+    # small device words are initialised by a host copy, not a fill kernel
+    totals = torch.tensor([0, 0, 0], dtype=torch.int64, device=dev)
     N.check(lib.esc_csv_count(C.c_void_p(d_bytes.data_ptr()), n, C.c_void_p(totals.data_ptr()),
                               C.c_void_p(ws.data_ptr()), C.c_size_t(ws_bytes), sp), "esc_csv_count")
     nsep, nrec, open_quote = (int(x) for x in totals.cpu().tolist())
@@ -246,7 +247,10 @@ def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=N
     if lone_cr >= 0:
         raise csv.Error("new-line character seen in unquoted field - do you need to open the file with newline=''?")
 
-    first_error = torch.full((1,), -1, dtype=torch.int64, device=dev)  # all ones = none
+    first_error = torch.tensor([-1], dtype=torch.int64, device=dev)  # all ones = none
+    # which columns hold a NULL at all (the parse kernel flags them): one read for every column (a
+    # column without NULLs keeps no mask, as the Column constructor would decide)
+    null_seen = torch.tensor([0] * max(ncols, 1), dtype=torch.int32, device=dev)
     out = []
     for c, (cname, kind) in enumerate(schema):
         code = _CODES["TEXT" if kind.is_text else "DECIMAL" if kind.is_decimal else kind.name]
@@ -257,16 +261,15 @@ def load_csv(text_or_file, name: str, schema, has_header: bool = False, device=N
                                   C.c_void_p(field_kind.data_ptr()) if nsep else None, first_field, nrows, ncols, c,
                                   code, kind.scale if kind.is_decimal else 0, C.c_void_p(vals.data_ptr()),
                                   C.c_void_p(lens.data_ptr()) if lens is not None else None,
-                                  C.c_void_p(nulls.data_ptr()), C.c_void_p(first_error.data_ptr()), sp),
+                                  C.c_void_p(nulls.data_ptr()), C.c_void_p(first_error.data_ptr()),
+                                  C.c_void_p(null_seen.data_ptr() + 4 * c), sp),
                 "esc_csv_parse")
-        out.append((vals[:nrows], nulls[:nrows].to(torch.bool), lens))
+        out.append((vals[:nrows], nulls[:nrows].view(torch.bool), lens))  # bytes are 0 / 1
     err = int(first_error.item()) & ((1 << 64) - 1)
     if err != (1 << 64) - 1:
         _raise_cell_error(data, field_end, field_kind, first_field, ncols, schema, name,
                           2 if has_header else 1, err >> 4, err & 15)
-    # which columns hold a NULL at all: one read for every column (a column without NULLs keeps
-    # no mask, as the Column constructor would decide with one wait per column)
-    has_null = torch.stack([o[1].any() for o in out]).tolist() if out and nrows else [False] * len(out)
+    has_null = [bool(x) for x in null_seen.tolist()[:len(out)]] if out and nrows else [False] * len(out)
     cols = []
     for (cname, kind), (vals, nulls, _), hn in zip(schema, out, has_null):
         mask = nulls if hn else None
@@ -314,7 +317,7 @@ def _encode_text(data, d_bytes, field_end, field_kind, first_field, nrows, ncols
     codes, rep, first, u = sorting.dict_encode(hashes, nulls)
     words = []
     if u:
-        bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        bad = torch.tensor([0], dtype=torch.int32, device=dev)
         N.check(N.load_library().esc_csv_verify_text(C.c_void_p(d_bytes.data_ptr()), C.c_void_p(field_end.data_ptr()),
                                                     C.c_void_p(field_kind.data_ptr()), first_field, nrows, ncols, col,
                                                     C.c_void_p(rep.data_ptr()), C.c_void_p(bad.data_ptr()), sp),

@@ -138,9 +138,11 @@ def dict_encode(hashes: torch.Tensor, nulls: torch.Tensor | None):
     codes = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     rep = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     first = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
-    n_codes = torch.zeros(1, dtype=torch.int64, device=dev)
+    n_codes = torch.tensor([0], dtype=torch.int64, device=dev)  # a host copy, not a fill kernel
     tmp = torch.empty(max(int(lib.esc_dict_temp_bytes(n)), 1), dtype=torch.uint8, device=dev)
-    nl = nulls.to(torch.uint8).contiguous() if nulls is not None else None
+    nl = None
+    if nulls is not None:  # bool bytes are 0 / 1: viewed, not converted
+        nl = (nulls.view(torch.uint8) if nulls.dtype == torch.bool else nulls.to(torch.uint8)).contiguous()
     N.check(lib.esc_dict_encode(C.c_void_p(hashes.contiguous().data_ptr()),
                                 C.c_void_p(nl.data_ptr()) if nl is not None else None, n,
                                 C.c_void_p(codes.data_ptr()), C.c_void_p(rep.data_ptr()), C.c_void_p(first.data_ptr()),

@@ -226,11 +226,11 @@ class Column:
 
             lib = N.load_library()
             n = len(self)
-            bits = torch.zeros(max(int(lib.esc_null_bits_words(n)), 4), dtype=torch.int32, device=self.values.device)
-            if n:
-                N.check(lib.esc_pack_nulls(C.c_void_p(self.nulls.data_ptr()), n, C.c_void_p(bits.data_ptr()),
-                                           C.c_void_p(torch.cuda.current_stream(self.values.device).cuda_stream)),
-                        "esc_pack_nulls")
+            # esc_pack_nulls writes every word, the padding words past the rows included
+            bits = torch.empty(int(lib.esc_null_bits_words(n)), dtype=torch.int32, device=self.values.device)
+            N.check(lib.esc_pack_nulls(C.c_void_p(self.nulls.data_ptr() if n else None), n, C.c_void_p(bits.data_ptr()),
+                                       C.c_void_p(torch.cuda.current_stream(self.values.device).cuda_stream)),
+                    "esc_pack_nulls")
             self._null_bits = bits
         return self._null_bits
 

@@ -125,8 +125,8 @@ def test_join_csv_plan_entry_points_validate_arguments(native_lib):
     err(native_lib.esc_csv_count(None, 10, tot, None, 0, None), "bad CSV arguments")
     ws = (C.c_uint8 * 16)()
     err(native_lib.esc_csv_count(b"a,b\n", 4, tot, ws, 16, None), "workspace too small")
-    err(native_lib.esc_csv_parse(None, None, None, 0, 5, 2, 3, 0, 0, None, None, None, None, None), "bad CSV parse")
-    err(native_lib.esc_csv_parse(None, None, None, 0, 5, 2, 1, 1, 19, None, None, None, None, None), "bad CSV parse")
+    err(native_lib.esc_csv_parse(None, None, None, 0, 5, 2, 3, 0, 0, None, None, None, None, None, None), "bad CSV parse")
+    err(native_lib.esc_csv_parse(None, None, None, 0, 5, 2, 1, 1, 19, None, None, None, None, None, None), "bad CSV parse")
     err(native_lib.esc_copy_regions(N.MAX_REGIONS + 1 if hasattr(N, "MAX_REGIONS") else 73, None, None, None, None),
         "region count")
     err(native_lib.esc_step_plan_launch(None, 3, None), "null plan")

@@ -51,3 +51,25 @@ pr.disable()
 st = pstats.Stats(pr)
 st.sort_stats("tottime").print_stats(30)
 st.sort_stats("cumulative").print_stats(25)
+
+# sections of the step without the profiler (medians over 100 steps, us)
+from paper_1901_01488_b200 import executor
+
+secs = {"launch": [], "wait": [], "finish": [], "register": [], "sweep": []}
+prepared = ("t", t, pred, list(w.project), n, True, (1 * n) // 5)
+for i in range(120):
+    a = time.perf_counter()
+    ps = executor.launch_step(t, pred, list(w.project), (1 * n) // 5, materialize=True, slot=1)
+    b = time.perf_counter()
+    executor._stream(dev).synchronize()
+    c = time.perf_counter()
+    count, cols = executor.finish_step(ps)
+    d = time.perf_counter()
+    cat.materialize_temp(cols)
+    e = time.perf_counter()
+    cat.temps.sweep()
+    f = time.perf_counter()
+    if i >= 20:
+        for k, v in zip(secs, (b - a, c - b, d - c, e - d, f - e)):
+            secs[k].append(v * 1e6)
+print("sections (us):", {k: round(statistics.median(v), 1) for k, v in secs.items()})
