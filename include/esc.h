@@ -115,7 +115,8 @@ enum {
   ESC_UDF_JMP = 19,     /* skip `arg` ops */
   /* math.floor / math.ceil / int(): integral result (ValueError on NaN, OverflowError on inf) */
   ESC_UDF_FLOOR = 20, ESC_UDF_CEIL = 21, ESC_UDF_TRUNC = 22,
-  ESC_UDF_SQRT = 23     /* math.sqrt (ValueError "math domain error" below zero) */
+  ESC_UDF_SQRT = 23,    /* math.sqrt (ValueError "math domain error" below zero) */
+  ESC_UDF_RINT = 24     /* round(x): nearest integer, ties to even (errors as ESC_UDF_FLOOR) */
 };
 
 /* UDF failure codes (low 3 bits of esc_result_t.udf_fail[]) */

@@ -30,7 +30,7 @@ CMP_EQ, CMP_NE, CMP_LT, CMP_LE, CMP_GT, CMP_GE = range(6)
 DOM_I64, DOM_F32, DOM_F64 = 0, 1, 2
 (UDF_ARG, UDF_CONST, UDF_ADD, UDF_SUB, UDF_MUL, UDF_DIV, UDF_MOD, UDF_FLOORDIV, UDF_NEG, UDF_ABS,
  UDF_SQUARE, UDF_LT, UDF_LE, UDF_GT, UDF_GE, UDF_EQ, UDF_NE, UDF_JMPF, UDF_JMP, UDF_FLOOR, UDF_CEIL, UDF_TRUNC,
- UDF_SQRT) = range(1, 24)
+ UDF_SQRT, UDF_RINT) = range(1, 25)
 FAIL_DIV, FAIL_MOD, FAIL_FLOORDIV, FAIL_POW, FAIL_NAN_INT, FAIL_INF_INT, FAIL_DOMAIN = 1, 2, 3, 4, 5, 6, 7
 COL_STAGE = 1
 

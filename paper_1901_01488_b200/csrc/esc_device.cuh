@@ -445,11 +445,12 @@ __device__ __noinline__ double udf_eval(const KParams& p, const esc_udf_t& u, co
         if (stk[--sp] == 0.0) i += o.arg;
         break;
       case ESC_UDF_JMP: i += o.arg; break;
-      case ESC_UDF_FLOOR: case ESC_UDF_CEIL: case ESC_UDF_TRUNC: {
+      case ESC_UDF_FLOOR: case ESC_UDF_CEIL: case ESC_UDF_TRUNC: case ESC_UDF_RINT: {
         const double x = stk[sp - 1];
         if (isnan(x)) { *fail = ESC_FAIL_NAN_INT; return 0.0; }
         if (isinf(x)) { *fail = ESC_FAIL_INF_INT; return 0.0; }
-        stk[sp - 1] = o.op == ESC_UDF_FLOOR ? floor(x) : o.op == ESC_UDF_CEIL ? ceil(x) : trunc(x);
+        stk[sp - 1] = o.op == ESC_UDF_FLOOR ? floor(x) : o.op == ESC_UDF_CEIL ? ceil(x)
+                    : o.op == ESC_UDF_TRUNC ? trunc(x) : rint(x);  // rint: ties to even, as round()
         break;
       }
       case ESC_UDF_SQRT: {

@@ -211,7 +211,7 @@ int validate_program(const esc_program_t* prog, int32_t ncols) {
         } else if (o.op == ESC_UDF_CONST) {
           ++sp;
         } else if (o.op == ESC_UDF_NEG || o.op == ESC_UDF_ABS || o.op == ESC_UDF_SQUARE ||
-                   (o.op >= ESC_UDF_FLOOR && o.op <= ESC_UDF_SQRT)) {
+                   (o.op >= ESC_UDF_FLOOR && o.op <= ESC_UDF_RINT)) {
           if (sp < 1) return fail(ESC_ERR_INVALID, "UDF stack underflow");
         } else if ((o.op >= ESC_UDF_ADD && o.op <= ESC_UDF_FLOORDIV) || (o.op >= ESC_UDF_LT && o.op <= ESC_UDF_NE)) {
           if (sp < 2) return fail(ESC_ERR_INVALID, "UDF stack underflow");

@@ -50,8 +50,8 @@ _BINARY = {"add": N.UDF_ADD, "sub": N.UDF_SUB, "mul": N.UDF_MUL, "truediv": N.UD
 _CMP = {"lt": N.UDF_LT, "le": N.UDF_LE, "gt": N.UDF_GT, "ge": N.UDF_GE, "eq": N.UDF_EQ, "ne": N.UDF_NE}
 _SWAPPED = {"lt": "gt", "le": "ge", "gt": "lt", "ge": "le", "eq": "eq", "ne": "ne"}
 _UNARY = {"neg": N.UDF_NEG, "abs": N.UDF_ABS, "square": N.UDF_SQUARE, "floor": N.UDF_FLOOR,
-          "ceil": N.UDF_CEIL, "trunc": N.UDF_TRUNC, "sqrt": N.UDF_SQRT}
-_MAY_FAIL_UNARY = {"square", "floor", "ceil", "trunc", "sqrt"}
+          "ceil": N.UDF_CEIL, "trunc": N.UDF_TRUNC, "sqrt": N.UDF_SQRT, "rint": N.UDF_RINT}
+_MAY_FAIL_UNARY = {"square", "floor", "ceil", "trunc", "sqrt", "rint"}
 _MAY_FAIL_DIVISOR = {N.UDF_DIV, N.UDF_MOD, N.UDF_FLOORDIV}
 _EXACT = 2 ** 53
 MAX_PATHS = 64
@@ -232,11 +232,16 @@ class Sym:
     def __ceil__(self): return self._integral("ceil")
     def __trunc__(self): return self._integral("trunc")
 
-    def __float__(self):
-        raise UnsupportedUdf("float()/int()/round() of a UDF argument cannot be traced (math.floor/ceil/trunc, "
-                             "math.sqrt/fabs and arithmetic can)")
+    def __round__(self, ndigits=None):
+        if ndigits is not None:
+            raise UnsupportedUdf("round(x, ndigits) of a UDF argument cannot be traced (round(x) can)")
+        return self._integral("rint")
 
-    __int__ = __index__ = __round__ = __float__
+    def __float__(self):
+        raise UnsupportedUdf("float()/int() of a UDF argument can only be traced when the UDF calls them by "
+                             "name (math.floor/ceil/trunc, math.sqrt/fabs, round() and arithmetic trace too)")
+
+    __int__ = __index__ = __float__
 
 
 # ---- the tracing math module --------------------------------------------------------------------
@@ -274,6 +279,28 @@ _MATH_OVERRIDES = {"sqrt": _sym_sqrt, "fabs": _sym_fabs, "isnan": _sym_isnan, "i
                    "isfinite": _sym_isfinite}
 
 
+# builtins a UDF calls by name: float() of a traced value is the value itself (arguments are
+# float64 already; floor/ceil/trunc/round results are integral doubles, exactly representable),
+# int() truncates toward zero like math.trunc; anything else goes to the real builtin
+def _sym_float(x=0.0):
+    if isinstance(x, Sym):
+        return Sym(x.node)
+    if isinstance(x, SymBool):
+        return float(x._num())
+    return float(x)
+
+
+def _sym_int(x=0, *base):
+    if isinstance(x, Sym) and not base:
+        return x._integral("trunc")
+    if isinstance(x, SymBool) and not base:
+        return x._num()
+    return int(x, *base)
+
+
+_BUILTIN_OVERRIDES = {"float": _sym_float, "int": _sym_int}
+
+
 class _TracingMath(types.ModuleType):
     """``math`` with tracing sqrt / fabs / isnan / isinf / isfinite (floor / ceil / trunc trace
     through the dunder methods already); every other attribute is the real one."""
@@ -304,6 +331,8 @@ def _traceable(fn):
             patch[name] = _TMATH
         elif v in _REAL_TO_SYM if _hashable(v) else False:
             patch[name] = _REAL_TO_SYM[v]
+        elif v is None and name in _BUILTIN_OVERRIDES:  # the builtin itself, not a global of that name
+            patch[name] = _BUILTIN_OVERRIDES[name]
     if not patch:
         return fn
     ng = dict(g)
@@ -357,6 +386,8 @@ class UdfProgram:
                 stack[-1] = float(math.trunc(stack[-1]))
             elif op == N.UDF_SQRT:
                 stack[-1] = math.sqrt(stack[-1])
+            elif op == N.UDF_RINT:
+                stack[-1] = float(round(stack[-1]))
             elif op == N.UDF_JMPF:
                 if stack.pop() == 0.0:
                     i += a

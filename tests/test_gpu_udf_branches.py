@@ -1,5 +1,6 @@
 """UDFs with branches and math on the device vs the oracle (the reference's per-row Python call):
-conditional expressions, if/else, min/max, and/or, math.floor/ceil/trunc/sqrt/fabs/isnan, in the
+conditional expressions, if/else, min/max, and/or, math.floor/ceil/trunc/sqrt/fabs/isnan,
+float()/int()/round(), in the
 interpreter and the JIT tier, over the mixed-kind table (NULLs, DECIMAL, DATE, float32), with the
 reference's error semantics (a failing op on a branch Python does not take never fails)."""
 
@@ -42,6 +43,11 @@ BRANCHY = {
     "isn": lambda x: 0.0 if math.isnan(x) else math.fabs(x),
     "pw": _piecewise,
     "cmpres": lambda x, y: x > y,                          # a bool result: 1.0 / 0.0
+    # builtins called by name: float() is the value, int() truncates, round() ties to even
+    "flt": lambda x: float(x) / 3.0 + 1.0,
+    "it": lambda x: int(x / 7.0) % 4,
+    "rnd": lambda x: round(x / 4.0) * 2.0,
+    "rndf": lambda x, y: round(x / y),                     # ZeroDivisionError, NaN / inf errors
 }
 ALL = {**UDFS, **BRANCHY}
 
@@ -71,7 +77,8 @@ def _cases():
     for name, args in (("relu", [b]), ("clip", [b]), ("mn", [a, b]), ("mx3", [a, b]), ("safe", [a, b]),
                        ("unsafe", [a, b]), ("fl", [b]), ("cl", [a]), ("tr", [val]), ("sq", [b]),
                        ("sqfail", [a]), ("band", [b, f]), ("isn", [f]), ("pw", [b, a]), ("cmpres", [a, b]),
-                       ("fl", [f]), ("cl", [when])):
+                       ("fl", [f]), ("cl", [when]), ("flt", [a]), ("it", [b]), ("rnd", [val]), ("rndf", [a, b]),
+                       ("rnd", [f]), ("it", [f])):
         for op, k in ((">", 0.0), ("<=", 2.0), ("=", 1.0)):
             out.append(["fn", name, args, op, k])
     # short circuits around failing branchy UDFs (reference whole-slice semantics)

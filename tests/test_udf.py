@@ -51,7 +51,7 @@ def test_may_fail_flags():
     (lambda x: math.exp(x), "float()"),
     (lambda x: x ** 3, "\\*\\* 3"),
     (lambda x: "s", "returns str"),
-    (lambda x: round(x), "float()"),
+    (lambda x: round(x, 2), "ndigits"),
 ])
 def test_untraceable_udfs_are_refused(fn, msg):
     with pytest.raises(UnsupportedUdf, match=msg):
@@ -106,8 +106,44 @@ def test_branchy_trace_equals_python(fn, n):
             assert want == got, args
 
 
-@pytest.mark.parametrize("fn", [lambda x: math.floor(x) + math.floor(x), lambda x: float(x), lambda x: math.exp(x),
-                                lambda x: math.floor(x) * 2, lambda x: x ** 3, lambda x: round(x)])
+@pytest.mark.parametrize("fn", [lambda x: math.floor(x) + math.floor(x), lambda x: x.__float__(), lambda x: math.exp(x),
+                                lambda x: math.floor(x) * 2, lambda x: x ** 3, lambda x: round(x, 1),
+                                lambda x: int(x) * 2])
 def test_untraceable_branchy_refused(fn):
     with pytest.raises(UnsupportedUdf):
         trace(fn, 1)
+
+
+def _builtin_calls():
+    return {
+        "float": (lambda a, b: float(a) / 3 + b),
+        "int": (lambda a, b: int(a / 7) + b),
+        "round": (lambda a, b: round(a / 4) - b),
+        "round_cmp": (lambda a, b: 1.0 if round(a * 0.5) == round(b * 0.5) else 0.0),
+        "int_mod": (lambda a, b: int(a) % 3 if a > 0 else int(b) // 2),
+        "round_fails": (lambda a, b: round(a / b)),
+    }
+
+
+@pytest.mark.parametrize("name", sorted(_builtin_calls()))
+def test_builtin_float_int_round_trace(name):
+    """float() / int() / round() called by name trace (identity, truncation, ties-to-even) and the
+    program equals the Python call, errors included (NaN / inf / division by zero)."""
+    fn = _builtin_calls()[name]
+    prog = trace(fn, 2, name)
+    g = random.Random(9)
+    for _ in range(3000):
+        a = g.choice([g.uniform(-50, 50), g.randint(-20, 20) + 0.5, float(g.randint(-9, 9)), 0.0, math.inf, math.nan])
+        b = g.choice([g.uniform(-50, 50), float(g.randint(-20, 20)), 0.0, -2.5])
+        try:
+            want = ("ok", fn(a, b))
+        except (ArithmeticError, ValueError) as exc:
+            want = ("err", str(exc))
+        try:
+            got = ("ok", prog.evaluate([a, b]))
+        except (ArithmeticError, ValueError) as exc:
+            got = ("err", str(exc))
+        if want[0] == got[0] == "ok" and isinstance(want[1], float) and math.isnan(want[1]):
+            assert math.isnan(got[1]), (a, b)
+        else:
+            assert want == got, (a, b)
