@@ -754,9 +754,11 @@ def _star_cpu_baseline(eng, plan_, res, sample_rows: int = 6_000_000):
                       f"executor.probe_joins, numpy); sample COUNT {stage[-1]}"}
 
 
-def _port_count_threads(cols: dict, pred) -> int:
-    """The reference port's count_star over every row, 2.5M-row chunks on the host threads
-    (numpy releases the GIL in the comparisons): the full-size parity pin of a sweep point."""
+def _port_digest_threads(cols: dict, pred, names: list) -> tuple:
+    """The reference port's selection over every row (2.5M-row chunks on the host threads): its
+    count and, per column of ``names``, an order-sensitive digest of the selected values in row
+    order — (sum v, sum position * v), both mod 2**64 — the full-size pin of a sweep point's
+    compacted columns."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import esc_oracle as O
@@ -766,10 +768,31 @@ def _port_count_threads(cols: dict, pred) -> int:
     def one(lo):
         hi = min(lo + PARITY_CHUNK, n)
         t = O.OTable("t", {k: O.OColumn(v[lo:hi], np.zeros(hi - lo, bool)) for k, v in cols.items()})
-        return O.count_star(t, pred, {})
+        idx = O.eval_predicate(t, pred, None, {})
+        j = np.arange(idx.size, dtype=np.uint64)
+        parts = []
+        for c in names:
+            v = cols[c][lo:hi][idx].astype(np.int64).view(np.uint64)
+            parts.append((int(v.sum(dtype=np.uint64)), int((j * v).sum(dtype=np.uint64))))
+        return idx.size, parts
 
     with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
-        return sum(ex.map(one, range(0, n, PARITY_CHUNK)))
+        res = list(ex.map(one, range(0, n, PARITY_CHUNK)))
+    mask = (1 << 64) - 1
+    total, dig = 0, [[0, 0] for _ in names]
+    for k, parts in res:  # positions continue across chunks in row order
+        for d, (s0, s1) in zip(dig, parts):
+            d[0] = (d[0] + s0) & mask
+            d[1] = (d[1] + total * s0 + s1) & mask
+        total += k
+    return total, [tuple(d) for d in dig]
+
+
+def _values_digest(v: np.ndarray) -> tuple:
+    """(sum v, sum position * v) mod 2**64 of a compacted column, in its order."""
+    u = v.astype(np.int64).view(np.uint64)
+    j = np.arange(u.size, dtype=np.uint64)
+    return int(u.sum(dtype=np.uint64)), int((j * u).sum(dtype=np.uint64))
 
 
 def run_sweep(args, dev, peak):
@@ -812,9 +835,16 @@ def run_sweep(args, dev, peak):
             pw = [t.column(c).values.element_size() for c in wl.project]
             lines = sum(n * w * (1.0 - (1.0 - se) ** (128 // w)) for w in pw)
             floor = bc + n / 4 + lines + k * sum(pw)
-            ref_k = _port_count_threads(host, wl.pred)
+            # full-size pin: the count AND the compacted (c0, c1) columns (c1 is gathered for the
+            # single-range predicate) against the reference port over all rows, outside the timing
+            names = [c for c in ("c0", "c1") if c in wl.project]
+            ref_k, ref_dig = _port_digest_threads(host, wl.pred, names)
+            got = executor.materialize(t, p, names, count=k)
+            dev_dig = [_values_digest(c.values.cpu().numpy()) for c in got]
+            del got
             res.append({"pred": "conj4" if conj4 else "single", "s": s, "count": k, "count_ms": cms,
-                        "count_reference_port": ref_k, "bit_exact": ref_k == k,
+                        "count_reference_port": ref_k, "rows_digest_equal": dev_dig == ref_dig,
+                        "bit_exact": ref_k == k and dev_dig == ref_dig,
                         "count_GBps": bc / cms / 1e6, "count_frac": bc / cms / 1e6 / peak,
                         "compact_ms": mms, "compact_GBps": bm / mms / 1e6, "compact_frac": bm / mms / 1e6 / peak,
                         "line_floor_ms": floor / peak / 1e6, "line_floor_frac": floor / peak / 1e6 / mms})
