@@ -1837,43 +1837,55 @@ __global__ void __launch_bounds__(kSelWarps * 32, kList ? 3 : 4) sel_compact_ker
         if (lane >= d) incl += t;
       }
       const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      for (uint32_t e0 = (uint32_t)r * 32; e0 < total; e0 += 32u * R) {
-        const uint32_t e = e0 + lane;
-        // owning lane: the first whose inclusive count exceeds e (binary search over the lanes)
-        int sl = 0;
+      // two entries per lane per pass (e, e + 32R): both entries' loads are in flight before
+      // their stores, so a group of up to 64 captured hits costs one round trip
+      for (uint32_t e0 = (uint32_t)r * 32; e0 < total; e0 += 64u * R) {
+        bool ok[2];
+        unsigned long long pos[2];
+        size_t slot[2];
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, sl + step - 1);
-          if (v <= e) sl += step;
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t e = e0 + (uint32_t)h * 32u * R + lane;
+          // owning lane: the first whose inclusive count exceeds e (binary search over the lanes)
+          int sl = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t v = __shfl_sync(0xFFFFFFFFu, incl, sl + step - 1);
+            if (v <= e) sl += step;
+          }
+          const uint32_t s_incl = __shfl_sync(0xFFFFFFFFu, incl, sl);
+          const uint32_t s_cnt = __shfl_sync(0xFFFFFFFFu, ccnt, sl);
+          const unsigned long long s_off = __shfl_sync(0xFFFFFFFFu, myoff, sl);
+          const uint32_t idx = e - (s_incl - s_cnt);
+          pos[h] = s_off + idx;
+          ok[h] = e < total && (long long)pos[h] < cap;
+          slot[h] = (size_t)idx * p.cap_stride + (size_t)(seg0 + sl);
         }
-        const uint32_t s_incl = __shfl_sync(0xFFFFFFFFu, incl, sl);
-        const uint32_t s_cnt = __shfl_sync(0xFFFFFFFFu, ccnt, sl);
-        const unsigned long long s_off = __shfl_sync(0xFFFFFFFFu, myoff, sl);
-        if (e >= total) continue;
-        const uint32_t idx = e - (s_incl - s_cnt);
-        const unsigned long long pos = s_off + idx;
-        if ((long long)pos >= cap) continue;
-        const size_t slot = (size_t)idx * p.cap_stride + (size_t)(seg0 + sl);
+        if (!ok[0] && !ok[1]) continue;
         for (int k0 = 0; k0 < p.n_proj; k0 += 4) {
-          unsigned long long v[4];
-          uint8_t nb[4];
+          unsigned long long v[2][4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int k = k0 + j;
             const int ci = k < p.n_proj ? p.cap_index[k] : -1;
-            v[j] = 0;
-            nb[j] = 0;
-            if (ci >= 0) {
-              v[j] = ld_w(p.cols[k].width, static_cast<const uint8_t*>(p.cap_values[ci]) + slot * p.cols[k].width, 0);
-              if (p.outs.out_nulls[k] != nullptr && p.cap_nulls[ci] != nullptr) nb[j] = p.cap_nulls[ci][slot];
-            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              v[h][j] = (ci >= 0 && ok[h])
+                            ? ld_w(p.cols[k].width, static_cast<const uint8_t*>(p.cap_values[ci]) + slot[h] * p.cols[k].width, 0)
+                            : 0ull;
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int k = k0 + j;
             if (k < p.n_proj && p.cap_index[k] >= 0) {
-              st_bits(p.cols[k].width, p.outs.out_values[k], pos, v[j]);
-              if (p.outs.out_nulls[k] != nullptr) p.outs.out_nulls[k][pos] = nb[j];
+              const int ci = p.cap_index[k];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (!ok[h]) continue;
+                st_bits(p.cols[k].width, p.outs.out_values[k], pos[h], v[h][j]);
+                if (p.outs.out_nulls[k] != nullptr)
+                  p.outs.out_nulls[k][pos[h]] = p.cap_nulls[ci] != nullptr ? p.cap_nulls[ci][slot[h]] : (uint8_t)0;
+              }
             }
           }
         }
