@@ -49,7 +49,8 @@ typedef unsigned long size_t;
 extern "C" {
 #endif
 
-#define ESC_ABI_VERSION 1
+/* 2: esc_csv_parse takes d_null_seen; esc_set_hit_lists; the ESC_UDF_RINT opcode */
+#define ESC_ABI_VERSION 2
 
 #define ESC_MAX_COLS 32     /* column slots one program may reference            */
 #define ESC_MAX_INSTRS 96   /* boolean program length                              */

@@ -18,7 +18,7 @@ from .errors import ExecutionError, NativeUnavailable
 LIB_NAME = "_esc_native.so"
 LIB_PATH = os.environ.get("ESC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_COLS, MAX_INSTRS, MAX_UDFS, MAX_UDF_OPS, MAX_UDF_ARGS, MAX_STACK, MAX_PROJ = 32, 96, 8, 128, 8, 16, 32
 
 # dtypes

@@ -36,7 +36,9 @@ def test_struct_layouts_match(native_lib):
 
 
 def test_version_and_device_queries(native_lib):
-    assert native_lib.esc_abi_version() == 1
+    from paper_1901_01488_b200 import _native as N
+
+    assert native_lib.esc_abi_version() == N.ABI_VERSION == 2
     assert native_lib.esc_device_sm_count() >= 0  # 0 without a GPU
 
 
@@ -60,7 +62,7 @@ def test_invalid_arguments_are_reported(native_lib):
     prog.abi_version = 7
     rc = native_lib.esc_scan_count(C.byref(prog), None, 0, 10, None, C.byref(res), ws, 4096, None)
     assert rc == 1 and b"ABI version" in native_lib.esc_last_error()
-    prog.abi_version = 1
+    prog.abi_version = N.ABI_VERSION
     prog.n_instrs = 1
     prog.instrs[0].op = N.OP_PUSH
     rc = native_lib.esc_scan_count(C.byref(prog), None, 0, 10, None, C.byref(res), ws, 4096, None)
