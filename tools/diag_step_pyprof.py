@@ -73,3 +73,33 @@ for i in range(120):
         for k, v in zip(secs, (b - a, c - b, d - c, e - d, f - e)):
             secs[k].append(v * 1e6)
 print("sections (us):", {k: round(statistics.median(v), 1) for k, v in secs.items()})
+
+# the host functions of one step, each timed by a wrapper (medians over 100 steps, us)
+import functools
+
+from paper_1901_01488_b200 import _native as N, compiler
+from paper_1901_01488_b200 import storage
+
+parts = {}
+
+
+def timed(mod, name):
+    f = getattr(mod, name)
+
+    @functools.wraps(f)
+    def g(*a, **k):
+        t0 = time.perf_counter()
+        r = f(*a, **k)
+        parts.setdefault(f"{getattr(mod, '__name__', type(mod).__name__).rsplit('.', 1)[-1]}.{name}", []).append((time.perf_counter() - t0) * 1e6)
+        return r
+
+    setattr(mod, name, g)
+
+
+for mod, name in ((executor, "compile_predicate"), (N, "workspace"), (executor, "_step_plan"),
+                  (executor, "_take_outputs"), (executor, "raise_udf_errors"), (executor, "_plan_lend")):
+    timed(mod, name)
+timed(cat, "materialize_temp")
+for i in range(120):
+    step()
+print("functions (us):", {k: round(statistics.median(v[20:]), 2) for k, v in parts.items()})
