@@ -1644,12 +1644,15 @@ __device__ __forceinline__ void gather_rows(const SelParams& p, const bool (&hit
 //     dense segments (> one hit per 32 rows) - the whole warp, one row per lane of each word;
 //  B. sparse segments, one LANE per 128-row chunk (4 bitmap words): a 16-byte bitmap load, a
 //     width-CPS segmented scan for the chunk's output base, then the chunk's hits four at a time
-//     (every column's loads in flight before the stores).  Spreading chunks, not segments, over
+//     (each column's 4 loads in flight before its stores).  Spreading chunks, not segments, over
 //     the warps keeps small selections from running on a handful of SMs.  When the segment
 //     groups alone fill the GPU (sparse_in_a), phase A writes its own sparse segments the same
 //     way, chunk by chunk, and phase B is skipped: no second pass over the segment counts.
+// sel_compact_kernel<true> (sparse selections, sparse_in_a): phase A's sparse segments go
+// through per-warp hit lists instead (candidate-segment rounds, the hits listed in shared
+// memory and gathered 32+ at a time by the whole warp, every column's loads in flight).
 // The hits of one 128-row chunk (4 bitmap words `w4` of segment `seg`, chunk `sub`), written
-// from output position `pos` on, four at a time (phase B: small selections).
+// from output position `pos` on, four at a time.
 __device__ __forceinline__ void sparse_chunk(const SelParams& p, int64_t seg, int sub, uint4 w4,
                                              unsigned long long pos, bool scap) {
   const int W = p.seg_rows / 32;
