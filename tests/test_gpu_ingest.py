@@ -65,3 +65,33 @@ def test_engine_load_csv_file_and_roundtrip(cuda, tmp_path):
     assert dump_csv(t2) == out
     assert count_star(t, ex.Comparison(ex.ColumnRef("t", "i"), ">", 0)) == int(
         ((t.columns[0].to_numpy()[0] > 0) & ~t.columns[0].to_numpy()[1]).sum())
+
+
+def test_null_masks_only_where_nulls_occur(cuda):
+    """The parse kernel flags the columns that hold a NULL (d_null_seen): those get a bool mask
+    with exactly the NULL rows, the others none — for INT64, DECIMAL and TEXT columns, with the
+    NULLs early, late and absent."""
+    from paper_1901_01488_b200.ingest import NULL_TOKEN, load_csv
+    from paper_1901_01488_b200.storage import parse_kind
+
+    n = 20_011
+    g = np.random.default_rng(5)
+    null_i = g.random(n) < 0.01
+    null_i[-1] = True                       # a NULL in the very last row
+    null_t = np.zeros(n, bool)
+    null_t[0] = True                        # a single NULL in the first row
+    lines = []
+    for r in range(n):
+        i = NULL_TOKEN if null_i[r] else str(r * 7 - 5)
+        t = NULL_TOKEN if null_t[r] else f"w{r % 13}"
+        lines.append(f"{i},{r % 97},{t},{r}.25\n")
+    schema = [("i", parse_kind("int64")), ("k", parse_kind("int64")), ("t", parse_kind("text")),
+              ("d", parse_kind("decimal(15,2)"))]
+    tab = load_csv("".join(lines), "n", schema, device=cuda)
+    ci, ck, ct, cd = tab.columns
+    assert ci.nulls is not None and np.array_equal(ci.nulls.cpu().numpy(), null_i)
+    assert ct.nulls is not None and np.array_equal(ct.nulls.cpu().numpy(), null_t)
+    assert ck.nulls is None and cd.nulls is None
+    vi = ci.values.cpu().numpy()
+    assert np.array_equal(vi[~null_i], (np.arange(n) * 7 - 5)[~null_i])
+    assert np.array_equal(ck.values.cpu().numpy(), np.arange(n) % 97)
